@@ -1,0 +1,325 @@
+/*
+ * grape_oracle.c — the CPU ORACLE for the GRAPE walk hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load or execute this
+ * code.  The product path (paper_2110_06196_b200/) never links, imports or
+ * calls it, and this file includes no header of the product path.
+ *
+ * Plain, slow, obviously-correct, single-threaded C.  Every function follows
+ * the rule it cites, step by step, in the order SURVEY.md §8(c) writes it:
+ *
+ *   P:NNN  = /root/reference/PAPER.md line NNN (section / equation named)
+ *   S:NNN  = /root/reference/SPEC.md line NNN
+ *   §8(c)  = /root/repo/SURVEY.md §8(c), the readings this build adopts
+ *            (restated, each with its justification).
+ *
+ * What the paper fixes (and what the tests pin this file against):
+ *   - the node2vec transition law  pi_vx = alpha_pq(t,x) * w_vx   (§4.3.1 Eq.1)
+ *     with alpha = 1/p if x == t, 1 if x in N(t), 1/q otherwise   (Eq.2-3 reformulated)
+ *   - the weighted first-order law P(x|v) = w_vx / sum_y w_vy       (§4.3.2 steps 1-4)
+ *   - the unweighted first-order law: uniform over N(v)
+ * What the paper leaves open and §8(c) fixes (parity conventions; pinned
+ * against the CUDA toolkit's independent Philox and by exact arithmetic):
+ *   - Philox4x32-10 counter = (wid lo, wid hi, step, attempt), key = seed  (§8(c) c7)
+ *   - bounded integer = (x64 * W) >> 64                                    (§8(c) c8)
+ *   - integer acceptance thresholds from 1/p, 1, 1/q                       (§8(c) c9)
+ *   - dead ends pad with 0xFFFFFFFF; bad start ids give all-PAD rows       (§8(c) c3, c14)
+ *   - the first node2vec step is a first-order step (attempt 0)            (§8(c) c2)
+ *
+ * Parity status: every function here is pinned by a -m "not gpu" test in
+ * tests/test_oracle_*.py (see DESIGN.md §4 for the pin of each one).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stddef.h>
+
+#define ORACLE_PAD 0xFFFFFFFFu
+#define ORACLE_NONE 0xFFFFFFFFu
+
+/* ---------------------------------------------------------------------------
+ * Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11), the counter-based RNG
+ * §8(c) c7 adopts in place of the paper's unspecified assembly PRNG.
+ * Constants of the construction: multipliers M0, M1 and Weyl key bumps W0, W1.
+ * One round:  (hi0,lo0) = M0*c0, (hi1,lo1) = M1*c2   (32x32 -> 64)
+ *             c' = (hi1 ^ c1 ^ k0, lo1, hi0 ^ c3 ^ k1, lo0)
+ * Ten rounds, the key bumped by (W0, W1) between consecutive rounds.
+ * ------------------------------------------------------------------------- */
+static const uint32_t PHILOX_M0 = 0xD2511F53u;
+static const uint32_t PHILOX_M1 = 0xCD9E8D57u;
+static const uint32_t PHILOX_W0 = 0x9E3779B9u;
+static const uint32_t PHILOX_W1 = 0xBB67AE85u;
+
+void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4])
+{
+    uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+    uint32_t k0 = key[0], k1 = key[1];
+    int round;
+    for (round = 0; round < 10; round++) {
+        uint64_t prod0, prod1;
+        uint32_t hi0, lo0, hi1, lo1;
+        if (round > 0) {
+            k0 = k0 + PHILOX_W0;
+            k1 = k1 + PHILOX_W1;
+        }
+        prod0 = (uint64_t)PHILOX_M0 * (uint64_t)c0;
+        prod1 = (uint64_t)PHILOX_M1 * (uint64_t)c2;
+        hi0 = (uint32_t)(prod0 >> 32);
+        lo0 = (uint32_t)prod0;
+        hi1 = (uint32_t)(prod1 >> 32);
+        lo1 = (uint32_t)prod1;
+        c0 = hi1 ^ c1 ^ k0;
+        c1 = lo1;
+        c2 = hi0 ^ c3 ^ k1;
+        c3 = lo0;
+    }
+    out[0] = c0;
+    out[1] = c1;
+    out[2] = c2;
+    out[3] = c3;
+}
+
+/* DRAW(seed, wid, s, a)  (§8(c) c7): the four output words of one attempt. */
+void oracle_draw(uint64_t seed, uint64_t wid, uint32_t s, uint32_t a, uint32_t out[4])
+{
+    uint32_t ctr[4];
+    uint32_t key[2];
+    ctr[0] = (uint32_t)(wid & 0xFFFFFFFFu);
+    ctr[1] = (uint32_t)(wid >> 32);
+    ctr[2] = s;
+    ctr[3] = a;
+    key[0] = (uint32_t)(seed & 0xFFFFFFFFu);
+    key[1] = (uint32_t)(seed >> 32);
+    oracle_philox4x32_10(ctr, key, out);
+}
+
+/* BOUNDED(x64, W) = floor(x64 * W / 2^64), a uniform-ish integer in [0, W)
+ * (§8(c) c8).  W >= 1. */
+uint64_t oracle_bounded(uint64_t x64, uint64_t W)
+{
+    unsigned __int128 prod = (unsigned __int128)x64 * (unsigned __int128)W;
+    return (uint64_t)(prod >> 64);
+}
+
+/* THRESHOLDS(p, q) (§8(c) c9): the acceptance thresholds of the three
+ * node2vec classes, proportional to alpha = 1/p, 1, 1/q (Eq.1),
+ * scaled so that the largest class is accepted with certainty:
+ *     mn = min(p, 1, q);  T_c = floor(2^32 * mn / c)  for c in (p, 1, q).
+ * Returns 0 on success, 1 if p or q is not finite and > 0, or if
+ * max(p,1,q)/min(p,1,q) > 2^24 (§8(c) c10: keeps every T_c >= 2^8). */
+int oracle_thresholds(double p, double q, uint64_t T[3])
+{
+    double mn, mx;
+    if (!(p > 0.0) || !(q > 0.0) || isinf(p) || isinf(q) || isnan(p) || isnan(q))
+        return 1;
+    mn = 1.0;
+    if (p < mn) mn = p;
+    if (q < mn) mn = q;
+    mx = 1.0;
+    if (p > mx) mx = p;
+    if (q > mx) mx = q;
+    if (mx / mn > 16777216.0)
+        return 1;
+    T[0] = (uint64_t)floor(ldexp(mn / p, 32));
+    T[1] = (uint64_t)floor(ldexp(mn, 32));
+    T[2] = (uint64_t)floor(ldexp(mn / q, 32));
+    return 0;
+}
+
+/* Per-row inclusive prefix sums of the integer weights (the paper's
+ * "un-normalized cumulative distribution", step 2), built once:
+ *     cw[off[v] + i] = w[off[v]] + ... + w[off[v] + i].
+ * weights may be NULL (unweighted): then cw[off[v]+i] = i + 1. */
+void oracle_prefix(uint32_t n, const uint64_t* off, const uint32_t* w, uint64_t* cw)
+{
+    uint32_t v;
+    for (v = 0; v < n; v++) {
+        uint64_t acc = 0;
+        uint64_t e;
+        for (e = off[v]; e < off[v + 1]; e++) {
+            acc += (w != NULL) ? (uint64_t)w[e] : 1u;
+            cw[e] = acc;
+        }
+    }
+}
+
+/* Smallest i in [0, d) with row[i] > r, for a non-decreasing row with
+ * row[d-1] > r ("a binary search"; §8(c) c11: any search returning
+ * this index is valid).  Plain bisection on [lo, hi). */
+uint64_t oracle_upper_bound(const uint64_t* row, uint64_t d, uint64_t r)
+{
+    uint64_t lo = 0, hi = d;
+    while (lo < hi) {
+        uint64_t mid = lo + (hi - lo) / 2;
+        if (row[mid] > r)
+            hi = mid;
+        else
+            lo = mid + 1;
+    }
+    return lo;
+}
+
+/* INMEMBER(t, x): does x occur in the sorted row col[off[t] .. off[t+1])?
+ * (beta_q uses "x in N(t)"; rows are sorted index vectors.) */
+int oracle_in_row(const uint64_t* off, const uint32_t* col, uint32_t t, uint32_t x)
+{
+    uint64_t lo = off[t], hi = off[t + 1];
+    while (lo < hi) {
+        uint64_t mid = lo + (hi - lo) / 2;
+        if (col[mid] == x)
+            return 1;
+        if (col[mid] < x)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return 0;
+}
+
+/* PROPOSE(v, x64) (§8(c)): a neighbour of v drawn with probability w_vx / W_v
+ * (uniform draw in [0, W_v), then search of the cumulative sum).
+ * cw == NULL means unweighted: the index is BOUNDED(x64, deg(v)).
+ * Requires deg(v) >= 1. */
+uint32_t oracle_propose(const uint64_t* off, const uint32_t* col, const uint64_t* cw,
+                        uint32_t v, uint64_t x64)
+{
+    uint64_t lo = off[v];
+    uint64_t d = off[v + 1] - lo;
+    uint64_t i;
+    if (cw != NULL) {
+        uint64_t W = cw[lo + d - 1];
+        uint64_t r = oracle_bounded(x64, W);
+        i = oracle_upper_bound(cw + lo, d, r);
+    } else {
+        i = oracle_bounded(x64, d);
+    }
+    return col[lo + i];
+}
+
+static uint64_t x64_of(const uint32_t o[4])
+{
+    return ((uint64_t)o[1] << 32) | (uint64_t)o[0];
+}
+
+/* One node2vec step from v, coming from t (t != ORACLE_NONE), at step index s
+ * of walk wid (the attempt loop of §8(c) WALK):  for a = 0, 1, 2, ...:
+ *   (x64, u) = DRAW(seed, wid, s, a);  x = PROPOSE(v, x64);
+ *   T = T_p if x == t  (gamma_p: d(t,x) = 0)
+ *       T_1 if x in N(t) (beta_q: d(t,x) = 1)
+ *       T_q otherwise    (d(t,x) = 2)
+ *   accept iff u < T.
+ * Accepting x with probability T_class(x)/2^32 after proposing it with
+ * probability w_vx/W_v samples x with probability proportional to
+ * w_vx * T_class(x), i.e. to alpha_pq(t,x) * w_vx (Eq.1) because the T_c are
+ * proportional to 1/p, 1, 1/q.  Returns x; *attempts = number of draws used. */
+uint32_t oracle_node2vec_step(const uint64_t* off, const uint32_t* col, const uint64_t* cw,
+                              const uint64_t T[3], uint64_t seed, uint64_t wid, uint32_t s,
+                              uint32_t t, uint32_t v, uint32_t* attempts)
+{
+    uint32_t a = 0;
+    for (;;) {
+        uint32_t o[4];
+        uint32_t x;
+        uint64_t thr;
+        oracle_draw(seed, wid, s, a, o);
+        x = oracle_propose(off, col, cw, v, x64_of(o));
+        if (x == t)
+            thr = T[0];
+        else if (oracle_in_row(off, col, t, x))
+            thr = T[1];
+        else
+            thr = T[2];
+        a++;
+        if ((uint64_t)o[2] < thr) {
+            *attempts = a;
+            return x;
+        }
+    }
+}
+
+/* WALK (§8(c)) for num_walks start nodes.  Row i of out (length L) is the walk
+ * with id base + i.  mode 0 = first-order, mode 1 = node2vec
+ * (P:415-497).  L = nodes per row including the start (§8(c) c1).  A start id
+ * >= n gives an all-PAD row (c14); a node with out-degree 0 ends the walk and
+ * the rest of the row stays PAD (c3).  The first node2vec step, having no t,
+ * is a first-order step with attempt 0 (c2).
+ * Returns 0, or 1 if (mode == 1 and) the thresholds are invalid.
+ * If steps_out != NULL, *steps_out += realised transitions;
+ * if attempts_out != NULL, *attempts_out += draws used by node2vec steps s >= 2. */
+int oracle_walks(uint32_t n, const uint64_t* off, const uint32_t* col, const uint64_t* cw,
+                 const uint32_t* starts, uint64_t num_walks, uint64_t base, uint32_t L,
+                 int mode, double p, double q, uint64_t seed, uint32_t* out,
+                 uint64_t* steps_out, uint64_t* attempts_out)
+{
+    uint64_t T[3] = {0, 0, 0};
+    uint64_t i;
+    uint64_t steps = 0, attempts = 0;
+    if (mode == 1 && oracle_thresholds(p, q, T) != 0)
+        return 1;
+    for (i = 0; i < num_walks; i++) {
+        uint32_t* row = out + i * (uint64_t)L;
+        uint64_t wid = base + i;
+        uint32_t start = starts[i];
+        uint32_t t, v, s, j;
+        for (j = 0; j < L; j++)
+            row[j] = ORACLE_PAD;
+        if (start >= n || L == 0)
+            continue;
+        row[0] = start;
+        t = ORACLE_NONE;
+        v = start;
+        for (s = 1; s < L; s++) {
+            uint32_t x;
+            if (off[v + 1] == off[v])
+                break;
+            if (mode == 0 || t == ORACLE_NONE) {
+                uint32_t o[4];
+                oracle_draw(seed, wid, s, 0, o);
+                x = oracle_propose(off, col, cw, v, x64_of(o));
+            } else {
+                uint32_t a = 0;
+                x = oracle_node2vec_step(off, col, cw, T, seed, wid, s, t, v, &a);
+                attempts += a;
+            }
+            row[s] = x;
+            steps++;
+            t = v;
+            v = x;
+        }
+    }
+    if (steps_out != NULL)
+        *steps_out += steps;
+    if (attempts_out != NULL)
+        *attempts_out += attempts;
+    return 0;
+}
+
+/* Batched single steps for the statistical pins (tests only).
+ * First-order: x_out[k] = the step-s proposal from v for walk id wid0 + k.
+ * Node2vec:    x_out[k], att_out[k] = the step-s node2vec step from v coming
+ *              from t for walk id wid0 + k.  Returns 1 on invalid thresholds. */
+void oracle_first_order_steps(const uint64_t* off, const uint32_t* col, const uint64_t* cw,
+                              uint64_t seed, uint32_t v, uint32_t s, uint64_t wid0,
+                              uint64_t count, uint32_t* x_out)
+{
+    uint64_t k;
+    for (k = 0; k < count; k++) {
+        uint32_t o[4];
+        oracle_draw(seed, wid0 + k, s, 0, o);
+        x_out[k] = oracle_propose(off, col, cw, v, x64_of(o));
+    }
+}
+
+int oracle_node2vec_steps(const uint64_t* off, const uint32_t* col, const uint64_t* cw,
+                          double p, double q, uint64_t seed, uint32_t t, uint32_t v,
+                          uint32_t s, uint64_t wid0, uint64_t count, uint32_t* x_out,
+                          uint32_t* att_out)
+{
+    uint64_t T[3];
+    uint64_t k;
+    if (oracle_thresholds(p, q, T) != 0)
+        return 1;
+    for (k = 0; k < count; k++)
+        x_out[k] = oracle_node2vec_step(off, col, cw, T, seed, wid0 + k, s, t, v, &att_out[k]);
+    return 0;
+}

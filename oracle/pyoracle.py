@@ -1,0 +1,143 @@
+"""Pure-Python transliteration of ``grape_oracle.c`` — TEST INFRASTRUCTURE ONLY.
+
+Written independently of the C file from the same rules,
+with Python big integers for the 128-bit product and ``bisect`` for the
+searches, for tiny graphs only.  Its purpose is to catch implementation slips
+in the C oracle (overflow, word order, off-by-one) by bit-exact comparison;
+the *rules themselves* are pinned by the statistical / closed-form tests.
+
+The ``mutation`` knob builds deliberately wrong samplers for the test-power
+checks (tests/test_oracle_stats.py): a statistical pin that cannot tell these
+apart from the correct rule has no power.
+"""
+from __future__ import annotations
+
+import bisect
+from fractions import Fraction
+import math
+
+PAD = 0xFFFFFFFF
+NONE = 0xFFFFFFFF
+_MASK32 = 0xFFFFFFFF
+
+
+def philox4x32_10(ctr, key):
+    c0, c1, c2, c3 = (int(v) & _MASK32 for v in ctr)
+    k0, k1 = (int(v) & _MASK32 for v in key)
+    for rnd in range(10):
+        if rnd:
+            k0 = (k0 + 0x9E3779B9) & _MASK32
+            k1 = (k1 + 0xBB67AE85) & _MASK32
+        p0 = 0xD2511F53 * c0
+        p1 = 0xCD9E8D57 * c2
+        c0, c1, c2, c3 = ((p1 >> 32) ^ c1 ^ k0) & _MASK32, p1 & _MASK32, \
+                         ((p0 >> 32) ^ c3 ^ k1) & _MASK32, p0 & _MASK32
+    return c0, c1, c2, c3
+
+
+def draw(seed, wid, s, a):
+    return philox4x32_10((wid & _MASK32, wid >> 32, s, a), (seed & _MASK32, seed >> 32))
+
+
+def bounded(x64, W):
+    return (x64 * W) >> 64
+
+
+def thresholds(p, q):
+    if not (p > 0 and q > 0 and math.isfinite(p) and math.isfinite(q)):
+        return None
+    mn, mx = min(p, 1.0, q), max(p, 1.0, q)
+    if mx / mn > 2.0 ** 24:
+        return None
+    return tuple(int(math.floor(math.ldexp(mn / c, 32))) for c in (p, 1.0, q))
+
+
+class PyGraph:
+    def __init__(self, n, off, col, w=None):
+        self.n = int(n)
+        self.off = [int(v) for v in off]
+        self.col = [int(v) for v in col]
+        self.rows = [self.col[self.off[v]:self.off[v + 1]] for v in range(self.n)]
+        self.cw = None
+        if w is not None:
+            w = [int(v) for v in w]
+            self.cw = []
+            for v in range(self.n):
+                acc, row = 0, []
+                for e in range(self.off[v], self.off[v + 1]):
+                    acc += w[e]
+                    row.append(acc)
+                self.cw.append(row)
+
+    def propose(self, v, x64):
+        row = self.rows[v]
+        if self.cw is None:
+            return row[bounded(x64, len(row))]
+        c = self.cw[v]
+        r = bounded(x64, c[-1])
+        return row[bisect.bisect_right(c, r)]
+
+    def member(self, t, x):
+        row = self.rows[t]
+        i = bisect.bisect_left(row, x)
+        return i < len(row) and row[i] == x
+
+    def node2vec_step(self, T, seed, wid, s, t, v, mutation=None):
+        a = 0
+        while True:
+            o = draw(seed, wid, s, a + (1 if mutation == "attempt+1" else 0))
+            x = self.propose(v, (o[1] << 32) | o[0])
+            if x == t and mutation != "drop-return":
+                thr = T[0]
+            elif self.member(t, x):
+                thr = T[2] if mutation == "swap-1-q" else T[1]
+            else:
+                thr = T[1] if mutation == "swap-1-q" else T[2]
+            a += 1
+            if o[2] < thr:
+                return x, a
+
+    def walk(self, start, wid, L, mode="node2vec", p=1.0, q=1.0, seed=42, mutation=None):
+        row = [PAD] * L
+        if start >= self.n or L == 0:
+            return row, 0
+        T = thresholds(p, q) if mode == "node2vec" else None
+        if mode == "node2vec" and T is None:
+            raise ValueError("bad p/q")
+        row[0] = start
+        t, v, steps = NONE, start, 0
+        for s in range(1, L):
+            if not self.rows[v]:
+                break
+            if mode == "first_order" or t == NONE:
+                o = draw(seed, wid, s, 0)
+                x = self.propose(v, (o[1] << 32) | o[0])
+            else:
+                x, _ = self.node2vec_step(T, seed, wid, s, t, v, mutation)
+            row[s] = x
+            steps += 1
+            t, v = v, x
+        return row, steps
+
+
+def eq1_law(g: PyGraph, t, v, p, q, weights_of=None):
+    """Exact node2vec step law from Eq.1 as Fractions:
+    pi_vx = alpha_pq(t,x) w_vx, alpha = 1/p (x == t), 1 (x in N(t)), 1/q (else)."""
+    p, q = Fraction(p), Fraction(q)
+    row = g.rows[v]
+    if g.cw is None:
+        w = [1] * len(row)
+    else:
+        c = g.cw[v]
+        w = [c[0]] + [c[i] - c[i - 1] for i in range(1, len(c))]
+    pis = []
+    for x, wx in zip(row, w):
+        if x == t:
+            alpha = 1 / p
+        elif g.member(t, x):
+            alpha = Fraction(1)
+        else:
+            alpha = 1 / q
+        pis.append(alpha * wx)
+    tot = sum(pis)
+    return {x: pi / tot for x, pi in zip(row, pis)}
