@@ -1,0 +1,27 @@
+# Build the product library (CUDA, sm_100a) and the CPU oracle (test infrastructure).
+NVCC      ?= nvcc
+ARCH      ?= -gencode arch=compute_100a,code=sm_100a
+NVFLAGS   ?= -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -Wall -Iinclude \
+             -Xptxas -v --expt-relaxed-constexpr
+PKG       := paper_2110_06196_b200
+SRCS      := $(wildcard $(PKG)/csrc/*.cu)
+HDRS      := $(wildcard $(PKG)/csrc/*.h $(PKG)/csrc/*.cuh) include/grape_walk.h
+OBJS      := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRCS))
+LIB       := $(PKG)/libgrape_walk.so
+
+all: $(LIB) oracle/liboracle.so
+
+build/%.o: $(PKG)/csrc/%.cu $(HDRS)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -cudart static
+
+oracle/liboracle.so: oracle/grape_oracle.c
+	gcc -O2 -std=gnu99 -fPIC -shared -ffp-contract=off -fno-fast-math -Wall -o $@ $< -lm
+
+clean:
+	rm -rf build $(LIB) oracle/liboracle.so
+
+.PHONY: all clean

@@ -1,0 +1,343 @@
+#!/usr/bin/env python
+"""Benchmark: node2vec random-walk steps/s on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N --steps K --warmup W] [--config 2] [--impl ours|reference]
+
+One "step" of this benchmark = one pass of the whole hot path over one batch:
+grape_walks_node2vec over every walk of the workload (BASELINE configs[1] by
+default: Chung-Lu 1M nodes / ~20M edges, weights U{1..100}, p=0.5, q=2,
+10 walks per node, L=80).  N > 1 (torchrun): every rank holds a replica of
+the graph and runs the same per-GPU workload on its own walk-id range
+(weak scaling, no collective on the data path).  Rank 0 prints one JSON line.
+
+--impl reference times the CPU oracle (the only reference this paper-tier
+task has) on a bounded sample of the same workload on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from graphgen import CONFIGS, config_graph, config_walks, starts_per_node  # noqa: E402
+
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.gpu)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend, rank=rank, world_size=world)
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    return world, rank, local
+
+
+def _allreduce(x: float, op, world):
+    if world == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    dist.all_reduce(t, op=op)
+    return float(t.item())
+
+
+def _oracle_sample(g_cpu, wk, budget_s: float, first_wid: int = 0, cores: int | None = None):
+    """Run the oracle (as it stands) on consecutive walks until ~budget_s of CPU
+    work per thread; returns (realised steps, seconds, walks, threads, attempts)."""
+    from oracle.oracle import Oracle
+    o = Oracle(*g_cpu.numpy())
+    n = g_cpu.n
+    cores = cores or os.cpu_count() or 1
+    W = n * wk["walks_per_node"]
+    starts_all = (np.arange(W, dtype=np.int64) % n).astype(np.uint32)
+    # calibrate the per-thread batch on 64 walks
+    t0 = time.perf_counter()
+    _, s0 = o.walks(starts_all[:64], wk["L"], mode=wk["mode"], p=wk["p"], q=wk["q"], seed=wk["seed"])
+    dt = max(time.perf_counter() - t0, 1e-4)
+    per_thread = max(64, int(64 * budget_s / dt))
+    total = min(W - first_wid, per_thread * cores)
+    chunks = np.array_split(np.arange(first_wid, first_wid + total), cores)
+    res = [None] * cores
+
+    def work(k):
+        ids = chunks[k]
+        if len(ids) == 0:
+            res[k] = (0, 0)
+            return
+        _, st, att = o.walks(starts_all[ids[0]:ids[-1] + 1], wk["L"], mode=wk["mode"], p=wk["p"],
+                             q=wk["q"], seed=wk["seed"], base=int(ids[0]), with_attempts=True)
+        res[k] = (st, att)
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(cores)]
+    t0 = time.perf_counter()
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    secs = time.perf_counter() - t0
+    steps = sum(r[0] for r in res)
+    att = sum(r[1] for r in res)
+    return steps, secs, int(total), cores, att
+
+
+def _workload_desc(k, g, wk, W):
+    return {"workload": f"BASELINE configs[{k - 1}]: {CONFIGS[k]['name']}", "graph": g.name,
+            "nodes": g.n, "arcs": g.m, "weighted": g.w is not None, "walks_per_gpu": W, "L": wk["L"],
+            "p": wk["p"], "q": wk["q"], "seed": wk["seed"],
+            "l2": "no flush: per-step output (W*L*4 B) and graph exceed the 126 MB L2"}
+
+
+def run_reference(args):
+    world, rank, _ = _dist_setup(args)
+    if rank != 0:
+        return
+    k = args.config
+    wk = config_walks(k)
+    g = config_graph(k)
+    W = g.n * wk["walks_per_node"]
+    vals, total_steps, total_secs = [], 0, 0.0
+    for i in range(args.warmup + args.steps):
+        steps, secs, walks, cores, _ = _oracle_sample(g, wk, args.ref_budget, first_wid=(i * 997) % max(W - 1, 1))
+        if i >= args.warmup:
+            vals.append(steps / secs)
+            total_steps += steps
+            total_secs += secs
+    v = total_steps / total_secs
+    line = {"impl": "reference", "metric": "random-walk steps/sec (node2vec 2nd-order)", "value": v,
+            "unit": "steps/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * total_secs / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32/u64 integer", "data": "synthetic (seeded generator)",
+            "config": _workload_desc(k, g, wk, W),
+            "cpu_baseline": {"value": v, "unit": "steps/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{walks} consecutive walks per step of the workload (bounded sample)"},
+            "e2e": {"value": v, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    world, rank, local = _dist_setup(args)
+    import paper_2110_06196_b200 as grape
+    k = args.config
+    wk = config_walks(k)
+    dev = torch.device("cuda", local)
+    g = config_graph(k, device=dev)
+    dg = grape.graph_from_csr(g.off, g.col, g.w, device=local, symmetric=g.symmetric)
+    info = dg.info
+    W = g.n * wk["walks_per_node"]
+    L = wk["L"]
+    base = rank * W
+    starts = starts_per_node(g.n, wk["walks_per_node"], device=dev)
+    out = torch.empty((W, L), dtype=torch.int32, device=dev)
+    steps_ctr = torch.zeros(1, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    node2vec = wk["mode"] == "node2vec"
+
+    def one(ctr):
+        if node2vec:
+            grape.walks_node2vec(dg, starts, L, wk["p"], wk["q"], seed=wk["seed"], walk_id_base=base,
+                                 out=out, steps=ctr)
+        else:
+            grape.walks_first_order(dg, starts, L, seed=wk["seed"], walk_id_base=base, out=out, steps=ctr)
+
+    for _ in range(args.warmup):
+        one(None)
+    torch.cuda.synchronize(dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        t_wall = time.perf_counter()
+        for i in range(args.steps):
+            ev[i][0].record(stream)
+            one(steps_ctr)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+        t_wall = time.perf_counter() - t_wall
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    kernel_ms = [a.elapsed_time(b) for a, b in ev]
+    my_ms = float(sum(kernel_ms))
+    my_steps = float(steps_ctr.item())
+    max_ms = _allreduce(my_ms, dist.ReduceOp.MAX, world)
+    tot_steps = _allreduce(my_steps, dist.ReduceOp.SUM, world)
+    value = tot_steps / (max_ms / 1e3)
+    steps_per_launch = my_steps / args.steps
+    avg_launch_ms = my_ms / args.steps
+
+    # ---- e2e: same metric through the C-ABI with HOST buffers (pinned), H2D/D2H inside
+    e2e = None
+    if not args.no_e2e:
+        h_starts = starts.cpu().pin_memory()
+        h_out = torch.empty((W, L), dtype=torch.int32, pin_memory=True)
+        h_steps = torch.zeros(1, dtype=torch.int64)
+        kw = dict(seed=wk["seed"], walk_id_base=base, out=h_out)
+        grape.walks_node2vec(dg, h_starts, L, wk["p"], wk["q"], **kw) if node2vec else \
+            grape.walks_first_order(dg, h_starts, L, **kw)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        e2e_steps = max(1, min(args.steps, 3))
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            if node2vec:
+                grape.walks_node2vec(dg, h_starts, L, wk["p"], wk["q"], steps=h_steps, **kw)
+            else:
+                grape.walks_first_order(dg, h_starts, L, steps=h_steps, **kw)
+        torch.cuda.synchronize(dev)
+        e2e_s = time.perf_counter() - t0
+        e2e_s = _allreduce(e2e_s, dist.ReduceOp.MAX, world)
+        e2e_tot = _allreduce(float(h_steps.item()), dist.ReduceOp.SUM, world)
+        e2e = {"value": e2e_tot / e2e_s, "unit": "steps/s", "h2d_bytes_per_step": int(W * 4),
+               "d2h_bytes_per_step": int(W * L * 4 + 8), "steps_timed": e2e_steps,
+               "path": "grape_walks_node2vec with pinned host starts/out (library-staged, chunked H2D/kernel/D2H)"}
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only) and the roofline model
+    cpu = None
+    att_per_step = None
+    if rank == 0:
+        g_cpu = g.to("cpu")
+        budget = args.cpu_budget if world == 1 else 2.0
+        s, secs, walks, cores, att = _oracle_sample(g_cpu, wk, budget)
+        if node2vec and s:
+            firsts = walks  # one first-order step per walk that moves (upper bound; all starts valid here)
+            att_per_step = (att + firsts) / s
+        if world == 1:
+            cpu = {"value": s / secs, "unit": "steps/s", "cores": cores, "kind": "oracle",
+                   "sample": f"first {walks} walks (wid 0..{walks - 1}) of the same workload, "
+                             f"{cores} threads, {secs:.1f} s"}
+    peak, peak_src = _peaks()
+    roof = None
+    if rank == 0:
+        cwb = info["cw_bytes"]
+        A = att_per_step if att_per_step is not None else 1.0
+        # compulsory random-sector model: per realised step one 32-B sector for
+        # off[v..v+1], one for W_v (weighted), and per attempt one sector of the prefix row
+        # (weighted), one of col (proposal) and one of N(t) (membership); + 4 B of output.
+        per_step = 32 * (1 + (1 if cwb else 0)) + A * 32 * ((1 if cwb else 0) + 1 + (1 if node2vec else 0)) + 4
+        achieved = per_step * steps_per_launch / (avg_launch_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": args.traffic_per_launch,
+                "kernel": "walk_kernel (node2vec)" if node2vec else "walk_kernel (first order)",
+                "bytes_per_step_model": per_step, "attempts_per_step": A, "peak_source": peak_src,
+                "avg_launch_ms": avg_launch_ms}
+    clocks = clk.summary()
+    if rank == 0:
+        line = {"metric": "random-walk steps/sec (node2vec 2nd-order)", "value": value, "unit": "steps/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32/u64 integer",
+                "data": "synthetic (seeded generator, graphgen/)", "config": _workload_desc(k, g, wk, W),
+                "gpu_launches": args.steps, "realised_steps_per_gpu_step": steps_per_launch,
+                "nominal_steps_per_gpu_step": W * (L - 1), "wall_s_timed": t_wall,
+                "clocks": clocks, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "graph_device_bytes": info["device_bytes"]}
+        print(json.dumps(line), flush=True)
+    dg.free()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work per thread")
+    ap.add_argument("--ref-budget", type=float, default=6.0)
+    ap.add_argument("--traffic-per-launch", type=float, default=None,
+                    help="ncu dram bytes per launch of the walk kernel (from profiles/)")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

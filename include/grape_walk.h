@@ -1,0 +1,170 @@
+/*
+ * grape_walk.h — C-ABI of the B200-native GRAPE random-walk engine.
+ *
+ * The hot path of GRAPE (arxiv 2110.06196) that this library implements:
+ * bulk first-order and second-order (node2vec p/q) random walks over a large
+ * sparse graph (§4.3).  Plain C types
+ * only: pointers, sizes, a CUDA stream handle.  Every call returns a
+ * grape_status; nothing throws across the ABI.  On failure a thread-local
+ * message is available from grape_last_error().
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n; S:n = SPEC.md line n;
+ * §8(x) = /root/repo/SURVEY.md §8(x); DESIGN.md §k = /root/repo/DESIGN.md.
+ *
+ * ---------------------------------------------------------------- the rules
+ * Walk matrix: row i (L entries, u32, row-major) is the walk with id
+ * wid = walk_id_base + i, starting at starts[i].  L counts nodes including the
+ * start, so a full walk makes L-1 transitions ("steps") (§8(c) c1).
+ *   - start >= num_nodes  -> the whole row is GRAPE_PAD (§8(c) c14);
+ *   - a node with out-degree 0 ends the walk; the rest of the row is
+ *     GRAPE_PAD (§8(c) c3; the paper is silent, SPEC S:233 truncates).
+ * Random draws: Philox4x32-10 with counter (wid & 0xffffffff, wid >> 32,
+ * step s, attempt a) and key (seed & 0xffffffff, seed >> 32); output words
+ * o0,o1 form x64 = o1<<32 | o0, o2 is the acceptance draw u (§8(c) c7).
+ * Proposal from v (§4.3.2 steps 2-4): r = (x64 * W_v) >> 64 with
+ * W_v = sum of v's weights; the neighbour is col[off[v] + i] for the smallest
+ * i whose row-local prefix sum exceeds r; unweighted: i = (x64 * deg v) >> 64
+ * (P:411).  Node2vec (Eq.1-3): from v, coming from t, attempt
+ * a = 0,1,...: propose x with draw (wid, s, a); accept iff u < T_class where
+ * class = p if x == t, 1 if x in N(t), q otherwise, and
+ *   T_c = floor(2^32 * min(p,1,q) / c)      (IEEE binary64, §8(c) c9)
+ * so x is taken with probability proportional to alpha_pq(t,x) * w_vx.
+ * The first step of a node2vec walk (no t yet) is a first-order step with
+ * attempt 0 (§8(c) c2), hence node2vec with p = q = 1 is bit-identical to
+ * first order.  Results are bit-identical to the CPU oracle (oracle/).
+ */
+#ifndef GRAPE_WALK_H
+#define GRAPE_WALK_H
+
+#include <stdint.h>
+#include <cuda_runtime_api.h>   /* cudaStream_t only */
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct grape_graph grape_graph;   /* opaque, device-resident, immutable */
+
+typedef enum {
+    GRAPE_OK = 0,
+    GRAPE_EINVAL = 1,    /* bad argument or invalid graph; nothing was launched */
+    GRAPE_ENOMEM = 2,    /* device allocation failed */
+    GRAPE_ECUDA = 3      /* a CUDA runtime call or launch failed */
+} grape_status;
+
+#define GRAPE_PAD 0xFFFFFFFFu
+
+/* Flags for grape_graph_from_csr. */
+enum {
+    /* Caller asserts arc (u,v) exists iff arc (v,u) exists (undirected graph).
+     * Lets the node2vec membership test "x in N(t)" be evaluated as
+     * "t in N(x)" on the shorter of the two rows — the same predicate
+     * (§8(c) c12).  Checked on the device unless GRAPE_SKIP_VALIDATION. */
+    GRAPE_SYMMETRIC = 1u << 0,
+    /* Skip the O(m) device validation of the CSR (trusted input). */
+    GRAPE_SKIP_VALIDATION = 1u << 1
+};
+
+typedef struct {
+    uint32_t num_nodes;
+    uint64_t num_arcs;
+    uint32_t weighted;        /* 1 if built with weights */
+    uint32_t flags;           /* GRAPE_SYMMETRIC / ... as accepted */
+    uint32_t cw_bytes;        /* bytes per stored prefix-sum entry: 0 (unweighted), 4 or 8 */
+    uint32_t max_degree;
+    uint64_t max_row_weight;  /* max_v W_v (deg for unweighted) */
+    uint64_t device_bytes;    /* device memory owned by the handle */
+    int device;
+} grape_graph_info;
+
+/*
+ * grape_graph_from_csr — build the device CSR (§8(a) a1; the paper's
+ * "explicit destinations vector" + "explicit out-bound degrees vector",
+ * P:368-374, plus the per-row cumulative weights of P:509).
+ *
+ *   num_nodes    n, node ids are [0, n); n < 2^32 - 1 so no id equals GRAPE_PAD.
+ *   num_arcs     m (an undirected edge counts twice).
+ *   row_offsets  u64[n+1]: off[0] = 0, off[n] = m, non-decreasing.
+ *   col_indices  u32[m]: every value < n, strictly increasing within a row
+ *                (sorted, no duplicate arcs; "sorted vectors").
+ *   weights      u32[m], every value >= 1, or NULL for an unweighted graph.
+ *   device       CUDA device ordinal that will own the graph.
+ *   flags        GRAPE_SYMMETRIC | GRAPE_SKIP_VALIDATION.
+ *   out          receives the handle.
+ * The three arrays may be host (pageable or pinned) or device pointers; they
+ * are copied, and the call is synchronous: the caller may free them on return.
+ * The handle stores off (u64[n+1]), col (u32[m]) and the row-local inclusive
+ * prefix sums of the weights — u32[m] when every row sum fits in 32 bits,
+ * else u64[m] (same selected index either way).
+ * Errors: GRAPE_EINVAL for null pointers, n >= 2^32-1, or a CSR that fails
+ * validation (message names the first check that failed); GRAPE_ENOMEM;
+ * GRAPE_ECUDA.  On error *out is set to NULL and nothing is leaked.
+ */
+grape_status grape_graph_from_csr(uint32_t num_nodes, uint64_t num_arcs,
+                                  const uint64_t* row_offsets, const uint32_t* col_indices,
+                                  const uint32_t* weights, int device, uint32_t flags,
+                                  grape_graph** out);
+
+/* Synchronises the owning device, then frees the handle.  NULL is a no-op. */
+grape_status grape_graph_free(grape_graph* g);
+
+/* Fills *info.  EINVAL on NULL arguments. */
+grape_status grape_graph_get_info(const grape_graph* g, grape_graph_info* info);
+
+/*
+ * grape_walks_first_order — first-order walks (DeepWalk; P:394, P:411 unweighted
+ * uniform, P:509-511 weighted), one per start.
+ *
+ *   g             graph handle; the current device must be g's device.
+ *   starts        u32[num_walks] start nodes (device, or host — see below).
+ *   num_walks     W; 0 returns GRAPE_OK without launching.
+ *   walk_id_base  wid of row 0 (sharding: rank r passes its first global wid).
+ *   walk_length   L >= 1 (nodes per row, including the start).
+ *   seed          64-bit Philox key.
+ *   out           u32[num_walks * L], row-major (device, or host).
+ *   steps_out     NULL, or one u64 to which the number of realised
+ *                 transitions is ADDED (device pointer, or host pointer).
+ *   stream        stream for all work (0 = legacy default stream).
+ * Device buffers: the call is asynchronous on `stream`; buffers must stay
+ * alive until the stream reaches this work; faults surface at the caller's
+ * next synchronisation.  Host buffers (starts and out both host memory;
+ * pinned memory gives copy/compute overlap): the library stages chunks
+ * through device memory, overlapping H2D / kernel / D2H, and the call returns
+ * when out (and *steps_out) are complete.  Mixing host and device for starts
+ * and out is EINVAL.
+ * Errors: EINVAL (NULL g/starts/out, L = 0, num_walks * L overflow, wrong
+ * current device); ENOMEM (staging); ECUDA (launch).
+ */
+grape_status grape_walks_first_order(const grape_graph* g, const uint32_t* starts,
+                                     uint64_t num_walks, uint64_t walk_id_base,
+                                     uint32_t walk_length, uint64_t seed, uint32_t* out,
+                                     uint64_t* steps_out, cudaStream_t stream);
+
+/*
+ * grape_walks_node2vec — second-order node2vec walks (Eq.1-3) by
+ * rejection sampling with integer thresholds (rules above).
+ *   p  return parameter, q  in-out parameter: finite, > 0, and
+ *      max(p,1,q) / min(p,1,q) <= 2^24 (keeps every T_c >= 2^8 so the
+ *      attempt loop ends; §8(c) c10) — else GRAPE_EINVAL.
+ * All other arguments, ownership and errors as grape_walks_first_order.
+ * Specialisation (the paper's 8 dispatch paths over p = 1?, q = 1?,
+ * weighted?) is internal and never changes a result.
+ */
+grape_status grape_walks_node2vec(const grape_graph* g, const uint32_t* starts,
+                                  uint64_t num_walks, uint64_t walk_id_base,
+                                  uint32_t walk_length, double p, double q, uint64_t seed,
+                                  uint32_t* out, uint64_t* steps_out, cudaStream_t stream);
+
+/* Static string for a status code. */
+const char* grape_status_string(grape_status s);
+
+/* Detail of the last error on the calling thread ("" if none). */
+const char* grape_last_error(void);
+
+/* Library version string, e.g. "grape-b200 0.1.0 (sm_100a)". */
+const char* grape_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GRAPE_WALK_H */

@@ -1,0 +1,157 @@
+"""paper_2110_06196_b200 — B200-native bulk random walks (GRAPE, arxiv 2110.06196).
+
+Thin Python binding over the C-ABI in ``include/grape_walk.h`` (argument
+marshalling only; every step of the walk runs in the CUDA kernels of
+``libgrape_walk.so``).  PyTorch supplies device memory and streams.
+
+    g = graph_from_csr(off, col, weights=None, device=0, symmetric=True)
+    out = walks_node2vec(g, starts, L=80, p=0.5, q=2.0, seed=42)   # int32 [W, L]; PAD = -1
+    out = walks_first_order(g, starts, L=32, seed=42)
+
+``starts`` on a CUDA device -> asynchronous on the current stream, result on
+the device.  ``starts`` on the CPU -> the library stages host buffers itself
+(H2D / kernel / D2H pipelined in chunks) and returns a (pinned) CPU tensor.
+Walk matrices are int32 tensors holding the u32 bit patterns: GRAPE_PAD
+(0xFFFFFFFF) reads as -1.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _capi
+from ._capi import (GRAPE_PAD, GRAPE_SYMMETRIC, GRAPE_SKIP_VALIDATION, GrapeError,  # noqa: F401
+                    GRAPE_OK, GRAPE_EINVAL, GRAPE_ENOMEM, GRAPE_ECUDA)
+
+_lib = _capi.load()
+PAD_I32 = -1
+
+
+def version() -> str:
+    return _lib.grape_version().decode()
+
+
+def _as_tensor(a, dtype) -> torch.Tensor:
+    if isinstance(a, torch.Tensor):
+        t = a
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(a))
+    if t.dtype == torch.uint32:
+        t = t.view(torch.int32)
+    if t.dtype == torch.uint64:
+        t = t.view(torch.int64)
+    if t.dtype != dtype:
+        t = t.to(dtype)
+    return t.contiguous()
+
+
+class Graph:
+    """Owning handle of a device CSR (grape_graph*)."""
+
+    def __init__(self, handle: int, device: int):
+        self._h = ctypes.c_void_p(handle)
+        self.device = device
+        info = _capi.GraphInfo()
+        _capi.check(_lib, _lib.grape_graph_get_info(self._h, ctypes.byref(info)), "grape_graph_get_info")
+        self.info = {f: getattr(info, f) for f, _ in _capi.GraphInfo._fields_}
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def num_nodes(self) -> int:
+        return self.info["num_nodes"]
+
+    @property
+    def num_arcs(self) -> int:
+        return self.info["num_arcs"]
+
+    def free(self) -> None:
+        if self._h is not None and self._h.value:
+            _capi.check(_lib, _lib.grape_graph_free(self._h), "grape_graph_free")
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    def __repr__(self):
+        return f"Graph({self.info})"
+
+
+def graph_from_csr(row_offsets, col_indices, weights=None, *, device: int = 0,
+                   symmetric: bool = False, validate: bool = True) -> Graph:
+    """grape_graph_from_csr: row_offsets u64/int64 [n+1], col_indices u32/int32 [m],
+    weights u32/int32 [m] >= 1 or None.  Host or device tensors / numpy arrays."""
+    off = _as_tensor(row_offsets, torch.int64)
+    col = _as_tensor(col_indices, torch.int32)
+    w = None if weights is None else _as_tensor(weights, torch.int32)
+    n = off.numel() - 1
+    m = col.numel()
+    flags = (GRAPE_SYMMETRIC if symmetric else 0) | (0 if validate else GRAPE_SKIP_VALIDATION)
+    h = ctypes.c_void_p()
+    st = _lib.grape_graph_from_csr(n, m, off.data_ptr(), col.data_ptr() if m else None,
+                                   None if w is None else w.data_ptr(), device, flags, ctypes.byref(h))
+    _capi.check(_lib, st, "grape_graph_from_csr")
+    return Graph(h.value, device)
+
+
+def _walks(fn_name, g: Graph, starts, L, args, seed, walk_id_base, out, steps, stream):
+    st = _as_tensor(starts, torch.int32)
+    W = st.numel()
+    fn = getattr(_lib, fn_name)
+    if st.is_cuda:
+        if st.device.index != g.device:
+            raise ValueError(f"starts on cuda:{st.device.index}, graph on cuda:{g.device}")
+        with torch.cuda.device(g.device):
+            if out is None:
+                out = torch.empty((W, L), dtype=torch.int32, device=st.device)
+            if stream is None:
+                stream = torch.cuda.current_stream(g.device).cuda_stream
+            elif isinstance(stream, torch.cuda.Stream):
+                stream = stream.cuda_stream
+            sp = None if steps is None else steps.data_ptr()
+            rc = fn(g.handle, st.data_ptr(), W, walk_id_base, L, *args, seed, out.data_ptr(), sp,
+                    ctypes.c_void_p(stream))
+        _capi.check(_lib, rc, fn_name)
+        return out
+    # host buffers: the library stages through the device itself
+    if out is None:
+        out = torch.empty((W, L), dtype=torch.int32, pin_memory=True)
+    hs = ctypes.c_uint64(0)
+    with torch.cuda.device(g.device):
+        if stream is None:
+            stream = torch.cuda.current_stream(g.device).cuda_stream
+        elif isinstance(stream, torch.cuda.Stream):
+            stream = stream.cuda_stream
+        rc = fn(g.handle, st.data_ptr(), W, walk_id_base, L, *args, seed, out.data_ptr(),
+                ctypes.byref(hs), ctypes.c_void_p(stream))
+    _capi.check(_lib, rc, fn_name)
+    if steps is not None:
+        steps += int(hs.value)
+    return out
+
+
+def walks_first_order(g: Graph, starts, L: int, *, seed: int = 42, walk_id_base: int = 0,
+                      out=None, steps=None, stream=None) -> torch.Tensor:
+    """grape_walks_first_order.  steps: optional int64 tensor (device path: 1-element
+    CUDA tensor, incremented on the device) to which realised transitions are added."""
+    return _walks("grape_walks_first_order", g, starts, L, (), seed, walk_id_base, out, steps, stream)
+
+
+def walks_node2vec(g: Graph, starts, L: int, p: float, q: float, *, seed: int = 42,
+                   walk_id_base: int = 0, out=None, steps=None, stream=None) -> torch.Tensor:
+    """grape_walks_node2vec (p = return, q = in-out parameter)."""
+    return _walks("grape_walks_node2vec", g, starts, L, (float(p), float(q)), seed, walk_id_base,
+                  out, steps, stream)
+
+
+# C-ABI names, for callers that mirror the header.
+grape_graph_from_csr = graph_from_csr
+grape_walks_first_order = walks_first_order
+grape_walks_node2vec = walks_node2vec

@@ -1,0 +1,78 @@
+"""ctypes declarations of include/grape_walk.h (argument marshalling only).
+
+The shared library is built in-tree (``make`` or ``__graft_entry__.build()``)
+as ``paper_2110_06196_b200/libgrape_walk.so``.  There is no fallback: if the
+library is missing, importing the package raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgrape_walk.so")
+
+GRAPE_OK, GRAPE_EINVAL, GRAPE_ENOMEM, GRAPE_ECUDA = 0, 1, 2, 3
+GRAPE_SYMMETRIC = 1 << 0
+GRAPE_SKIP_VALIDATION = 1 << 1
+GRAPE_PAD = 0xFFFFFFFF
+
+# Every entry point include/grape_walk.h declares (tests check the .so exports them all).
+EXPORTS = (
+    "grape_graph_from_csr", "grape_graph_free", "grape_graph_get_info",
+    "grape_walks_first_order", "grape_walks_node2vec",
+    "grape_status_string", "grape_last_error", "grape_version",
+)
+
+
+class GraphInfo(ctypes.Structure):
+    _fields_ = [
+        ("num_nodes", ctypes.c_uint32),
+        ("num_arcs", ctypes.c_uint64),
+        ("weighted", ctypes.c_uint32),
+        ("flags", ctypes.c_uint32),
+        ("cw_bytes", ctypes.c_uint32),
+        ("max_degree", ctypes.c_uint32),
+        ("max_row_weight", ctypes.c_uint64),
+        ("device_bytes", ctypes.c_uint64),
+        ("device", ctypes.c_int),
+    ]
+
+
+class GrapeError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(msg)
+        self.status = status
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    if not os.path.exists(path):
+        raise ImportError(
+            f"{path} is missing: build the CUDA library first (`make` or "
+            "`python -c 'import __graft_entry__ as g; g.build()'`). There is no CPU fallback.")
+    lib = ctypes.CDLL(path)
+    vp, u32, u64, i32, dbl = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int, ctypes.c_double
+    lib.grape_graph_from_csr.argtypes = [u32, u64, vp, vp, vp, i32, u32, ctypes.POINTER(vp)]
+    lib.grape_graph_from_csr.restype = i32
+    lib.grape_graph_free.argtypes = [vp]
+    lib.grape_graph_free.restype = i32
+    lib.grape_graph_get_info.argtypes = [vp, ctypes.POINTER(GraphInfo)]
+    lib.grape_graph_get_info.restype = i32
+    lib.grape_walks_first_order.argtypes = [vp, vp, u64, u64, u32, u64, vp, vp, vp]
+    lib.grape_walks_first_order.restype = i32
+    lib.grape_walks_node2vec.argtypes = [vp, vp, u64, u64, u32, dbl, dbl, u64, vp, vp, vp]
+    lib.grape_walks_node2vec.restype = i32
+    lib.grape_status_string.argtypes = [i32]
+    lib.grape_status_string.restype = ctypes.c_char_p
+    lib.grape_last_error.argtypes = []
+    lib.grape_last_error.restype = ctypes.c_char_p
+    lib.grape_version.argtypes = []
+    lib.grape_version.restype = ctypes.c_char_p
+    return lib
+
+
+def check(lib: ctypes.CDLL, status: int, what: str) -> None:
+    if status != GRAPE_OK:
+        detail = lib.grape_last_error().decode(errors="replace")
+        name = lib.grape_status_string(status).decode()
+        raise GrapeError(status, f"{what}: {name}: {detail}")

@@ -1,0 +1,298 @@
+// capi.cu — the extern "C" boundary (include/grape_walk.h): argument checks,
+// node2vec thresholds, device / host-buffer walk calls, error reporting.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include "internal.h"
+
+namespace grape {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...)
+{
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+grape_status cuda_fail(cudaError_t e, const char* what)
+{
+    set_error("%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+    cudaGetLastError();
+    return e == cudaErrorMemoryAllocation ? GRAPE_ENOMEM : GRAPE_ECUDA;
+}
+
+namespace {
+
+// T_c = floor(2^32 * min(p,1,q) / c) for c in (p, 1, q), IEEE binary64
+// (include/grape_walk.h; §8(c) c9-c10).  Host code: one division and one exact
+// power-of-two scaling per class.
+bool node2vec_thresholds(double p, double q, Thresholds* T)
+{
+    if (!std::isfinite(p) || !std::isfinite(q) || !(p > 0.0) || !(q > 0.0)) {
+        set_error("p and q must be finite and > 0 (got p=%g, q=%g)", p, q);
+        return false;
+    }
+    const double lo = std::fmin(std::fmin(p, 1.0), q);
+    const double hi = std::fmax(std::fmax(p, 1.0), q);
+    if (hi / lo > 16777216.0) {
+        set_error("max(p,1,q)/min(p,1,q) = %g exceeds 2^24", hi / lo);
+        return false;
+    }
+    T->Tp = (uint64_t)std::floor(std::ldexp(lo / p, 32));
+    T->T1 = (uint64_t)std::floor(std::ldexp(lo, 32));
+    T->Tq = (uint64_t)std::floor(std::ldexp(lo / q, 32));
+    return true;
+}
+
+enum class Mem { Device, Host, Invalid };
+
+Mem classify(const void* ptr)
+{
+    cudaPointerAttributes at;
+    cudaError_t e = cudaPointerGetAttributes(&at, ptr);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return Mem::Host;
+    }
+    switch (at.type) {
+    case cudaMemoryTypeDevice:
+    case cudaMemoryTypeManaged: return Mem::Device;
+    default: return Mem::Host;   // unregistered (pageable) or pinned host
+    }
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(int dev)
+    {
+        if (cudaGetDevice(&prev) != cudaSuccess) { prev = -1; ok = false; return; }
+        if (prev != dev && cudaSetDevice(dev) != cudaSuccess) ok = false;
+    }
+    ~DeviceGuard() { if (prev >= 0) cudaSetDevice(prev); }
+};
+
+// Host buffers: stage chunks through device memory.  Chunk k runs on the
+// caller's stream (H2D starts -> kernel), its D2H runs on an internal copy
+// stream, so the copy of chunk k overlaps the kernel of chunk k+1.
+grape_status walks_host(const grape_graph* g, const WalkArgs& a, bool n2v, const Thresholds& T,
+                        cudaStream_t stream, uint64_t* steps_host)
+{
+    const uint64_t L = a.L;
+    // ~256 MB of output per chunk, at least 1 walk.
+    uint64_t chunk = (256ull << 20) / (4 * L);
+    if (chunk < 1) chunk = 1;
+    if (chunk > a.num_walks) chunk = a.num_walks;
+    uint32_t* d_starts[2] = {nullptr, nullptr};
+    uint32_t* d_out[2] = {nullptr, nullptr};
+    unsigned long long* d_steps = nullptr;
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ev_kernel[2] = {nullptr, nullptr}, ev_copied[2] = {nullptr, nullptr};
+    grape_status st = GRAPE_OK;
+    cudaError_t e = cudaSuccess;
+    const int nbuf = a.num_walks > chunk ? 2 : 1;
+    for (int b = 0; b < nbuf && e == cudaSuccess; ++b) {
+        e = cudaMalloc(&d_starts[b], chunk * 4);
+        if (e == cudaSuccess) e = cudaMalloc(&d_out[b], chunk * L * 4);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_kernel[b], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_copied[b], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = cudaMalloc(&d_steps, 8);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMemsetAsync(d_steps, 0, 8, stream);
+    if (e != cudaSuccess) {
+        st = cuda_fail(e, "host-buffer staging setup");
+    } else {
+        uint64_t k = 0;
+        for (uint64_t lo = 0; lo < a.num_walks && e == cudaSuccess; lo += chunk, ++k) {
+            const int b = (int)(k % nbuf);
+            const uint64_t cnt = (a.num_walks - lo < chunk) ? a.num_walks - lo : chunk;
+            if (k >= (uint64_t)nbuf) e = cudaStreamWaitEvent(stream, ev_copied[b], 0);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(d_starts[b], a.starts + lo, cnt * 4, cudaMemcpyHostToDevice, stream);
+            if (e != cudaSuccess) break;
+            WalkArgs c = a;
+            c.starts = d_starts[b];
+            c.num_walks = cnt;
+            c.walk_id_base = a.walk_id_base + lo;
+            c.out = d_out[b];
+            c.steps_out = d_steps;
+            e = launch_walks(g, c, n2v, T, stream);
+            if (e == cudaSuccess) e = cudaEventRecord(ev_kernel[b], stream);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev_kernel[b], 0);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(a.out + lo * L, d_out[b], cnt * L * 4, cudaMemcpyDeviceToHost, cs);
+            if (e == cudaSuccess) e = cudaEventRecord(ev_copied[b], cs);
+        }
+        unsigned long long steps = 0;
+        if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&steps, d_steps, 8, cudaMemcpyDeviceToHost, stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+        if (e != cudaSuccess) st = cuda_fail(e, "host-buffer walks");
+        else if (steps_host) *steps_host += steps;
+    }
+    if (cs) { cudaStreamSynchronize(cs); cudaStreamDestroy(cs); }
+    for (int b = 0; b < 2; ++b) {
+        cudaFree(d_starts[b]);
+        cudaFree(d_out[b]);
+        if (ev_kernel[b]) cudaEventDestroy(ev_kernel[b]);
+        if (ev_copied[b]) cudaEventDestroy(ev_copied[b]);
+    }
+    cudaFree(d_steps);
+    return st;
+}
+
+grape_status walks_common(const grape_graph* g, const uint32_t* starts, uint64_t num_walks,
+                          uint64_t base, uint32_t L, bool n2v, double p, double q, uint64_t seed,
+                          uint32_t* out, uint64_t* steps_out, cudaStream_t stream)
+{
+    g_err[0] = 0;
+    if (g == nullptr || starts == nullptr || out == nullptr) {
+        set_error("graph, starts and out must be non-NULL");
+        return GRAPE_EINVAL;
+    }
+    if (L == 0) {
+        set_error("walk_length must be >= 1");
+        return GRAPE_EINVAL;
+    }
+    if (num_walks > (~0ull) / L / 4) {
+        set_error("num_walks * walk_length overflows");
+        return GRAPE_EINVAL;
+    }
+    Thresholds T{1ull << 32, 1ull << 32, 1ull << 32};
+    if (n2v && !node2vec_thresholds(p, q, &T)) return GRAPE_EINVAL;
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess) { cudaGetLastError(); cur = -1; }
+    if (cur != g->device) {
+        set_error("current device %d is not the graph's device %d", cur, g->device);
+        return GRAPE_EINVAL;
+    }
+    if (num_walks == 0) return GRAPE_OK;
+    const Mem ms = classify(starts), mo = classify(out);
+    if (ms != mo) {
+        set_error("starts and out must both be device or both be host memory");
+        return GRAPE_EINVAL;
+    }
+    WalkArgs a;
+    a.starts = starts;
+    a.num_walks = num_walks;
+    a.walk_id_base = base;
+    a.L = L;
+    a.seed = seed;
+    a.out = out;
+    a.steps_out = nullptr;
+    if (ms == Mem::Host) return walks_host(g, a, n2v, T, stream, steps_out);
+    if (steps_out != nullptr && classify(steps_out) != Mem::Device) {
+        set_error("with device buffers, steps_out must be device memory (or NULL)");
+        return GRAPE_EINVAL;
+    }
+    a.steps_out = (unsigned long long*)steps_out;
+    cudaError_t e = launch_walks(g, a, n2v, T, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "walk kernel launch");
+    return GRAPE_OK;
+}
+
+}  // namespace
+}  // namespace grape
+
+using namespace grape;
+
+extern "C" {
+
+grape_status grape_graph_from_csr(uint32_t num_nodes, uint64_t num_arcs, const uint64_t* row_offsets,
+                                  const uint32_t* col_indices, const uint32_t* weights, int device,
+                                  uint32_t flags, grape_graph** out)
+{
+    g_err[0] = 0;
+    if (out == nullptr) {
+        set_error("out must be non-NULL");
+        return GRAPE_EINVAL;
+    }
+    *out = nullptr;
+    if (row_offsets == nullptr || (num_arcs > 0 && col_indices == nullptr)) {
+        set_error("row_offsets and col_indices must be non-NULL");
+        return GRAPE_EINVAL;
+    }
+    if (num_nodes >= 0xFFFFFFFFu) {
+        set_error("num_nodes must be < 2^32 - 1 (0xFFFFFFFF is GRAPE_PAD)");
+        return GRAPE_EINVAL;
+    }
+    if (flags & ~(uint32_t)(GRAPE_SYMMETRIC | GRAPE_SKIP_VALIDATION)) {
+        set_error("unknown flags 0x%x", flags);
+        return GRAPE_EINVAL;
+    }
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+    if (device < 0 || device >= ndev) {
+        set_error("device %d out of range (%d devices)", device, ndev);
+        return GRAPE_EINVAL;
+    }
+    return build_graph(num_nodes, num_arcs, row_offsets, col_indices, weights, device, flags, out);
+}
+
+grape_status grape_graph_free(grape_graph* g)
+{
+    g_err[0] = 0;
+    if (g == nullptr) return GRAPE_OK;
+    DeviceGuard guard(g->device);
+    cudaError_t e = cudaDeviceSynchronize();
+    destroy_graph(g);
+    if (e != cudaSuccess) return cuda_fail(e, "grape_graph_free synchronize");
+    return GRAPE_OK;
+}
+
+grape_status grape_graph_get_info(const grape_graph* g, grape_graph_info* info)
+{
+    if (g == nullptr || info == nullptr) {
+        set_error("graph and info must be non-NULL");
+        return GRAPE_EINVAL;
+    }
+    info->num_nodes = g->n;
+    info->num_arcs = g->m;
+    info->weighted = g->cw_bytes != 0;
+    info->flags = g->flags;
+    info->cw_bytes = g->cw_bytes;
+    info->max_degree = g->max_degree;
+    info->max_row_weight = g->max_row_weight;
+    info->device_bytes = g->device_bytes;
+    info->device = g->device;
+    return GRAPE_OK;
+}
+
+grape_status grape_walks_first_order(const grape_graph* g, const uint32_t* starts, uint64_t num_walks,
+                                     uint64_t walk_id_base, uint32_t walk_length, uint64_t seed,
+                                     uint32_t* out, uint64_t* steps_out, cudaStream_t stream)
+{
+    return walks_common(g, starts, num_walks, walk_id_base, walk_length, false, 1.0, 1.0, seed, out,
+                        steps_out, stream);
+}
+
+grape_status grape_walks_node2vec(const grape_graph* g, const uint32_t* starts, uint64_t num_walks,
+                                  uint64_t walk_id_base, uint32_t walk_length, double p, double q,
+                                  uint64_t seed, uint32_t* out, uint64_t* steps_out, cudaStream_t stream)
+{
+    return walks_common(g, starts, num_walks, walk_id_base, walk_length, true, p, q, seed, out,
+                        steps_out, stream);
+}
+
+const char* grape_status_string(grape_status s)
+{
+    switch (s) {
+    case GRAPE_OK: return "GRAPE_OK";
+    case GRAPE_EINVAL: return "GRAPE_EINVAL: invalid argument";
+    case GRAPE_ENOMEM: return "GRAPE_ENOMEM: out of device memory";
+    case GRAPE_ECUDA: return "GRAPE_ECUDA: CUDA error";
+    default: return "GRAPE_UNKNOWN";
+    }
+}
+
+const char* grape_last_error(void) { return g_err; }
+
+const char* grape_version(void) { return "grape-b200 0.1.0 (sm_100a)"; }
+
+}  // extern "C"

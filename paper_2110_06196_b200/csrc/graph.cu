@@ -1,0 +1,278 @@
+// graph.cu — grape_graph_from_csr: copy, validate and prefix-sum the CSR on the device.
+//
+// Layout in HBM:
+//   off u64[n+1]   the paper's "explicit out-bound degrees vector" as offsets
+//   col u32[m]     the "explicit destinations vector", rows sorted
+//   cw  u32|u64[m] row-local inclusive prefix of the u32 weights ("un-normalized
+//                  cumulative distribution", built once instead of per step);
+//                  u32 when every row sum < 2^32, else u64.
+// All kernels here run once per graph (not on the timed path): one warp per row,
+// grid-stride over rows, so hub rows are scanned by a whole warp.
+#include <cstdio>
+#include <cstring>
+#include "internal.h"
+
+namespace grape {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarpsPerBlock = kThreads / 32;
+
+enum : unsigned {
+    BAD_OFF0 = 1u << 0,        // off[0] != 0
+    BAD_OFFN = 1u << 1,        // off[n] != m
+    BAD_MONO = 1u << 2,        // off[v] > off[v+1]
+    BAD_COL = 1u << 3,         // col >= n
+    BAD_SORT = 1u << 4,        // row not strictly increasing
+    BAD_W = 1u << 5,           // weight == 0
+    BAD_SYM = 1u << 6,         // GRAPE_SYMMETRIC asserted but an arc has no reverse
+};
+
+__global__ void check_offsets(const uint64_t* __restrict__ off, uint32_t n, uint64_t m,
+                              unsigned* __restrict__ bad)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v <= n; v += stride) {
+        const uint64_t a = off[v];
+        if (v == 0 && a != 0) atomicOr(bad, BAD_OFF0);
+        if (v == n && a != m) atomicOr(bad, BAD_OFFN);
+        if (v < n && a > off[v + 1]) atomicOr(bad, BAD_MONO);
+    }
+}
+
+__global__ void check_rows(const uint64_t* __restrict__ off, const uint32_t* __restrict__ col,
+                           const uint32_t* __restrict__ w, uint32_t n, unsigned* __restrict__ bad)
+{
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned mine = 0;
+    for (uint64_t v = warp; v < n; v += nwarps) {
+        const uint64_t lo = off[v], hi = off[v + 1];
+        for (uint64_t e = lo + lane; e < hi; e += 32) {
+            const uint32_t c = col[e];
+            if (c >= n) mine |= BAD_COL;
+            if (e > lo && col[e - 1] >= c) mine |= BAD_SORT;
+            if (w != nullptr && w[e] == 0) mine |= BAD_W;
+        }
+    }
+    if (mine) atomicOr(bad, mine);
+}
+
+// Every arc v -> u needs u -> v: binary search of v in row u.
+__global__ void check_symmetric(const uint64_t* __restrict__ off, const uint32_t* __restrict__ col,
+                                uint32_t n, unsigned* __restrict__ bad)
+{
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    bool ok = true;
+    for (uint64_t v = warp; v < n; v += nwarps) {
+        const uint64_t lo = off[v], hi = off[v + 1];
+        for (uint64_t e = lo + lane; e < hi; e += 32) {
+            const uint32_t u = col[e];
+            uint64_t a = off[u], b = off[u + 1];
+            while (a < b) {
+                const uint64_t mid = a + ((b - a) >> 1);
+                if (col[mid] < (uint32_t)v) a = mid + 1; else b = mid;
+            }
+            if (a == off[u + 1] || col[a] != (uint32_t)v) ok = false;
+        }
+    }
+    if (!ok) atomicOr(bad, BAD_SYM);
+}
+
+// Row sums (W_v) and degrees -> maxima.
+__global__ void row_stats(const uint64_t* __restrict__ off, const uint32_t* __restrict__ w, uint32_t n,
+                          unsigned long long* __restrict__ max_w, unsigned* __restrict__ max_deg)
+{
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned long long wmax = 0;
+    unsigned dmax = 0;
+    for (uint64_t v = warp; v < n; v += nwarps) {
+        const uint64_t lo = off[v], hi = off[v + 1];
+        unsigned long long s = 0;
+        if (w != nullptr)
+            for (uint64_t e = lo + lane; e < hi; e += 32) s += w[e];
+        else if (lane == 0)
+            s = hi - lo;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (s > wmax) wmax = s;
+        const uint64_t d = hi - lo;
+        if (d > dmax) dmax = (unsigned)(d > 0xFFFFFFFFull ? 0xFFFFFFFFull : d);
+    }
+    if (lane == 0) {
+        atomicMax(max_w, wmax);
+        atomicMax(max_deg, dmax);
+    }
+}
+
+// Row-local inclusive prefix sums: one warp per row, 32 arcs per iteration,
+// shuffle scan + running carry.
+template <typename CW>
+__global__ void row_prefix(const uint64_t* __restrict__ off, const uint32_t* __restrict__ w, uint32_t n,
+                           CW* __restrict__ cw)
+{
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t v = warp; v < n; v += nwarps) {
+        const uint64_t lo = off[v], hi = off[v + 1];
+        uint64_t carry = 0;
+        for (uint64_t b = lo; b < hi; b += 32) {
+            const uint64_t e = b + lane;
+            uint64_t x = e < hi ? (uint64_t)w[e] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if ((int)lane >= o) x += y;
+            }
+            if (e < hi) cw[e] = (CW)(carry + x);
+            carry += __shfl_sync(0xffffffffu, x, 31);
+        }
+    }
+}
+
+int grid_for(uint64_t items_per_warp_rows)
+{
+    uint64_t blocks = (items_per_warp_rows + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    if (blocks < 1) blocks = 1;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    return (int)blocks;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) { cudaGetDevice(&prev); cudaSetDevice(dev); }
+    ~DeviceGuard() { if (prev >= 0) cudaSetDevice(prev); }
+};
+
+}  // namespace
+
+void destroy_graph(grape_graph* g)
+{
+    if (!g) return;
+    cudaFree(g->off);
+    cudaFree(g->col);
+    cudaFree(g->cw);
+    delete g;
+}
+
+grape_status build_graph(uint32_t n, uint64_t m, const uint64_t* off_in, const uint32_t* col_in,
+                         const uint32_t* w_in, int device, uint32_t flags, grape_graph** out)
+{
+    DeviceGuard guard(device);
+    cudaError_t e = cudaGetLastError();  // clear stale errors
+    grape_graph* g = new grape_graph();
+    std::memset(g, 0, sizeof(*g));
+    g->device = device;
+    g->n = n;
+    g->m = m;
+    g->flags = flags & (GRAPE_SYMMETRIC);
+    uint32_t* w = nullptr;
+    unsigned* d_bad = nullptr;
+    unsigned long long* d_maxw = nullptr;
+    unsigned* d_maxdeg = nullptr;
+    grape_status st = GRAPE_OK;
+    auto fail = [&](grape_status s) {
+        cudaFree(w);
+        cudaFree(d_bad);
+        cudaFree(d_maxw);
+        cudaFree(d_maxdeg);
+        destroy_graph(g);
+        *out = nullptr;
+        return s;
+    };
+#define GRAPE_TRY_ALLOC(ptr, bytes)                                                        \
+    do {                                                                                    \
+        e = cudaMalloc((void**)&(ptr), (bytes) ? (bytes) : 4);                              \
+        if (e != cudaSuccess) {                                                             \
+            cudaGetLastError();                                                             \
+            set_error("cudaMalloc of %llu bytes failed: %s", (unsigned long long)(bytes),   \
+                      cudaGetErrorString(e));                                               \
+            return fail(GRAPE_ENOMEM);                                                      \
+        }                                                                                   \
+    } while (0)
+#define GRAPE_TRY_CUDA(call, what)                                                         \
+    do {                                                                                    \
+        e = (call);                                                                         \
+        if (e != cudaSuccess) return fail(cuda_fail(e, what));                              \
+    } while (0)
+
+    GRAPE_TRY_ALLOC(g->off, (n + 1ull) * 8);
+    GRAPE_TRY_ALLOC(g->col, m * 4);
+    GRAPE_TRY_ALLOC(d_bad, 4);
+    GRAPE_TRY_ALLOC(d_maxw, 8);
+    GRAPE_TRY_ALLOC(d_maxdeg, 4);
+    GRAPE_TRY_CUDA(cudaMemcpy(g->off, off_in, (n + 1ull) * 8, cudaMemcpyDefault), "copy row_offsets");
+    if (m) GRAPE_TRY_CUDA(cudaMemcpy(g->col, col_in, m * 4, cudaMemcpyDefault), "copy col_indices");
+    if (w_in) {
+        GRAPE_TRY_ALLOC(w, m * 4);
+        if (m) GRAPE_TRY_CUDA(cudaMemcpy(w, w_in, m * 4, cudaMemcpyDefault), "copy weights");
+    }
+    GRAPE_TRY_CUDA(cudaMemset(d_bad, 0, 4), "memset");
+    GRAPE_TRY_CUDA(cudaMemset(d_maxw, 0, 8), "memset");
+    GRAPE_TRY_CUDA(cudaMemset(d_maxdeg, 0, 4), "memset");
+
+    const int rows_grid = grid_for(n);
+    unsigned bad = 0;
+    if (!(flags & GRAPE_SKIP_VALIDATION)) {
+        int g1 = (int)((n + 1ull + kThreads - 1) / kThreads);
+        if (g1 > 148 * 32) g1 = 148 * 32;
+        check_offsets<<<g1, kThreads>>>(g->off, n, m, d_bad);
+        GRAPE_TRY_CUDA(cudaMemcpy(&bad, d_bad, 4, cudaMemcpyDeviceToHost), "validate offsets");
+        if (!bad) {
+            check_rows<<<rows_grid, kThreads>>>(g->off, g->col, w, n, d_bad);
+            if (flags & GRAPE_SYMMETRIC) check_symmetric<<<rows_grid, kThreads>>>(g->off, g->col, n, d_bad);
+            GRAPE_TRY_CUDA(cudaMemcpy(&bad, d_bad, 4, cudaMemcpyDeviceToHost), "validate rows");
+        }
+        if (bad) {
+            const char* what = (bad & BAD_OFF0)   ? "row_offsets[0] != 0"
+                               : (bad & BAD_OFFN) ? "row_offsets[num_nodes] != num_arcs"
+                               : (bad & BAD_MONO) ? "row_offsets decrease"
+                               : (bad & BAD_COL)  ? "a col_indices value >= num_nodes"
+                               : (bad & BAD_SORT) ? "a row of col_indices is not strictly increasing (unsorted or duplicate arc)"
+                               : (bad & BAD_W)    ? "a weight is 0 (weights must be >= 1)"
+                                                  : "GRAPE_SYMMETRIC asserted but an arc has no reverse arc";
+            set_error("invalid CSR: %s", what);
+            return fail(GRAPE_EINVAL);
+        }
+    }
+    row_stats<<<rows_grid, kThreads>>>(g->off, w, n, d_maxw, d_maxdeg);
+    unsigned long long maxw = 0;
+    unsigned maxdeg = 0;
+    GRAPE_TRY_CUDA(cudaMemcpy(&maxw, d_maxw, 8, cudaMemcpyDeviceToHost), "row stats");
+    GRAPE_TRY_CUDA(cudaMemcpy(&maxdeg, d_maxdeg, 4, cudaMemcpyDeviceToHost), "row stats");
+    g->max_row_weight = maxw;
+    g->max_degree = maxdeg;
+    if (w) {
+        if (maxw < (1ull << 32)) {
+            g->cw_bytes = 4;
+            GRAPE_TRY_ALLOC(g->cw, m * 4);
+            row_prefix<uint32_t><<<rows_grid, kThreads>>>(g->off, w, n, (uint32_t*)g->cw);
+        } else {
+            g->cw_bytes = 8;
+            GRAPE_TRY_ALLOC(g->cw, m * 8);
+            row_prefix<uint64_t><<<rows_grid, kThreads>>>(g->off, w, n, (uint64_t*)g->cw);
+        }
+        GRAPE_TRY_CUDA(cudaGetLastError(), "prefix kernel launch");
+    }
+    GRAPE_TRY_CUDA(cudaDeviceSynchronize(), "graph build");
+    cudaFree(w);
+    w = nullptr;
+    cudaFree(d_bad);
+    cudaFree(d_maxw);
+    cudaFree(d_maxdeg);
+    d_bad = nullptr; d_maxw = nullptr; d_maxdeg = nullptr;
+    g->device_bytes = (n + 1ull) * 8 + m * 4 + m * g->cw_bytes;
+    *out = g;
+    (void)st;
+    return GRAPE_OK;
+#undef GRAPE_TRY_ALLOC
+#undef GRAPE_TRY_CUDA
+}
+
+}  // namespace grape

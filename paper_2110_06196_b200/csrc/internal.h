@@ -1,0 +1,53 @@
+// internal.h — structures shared by the CUDA translation units of libgrape_walk.
+// Not part of the ABI (the ABI is include/grape_walk.h).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "grape_walk.h"
+
+struct grape_graph {
+    int device;
+    uint32_t n;
+    uint64_t m;
+    uint64_t* off;        // u64[n+1]
+    uint32_t* col;        // u32[m], rows strictly increasing
+    void* cw;             // row-local inclusive weight prefix: u32[m] or u64[m]; NULL if unweighted
+    uint32_t cw_bytes;    // 0, 4 or 8
+    uint32_t flags;       // GRAPE_SYMMETRIC ...
+    uint32_t max_degree;
+    uint64_t max_row_weight;
+    uint64_t device_bytes;
+};
+
+namespace grape {
+
+// Thread-local error message (capi.cu).
+void set_error(const char* fmt, ...);
+grape_status cuda_fail(cudaError_t e, const char* what);
+
+// Node2vec acceptance thresholds (T_p, T_1, T_q), computed on the host (capi.cu).
+struct Thresholds {
+    uint64_t Tp, T1, Tq;
+};
+
+struct WalkArgs {
+    const uint32_t* starts;
+    uint64_t num_walks;
+    uint64_t walk_id_base;
+    uint32_t L;
+    uint64_t seed;
+    uint32_t* out;
+    unsigned long long* steps_out;   // device, may be NULL
+};
+
+// walk.cu: launch one walk kernel (device buffers) on `stream`.
+// node2vec == false -> first order.  Returns cudaGetLastError() of the launch.
+cudaError_t launch_walks(const grape_graph* g, const WalkArgs& a, bool node2vec,
+                         const Thresholds& T, cudaStream_t stream);
+
+// graph.cu
+grape_status build_graph(uint32_t n, uint64_t m, const uint64_t* off, const uint32_t* col,
+                         const uint32_t* w, int device, uint32_t flags, grape_graph** out);
+void destroy_graph(grape_graph* g);
+
+}  // namespace grape

@@ -1,0 +1,225 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the CPU oracle, bit for bit.
+
+Walk matrices are integer work, so the bar is bit-exact equality of every
+compared row plus the realised-step counter.
+"""
+import numpy as np
+import pytest
+import torch
+
+from graphgen import CSR, config_graph, config_walks, tiny_graph, starts_per_node
+from oracle.oracle import Oracle
+
+pytestmark = pytest.mark.gpu
+
+PAD = 0xFFFFFFFF
+
+
+@pytest.fixture(scope="module")
+def grape():
+    assert torch.cuda.is_available(), "gpu tests need a CUDA device"
+    import paper_2110_06196_b200 as grape
+    return grape
+
+
+def _dev_graph(grape, g: CSR, symmetric=None):
+    sym = g.symmetric if symmetric is None else symmetric
+    return grape.graph_from_csr(g.off, g.col, g.w, device=0, symmetric=sym)
+
+
+def _run(grape, dg, starts, L, mode, p, q, seed, base=0):
+    st = torch.as_tensor(np.asarray(starts, dtype=np.uint32).view(np.int32)).cuda()
+    steps = torch.zeros(1, dtype=torch.int64, device="cuda")
+    if mode == "first_order":
+        out = grape.walks_first_order(dg, st, L, seed=seed, walk_id_base=base, steps=steps)
+    else:
+        out = grape.walks_node2vec(dg, st, L, p, q, seed=seed, walk_id_base=base, steps=steps)
+    torch.cuda.synchronize()
+    return out.cpu().numpy().view(np.uint32), int(steps.item())
+
+
+def _oracle(g: CSR):
+    return Oracle(*g.numpy())
+
+
+def test_cfg1_every_walk_bit_exact(grape):
+    """configs[0]: Chung-Lu 10k nodes, first-order, 1 walk/node, L=32, seed 42 — all walks."""
+    g = config_graph(1)
+    wk = config_walks(1)
+    starts = starts_per_node(g.n, wk["walks_per_node"]).numpy().view(np.uint32)
+    dg = _dev_graph(grape, g)
+    got, steps = _run(grape, dg, starts, wk["L"], wk["mode"], 1, 1, wk["seed"])
+    exp, esteps = _oracle(g).walks(starts, wk["L"], mode=wk["mode"], seed=wk["seed"])
+    assert np.array_equal(got, exp)
+    assert steps == esteps
+    # node2vec on the same graph (unweighted, symmetric), all walks
+    for p, q in [(0.5, 2.0), (1.0, 0.25), (4.0, 1.0)]:
+        got, steps = _run(grape, dg, starts, 32, "node2vec", p, q, 7)
+        exp, esteps = _oracle(g).walks(starts, 32, mode="node2vec", p=p, q=q, seed=7)
+        assert np.array_equal(got, exp), (p, q)
+        assert steps == esteps
+
+
+FUZZ = [(s, n, d, directed, weighted) for s, (n, d, directed, weighted) in enumerate([
+    (1, 0.0, False, False), (2, 1.0, False, True), (7, 0.4, True, False), (30, 0.15, False, True),
+    (30, 0.15, True, True), (64, 0.05, True, False), (200, 0.03, False, False), (200, 0.03, False, True),
+    (300, 0.02, True, True), (97, 0.3, False, True)])]
+
+
+@pytest.mark.parametrize("seed,n,dens,directed,weighted", FUZZ)
+@pytest.mark.parametrize("mode,p,q", [("first_order", 1, 1), ("node2vec", 0.5, 2.0), ("node2vec", 2.0, 0.5),
+                                      ("node2vec", 1.0, 0.25), ("node2vec", 0.25, 4.0), ("node2vec", 4.0, 1.0),
+                                      ("node2vec", 1.0, 1.0), ("node2vec", 0.3, 3.0)])
+def test_fuzz_graphs_every_walk(grape, seed, n, dens, directed, weighted, mode, p, q):
+    g = tiny_graph(1000 + seed, n, dens, directed=directed, weighted=weighted, self_loops=directed)
+    starts = np.concatenate([np.arange(n), np.arange(n)[::-1], [n, n + 1, 2 ** 32 - 2, 2 ** 32 - 1]])
+    starts = starts.astype(np.uint32)
+    o = _oracle(g)
+    for L in (1, 2, 3, 17, 64):
+        exp, esteps = o.walks(starts, L, mode=mode, p=p, q=q, seed=seed, base=3 * seed)
+        for sym in ([False, True] if not directed else [False]):
+            dg = _dev_graph(grape, g, symmetric=sym)
+            got, steps = _run(grape, dg, starts, L, mode, p, q, seed, base=3 * seed)
+            assert np.array_equal(got, exp), (L, sym)
+            assert steps == esteps
+
+
+def test_u64_prefix_path(grape):
+    """Row sums >= 2^32 force the u64 prefix layout; results stay bit-exact."""
+    g = tiny_graph(5, 40, 0.5, weighted=True)
+    rng = np.random.default_rng(0)
+    w = rng.integers(2 ** 30, 2 ** 32 - 1, g.m, dtype=np.uint64).astype(np.uint32)
+    # keep it symmetric-weighted is not required for correctness
+    g.w = torch.from_numpy(w.view(np.int32))
+    dg = _dev_graph(grape, g)
+    assert dg.info["cw_bytes"] == 8
+    starts = np.arange(g.n, dtype=np.uint32)
+    for mode, p, q in [("first_order", 1, 1), ("node2vec", 0.5, 2.0), ("node2vec", 1.0, 0.25)]:
+        got, steps = _run(grape, dg, starts, 50, mode, p, q, 11)
+        exp, esteps = _oracle(g).walks(starts, 50, mode=mode, p=p, q=q, seed=11)
+        assert np.array_equal(got, exp)
+        assert steps == esteps
+
+
+def test_edge_cases(grape):
+    g = tiny_graph(9, 20, 0.1, directed=True, weighted=True)
+    dg = _dev_graph(grape, g)
+    # num_walks = 0
+    out = grape.walks_node2vec(dg, torch.empty(0, dtype=torch.int32, device="cuda"), 5, 0.5, 2.0)
+    assert out.shape == (0, 5)
+    # all starts invalid -> all PAD
+    got, steps = _run(grape, dg, [20, 21, 2 ** 32 - 1], 7, "node2vec", 0.5, 2.0, 1)
+    assert np.all(got == PAD) and steps == 0
+    # a graph with no arcs: every row is [start, PAD, ...]
+    e = CSR(5, torch.zeros(6, dtype=torch.int64), torch.zeros(0, dtype=torch.int32), None, True)
+    de = _dev_graph(grape, e)
+    got, steps = _run(grape, de, np.arange(5), 4, "node2vec", 2.0, 0.5, 1)
+    assert np.all(got[:, 0] == np.arange(5)) and np.all(got[:, 1:] == PAD) and steps == 0
+
+
+def test_host_buffer_path_equals_device_path(grape):
+    g = config_graph(2, scale_down=6)
+    dg = _dev_graph(grape, g)
+    starts = starts_per_node(g.n, 3)
+    dev = grape.walks_node2vec(dg, starts.cuda(), 40, 0.5, 2.0, seed=42, walk_id_base=17)
+    steps = torch.zeros(1, dtype=torch.int64)
+    host = grape.walks_node2vec(dg, starts, 40, 0.5, 2.0, seed=42, walk_id_base=17, steps=steps)
+    assert not host.is_cuda
+    assert torch.equal(dev.cpu(), host)
+    dsteps = torch.zeros(1, dtype=torch.int64, device="cuda")
+    grape.walks_node2vec(dg, starts.cuda(), 40, 0.5, 2.0, seed=42, walk_id_base=17, steps=dsteps)
+    assert int(dsteps.item()) == int(steps.item())
+
+
+def test_sharding_and_determinism(grape):
+    """Rank slices [r W/G, (r+1) W/G) with walk_id_base = slice start reproduce the
+    single call bit for bit; re-running is deterministic."""
+    g = config_graph(2, scale_down=5)
+    dg = _dev_graph(grape, g)
+    starts = starts_per_node(g.n, 2).cuda()
+    W = starts.numel()
+    full = grape.walks_node2vec(dg, starts, 30, 0.5, 2.0, seed=42)
+    again = grape.walks_node2vec(dg, starts, 30, 0.5, 2.0, seed=42)
+    assert torch.equal(full, again)
+    for G in (2, 3, 8):
+        parts = []
+        for r in range(G):
+            lo, hi = r * W // G, (r + 1) * W // G
+            parts.append(grape.walks_node2vec(dg, starts[lo:hi], 30, 0.5, 2.0, seed=42, walk_id_base=lo))
+        assert torch.equal(torch.cat(parts), full)
+
+
+def test_specialisation_identities(grape):
+    g = config_graph(1)
+    dg = _dev_graph(grape, g)
+    dn = _dev_graph(grape, g, symmetric=False)
+    ones = CSR(g.n, g.off, g.col, torch.ones(g.m, dtype=torch.int32), True)
+    dw = _dev_graph(grape, ones)
+    starts = starts_per_node(g.n, 1).cuda()
+    a = grape.walks_node2vec(dg, starts, 32, 1.0, 1.0, seed=3)
+    b = grape.walks_first_order(dg, starts, 32, seed=3)
+    assert torch.equal(a, b)
+    for p, q in [(0.5, 2.0), (1.0, 0.25), (2.0, 1.0)]:
+        x = grape.walks_node2vec(dg, starts, 32, p, q, seed=3)
+        y = grape.walks_node2vec(dn, starts, 32, p, q, seed=3)   # no symmetric trick
+        z = grape.walks_node2vec(dw, starts, 32, p, q, seed=3)   # weighted, all ones
+        assert torch.equal(x, y) and torch.equal(x, z)
+
+
+@pytest.mark.parametrize("k", [2])
+def test_full_size_config_sampled(grape, k):
+    """BASELINE configs[1] at full size, in bench.py's launch configuration (one
+    call over all walks): a seeded sample of walks recomputed by the oracle one
+    by one (the counter-based RNG makes walk i a function of (seed, wid) alone)."""
+    g = config_graph(k, device="cuda")
+    wk = config_walks(k)
+    dg = _dev_graph(grape, g)
+    starts = starts_per_node(g.n, wk["walks_per_node"], device="cuda")
+    steps = torch.zeros(1, dtype=torch.int64, device="cuda")
+    out = grape.walks_node2vec(dg, starts, wk["L"], wk["p"], wk["q"], seed=wk["seed"], steps=steps)
+    torch.cuda.synchronize()
+    o = _oracle(g.to("cpu"))
+    W = starts.numel()
+    rng = np.random.default_rng(k)
+    # hubs and random walks: wids whose start is one of the 50 highest-degree nodes + random sample
+    deg = (g.off[1:] - g.off[:-1]).cpu()
+    hubs = torch.topk(deg, 50).indices.numpy()
+    sample = np.unique(np.concatenate([rng.integers(0, W, 1500), hubs, hubs + g.n, [0, W - 1]]))
+    host_out = out.cpu().numpy().view(np.uint32)
+    st_np = starts.cpu().numpy().view(np.uint32)
+    for i in sample:
+        exp, _ = o.walks(st_np[i:i + 1], wk["L"], mode=wk["mode"], p=wk["p"], q=wk["q"],
+                         seed=wk["seed"], base=int(i))
+        assert np.array_equal(host_out[i], exp[0]), i
+    # counter vs the matrix itself
+    realised = int(np.sum(host_out != PAD)) - int(np.sum(host_out[:, 0] != PAD))
+    assert realised == int(steps.item())
+
+
+def test_invalid_inputs_rejected(grape):
+    good = tiny_graph(3, 10, 0.3)
+    off, col = good.off.clone(), good.col.clone()
+    with pytest.raises(grape.GrapeError) as ei:
+        grape.graph_from_csr(off, col.flip(0))            # unsorted rows
+    assert ei.value.status == grape.GRAPE_EINVAL
+    bad = col.clone(); bad[0] = 10
+    with pytest.raises(grape.GrapeError):
+        grape.graph_from_csr(off, bad)                     # col >= n
+    bad_off = off.clone(); bad_off[-1] += 1
+    with pytest.raises(grape.GrapeError):
+        grape.graph_from_csr(bad_off, col)                 # off[n] != m
+    w = torch.ones(good.m, dtype=torch.int32); w[3] = 0
+    with pytest.raises(grape.GrapeError):
+        grape.graph_from_csr(off, col, w)                  # weight 0
+    d = tiny_graph(4, 10, 0.3, directed=True)
+    with pytest.raises(grape.GrapeError):
+        grape.graph_from_csr(d.off, d.col, symmetric=True)   # asymmetric with SYMMETRIC
+    dg = grape.graph_from_csr(off, col, symmetric=True)
+    st = torch.arange(10, dtype=torch.int32, device="cuda")
+    for p, q in [(0.0, 1.0), (1.0, -2.0), (float("nan"), 1.0), (2.0 ** 25, 1.0)]:
+        with pytest.raises(grape.GrapeError):
+            grape.walks_node2vec(dg, st, 5, p, q)
+    with pytest.raises(grape.GrapeError):
+        grape.walks_node2vec(dg, st, 0, 1.0, 1.0)
+    with pytest.raises(grape.GrapeError):   # host starts with a device out
+        grape.walks_node2vec(dg, st.cpu(), 5, 1.0, 1.0, out=torch.empty(10, 5, dtype=torch.int32, device="cuda"))

@@ -1,0 +1,82 @@
+"""The seeded input generators: deterministic, well-formed CSR, the stated shapes."""
+import numpy as np
+import pytest
+import torch
+
+from graphgen import chung_lu, rmat, tiny_graph, config_graph, starts_per_node, splitmix64
+
+
+def _check_csr(g, symmetric):
+    n, off, col, w = g.numpy()
+    assert off[0] == 0 and off[-1] == len(col)
+    assert np.all(off[1:] >= off[:-1])
+    assert np.all(col < n)
+    rows = np.repeat(np.arange(n), np.diff(off).astype(np.int64))
+    assert not np.any(rows == col), "self-loop"
+    same = rows[1:] == rows[:-1]
+    assert np.all(col[1:][same] > col[:-1][same]), "unsorted or duplicate"
+    if symmetric:
+        fwd = set(zip(rows.tolist(), col.tolist()))
+        assert all((b, a) in fwd for a, b in fwd)
+        if w is not None:
+            wd = dict(zip(zip(rows.tolist(), col.tolist()), w.tolist()))
+            assert all(wd[(a, b)] == wd[(b, a)] for a, b in wd)
+    if w is not None:
+        assert np.all(w >= 1)
+
+
+def test_splitmix64_reference_values():
+    # splitmix64 finaliser applied to 0 and 1 after the golden-gamma increment,
+    # computed here with Python integers
+    def ref(x):
+        x = (x + 0x9E3779B97F4A7C15) & (2 ** 64 - 1)
+        x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & (2 ** 64 - 1)
+        x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & (2 ** 64 - 1)
+        return x ^ (x >> 31)
+    xs = [0, 1, 2 ** 63, 2 ** 64 - 1, 12345678901234]
+    t = torch.tensor([v - 2 ** 64 if v >= 2 ** 63 else v for v in xs], dtype=torch.int64)
+    got = [int(v) & (2 ** 64 - 1) for v in splitmix64(t)]
+    assert got == [ref(v) for v in xs]
+
+
+def test_chung_lu_small_is_valid_and_deterministic():
+    a = chung_lu(3000, 30000, seed=9, weights=100)
+    b = chung_lu(3000, 30000, seed=9, weights=100, chunk=7777)   # chunking must not matter
+    _check_csr(a, True)
+    assert torch.equal(a.off, b.off) and torch.equal(a.col, b.col) and torch.equal(a.w, b.w)
+    assert 0.9 * 2 * 30000 < a.m <= 2 * 30000
+    w = a.w.numpy()
+    assert 1 <= w.min() and w.max() <= 100 and abs(w.mean() - 50.5) < 2
+    deg = np.diff(a.off.numpy())
+    assert deg.max() > 20 * deg.mean()          # power-law hubs
+    c = chung_lu(3000, 30000, seed=10, weights=100)
+    assert not torch.equal(a.col[:100], c.col[:100])
+
+
+def test_rmat_small_is_valid():
+    g = rmat(12, 8, seed=3, symmetric=True)
+    _check_csr(g, True)
+    d = rmat(12, 8, seed=5, symmetric=False, weights=("geometric", 10.0))
+    _check_csr(d, False)
+    w = d.w.numpy()
+    assert abs(w.mean() - 10.0) < 0.5 and w.min() == 1
+    # geometric: P(w=1) = 0.1
+    assert abs(np.mean(w == 1) - 0.1) < 0.01
+    deg = np.diff(g.off.numpy())
+    assert deg.max() > 30 * max(deg.mean(), 1)
+
+
+def test_config1_shape():
+    g = config_graph(1)
+    _check_csr(g, True)
+    assert g.n == 10_000 and 180_000 < g.m < 200_000 and g.w is None
+
+
+def test_starts_iteration_major():
+    s = starts_per_node(4, 3)
+    assert s.tolist() == [0, 1, 2, 3] * 3
+
+
+def test_tiny_graph_directed_has_sinks():
+    g = tiny_graph(1, 30, 0.03, directed=True)
+    assert np.any(np.diff(g.off.numpy()) == 0)
