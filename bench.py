@@ -276,7 +276,7 @@ def run_ours(args):
     # ---- CPU oracle baseline (rank 0, N = 1 only) and the roofline model
     cpu = None
     att_per_step = None
-    if rank == 0:
+    if rank == 0 and not args.no_cpu:
         g_cpu = g.to("cpu")
         budget = args.cpu_budget if world == 1 else 2.0
         s, secs, walks, cores, att = _oracle_sample(g_cpu, wk, budget)
@@ -330,6 +330,7 @@ def main():
     ap.add_argument("--traffic-per-launch", type=float, default=None,
                     help="ncu dram bytes per launch of the walk kernel (from profiles/)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the oracle baseline (profiling runs)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

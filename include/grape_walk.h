@@ -132,8 +132,9 @@ grape_status grape_graph_get_info(const grape_graph* g, grape_graph_info* info);
  * through device memory, overlapping H2D / kernel / D2H, and the call returns
  * when out (and *steps_out) are complete.  Mixing host and device for starts
  * and out is EINVAL.
- * Errors: EINVAL (NULL g/starts/out, L = 0, num_walks * L overflow, wrong
- * current device); ENOMEM (staging); ECUDA (launch).
+ * Errors: EINVAL (NULL g, NULL starts/out with num_walks > 0, L = 0,
+ * num_walks * L overflow, wrong current device); ENOMEM (staging); ECUDA
+ * (launch).  With num_walks = 0 the buffers may be NULL.
  */
 grape_status grape_walks_first_order(const grape_graph* g, const uint32_t* starts,
                                      uint64_t num_walks, uint64_t walk_id_base,

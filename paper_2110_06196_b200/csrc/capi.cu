@@ -151,7 +151,7 @@ grape_status walks_common(const grape_graph* g, const uint32_t* starts, uint64_t
                           uint32_t* out, uint64_t* steps_out, cudaStream_t stream)
 {
     g_err[0] = 0;
-    if (g == nullptr || starts == nullptr || out == nullptr) {
+    if (g == nullptr || (num_walks > 0 && (starts == nullptr || out == nullptr))) {
         set_error("graph, starts and out must be non-NULL");
         return GRAPE_EINVAL;
     }
