@@ -45,7 +45,10 @@ class GrapeError(RuntimeError):
         self.status = status
 
 
-def load(path: str = LIB_PATH) -> ctypes.CDLL:
+def load(path: str | None = None) -> ctypes.CDLL:
+    # GRAPE_WALK_LIB: an alternative in-tree build of the same library (used by
+    # tools/ experiments to compare compile-time variants); default LIB_PATH.
+    path = path or os.environ.get("GRAPE_WALK_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise ImportError(
             f"{path} is missing: build the CUDA library first (`make` or "

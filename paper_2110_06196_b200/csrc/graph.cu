@@ -10,6 +10,7 @@
 // grid-stride over rows, so hub rows are scanned by a whole warp.
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include "internal.h"
 
 namespace grape {
@@ -136,6 +137,35 @@ __global__ void row_prefix(const uint64_t* __restrict__ off, const uint32_t* __r
     }
 }
 
+// Node records: {row start, degree, W_v if it fits 32 bits}.
+template <typename CW>
+__global__ void build_nodes(const uint64_t* __restrict__ off, const CW* __restrict__ cw, uint32_t n,
+                            NodeRec* __restrict__ nodes)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
+        const uint64_t a = off[v], d = off[v + 1] - a;
+        NodeRec r;
+        r.start = a;
+        r.deg = (uint32_t)d;
+        if (cw == nullptr) r.w32 = (uint32_t)d;
+        else if (sizeof(CW) == 4) r.w32 = d ? (uint32_t)cw[a + d - 1] : 0u;
+        else r.w32 = 0u;
+        nodes[v] = r;
+    }
+}
+
+// Fence level: dst[k] = src[k*B + B - 1] for every full 32-byte block k of src.
+template <typename T>
+__global__ void build_fence(const T* __restrict__ src, uint64_t nsrc, T* __restrict__ dst)
+{
+    constexpr uint64_t B = 32 / sizeof(T);
+    const uint64_t nd = nsrc / B;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nd; k += stride)
+        dst[k] = src[k * B + B - 1];
+}
+
 int grid_for(uint64_t items_per_warp_rows)
 {
     uint64_t blocks = (items_per_warp_rows + kWarpsPerBlock - 1) / kWarpsPerBlock;
@@ -143,6 +173,10 @@ int grid_for(uint64_t items_per_warp_rows)
     if (blocks > 148 * 32) blocks = 148 * 32;
     return (int)blocks;
 }
+
+// Allocation size rounded up to whole 32-byte sectors plus one spare sector, so
+// an aligned sector load of the last (partial) block never leaves the buffer.
+uint64_t padded(uint64_t bytes) { return ((bytes + 31) / 32) * 32 + 32; }
 
 struct DeviceGuard {
     int prev = -1;
@@ -158,6 +192,11 @@ void destroy_graph(grape_graph* g)
     cudaFree(g->off);
     cudaFree(g->col);
     cudaFree(g->cw);
+    cudaFree(g->nodes);
+    for (int l = 0; l < kFenceLevels; ++l) {
+        cudaFree(g->col_fence[l]);
+        cudaFree(g->cw_fence[l]);
+    }
     delete g;
 }
 
@@ -177,6 +216,7 @@ grape_status build_graph(uint32_t n, uint64_t m, const uint64_t* off_in, const u
     unsigned long long* d_maxw = nullptr;
     unsigned* d_maxdeg = nullptr;
     grape_status st = GRAPE_OK;
+    uint64_t fence_bytes = 0;
     auto fail = [&](grape_status s) {
         cudaFree(w);
         cudaFree(d_bad);
@@ -203,7 +243,8 @@ grape_status build_graph(uint32_t n, uint64_t m, const uint64_t* off_in, const u
     } while (0)
 
     GRAPE_TRY_ALLOC(g->off, (n + 1ull) * 8);
-    GRAPE_TRY_ALLOC(g->col, m * 4);
+    GRAPE_TRY_ALLOC(g->col, padded(m * 4));
+    GRAPE_TRY_CUDA(cudaMemset(g->col, 0, padded(m * 4)), "memset");
     GRAPE_TRY_ALLOC(d_bad, 4);
     GRAPE_TRY_ALLOC(d_maxw, 8);
     GRAPE_TRY_ALLOC(d_maxdeg, 4);
@@ -251,14 +292,58 @@ grape_status build_graph(uint32_t n, uint64_t m, const uint64_t* off_in, const u
     if (w) {
         if (maxw < (1ull << 32)) {
             g->cw_bytes = 4;
-            GRAPE_TRY_ALLOC(g->cw, m * 4);
+            GRAPE_TRY_ALLOC(g->cw, padded(m * 4));
+            GRAPE_TRY_CUDA(cudaMemset(g->cw, 0, padded(m * 4)), "memset");
             row_prefix<uint32_t><<<rows_grid, kThreads>>>(g->off, w, n, (uint32_t*)g->cw);
         } else {
             g->cw_bytes = 8;
-            GRAPE_TRY_ALLOC(g->cw, m * 8);
+            GRAPE_TRY_ALLOC(g->cw, padded(m * 8));
+            GRAPE_TRY_CUDA(cudaMemset(g->cw, 0, padded(m * 8)), "memset");
             row_prefix<uint64_t><<<rows_grid, kThreads>>>(g->off, w, n, (uint64_t*)g->cw);
         }
         GRAPE_TRY_CUDA(cudaGetLastError(), "prefix kernel launch");
+    }
+    {
+        int gn = (int)((n + 255ull) / 256);
+        if (gn > 148 * 32) gn = 148 * 32;
+        if (gn < 1) gn = 1;
+        GRAPE_TRY_ALLOC(g->nodes, (uint64_t)n * sizeof(NodeRec));
+        if (g->cw_bytes == 4)
+            build_nodes<uint32_t><<<gn, 256>>>(g->off, (const uint32_t*)g->cw, n, g->nodes);
+        else if (g->cw_bytes == 8)
+            build_nodes<uint64_t><<<gn, 256>>>(g->off, (const uint64_t*)g->cw, n, g->nodes);
+        else
+            build_nodes<uint32_t><<<gn, 256>>>(g->off, nullptr, n, g->nodes);
+        GRAPE_TRY_CUDA(cudaGetLastError(), "node records");
+        fence_bytes = 0;
+        uint64_t len = m;
+        for (int l = 0; l < kFenceLevels; ++l) {
+            len /= 8;
+            GRAPE_TRY_ALLOC(g->col_fence[l], padded(len * 4));
+            GRAPE_TRY_CUDA(cudaMemset(g->col_fence[l], 0, padded(len * 4)), "memset");
+            fence_bytes += padded(len * 4);
+            const uint32_t* src = l == 0 ? g->col : g->col_fence[l - 1];
+            build_fence<uint32_t><<<grid_for(len / 8 + 1), kThreads>>>(src, len * 8, g->col_fence[l]);
+        }
+        if (g->cw_bytes) {
+            const uint64_t B = 32 / g->cw_bytes;
+            len = m;
+            for (int l = 0; l < kFenceLevels; ++l) {
+                len /= B;
+                GRAPE_TRY_ALLOC(g->cw_fence[l], padded(len * g->cw_bytes));
+                GRAPE_TRY_CUDA(cudaMemset(g->cw_fence[l], 0, padded(len * g->cw_bytes)), "memset");
+                fence_bytes += padded(len * g->cw_bytes);
+                if (g->cw_bytes == 4)
+                    build_fence<uint32_t><<<grid_for(len / 8 + 1), kThreads>>>(
+                        l == 0 ? (const uint32_t*)g->cw : (const uint32_t*)g->cw_fence[l - 1], len * B,
+                        (uint32_t*)g->cw_fence[l]);
+                else
+                    build_fence<uint64_t><<<grid_for(len / 8 + 1), kThreads>>>(
+                        l == 0 ? (const uint64_t*)g->cw : (const uint64_t*)g->cw_fence[l - 1], len * B,
+                        (uint64_t*)g->cw_fence[l]);
+            }
+        }
+        GRAPE_TRY_CUDA(cudaGetLastError(), "fence levels");
     }
     GRAPE_TRY_CUDA(cudaDeviceSynchronize(), "graph build");
     cudaFree(w);
@@ -267,7 +352,8 @@ grape_status build_graph(uint32_t n, uint64_t m, const uint64_t* off_in, const u
     cudaFree(d_maxw);
     cudaFree(d_maxdeg);
     d_bad = nullptr; d_maxw = nullptr; d_maxdeg = nullptr;
-    g->device_bytes = (n + 1ull) * 8 + m * 4 + m * g->cw_bytes;
+    g->device_bytes = (n + 1ull) * 8 + padded(m * 4) + (g->cw_bytes ? padded(m * g->cw_bytes) : 0) +
+                      (uint64_t)n * sizeof(NodeRec) + fence_bytes;
     *out = g;
     (void)st;
     return GRAPE_OK;

@@ -5,14 +5,33 @@
 #include <cuda_runtime.h>
 #include "grape_walk.h"
 
+namespace grape {
+// Fence levels over col and cw: level l+1 holds the last entry of
+// every full 32-byte block of level l, so a search reads one sector per level
+// below a short binary search on the (small, L2-resident) top level.
+constexpr int kFenceLevels = 3;
+
+// Per-node record, one 16-byte load per visited node: row start, degree and the
+// row's total weight W_v when it fits 32 bits (else w32 = 0 and W_v is read
+// from the u64 prefix row).
+struct alignas(16) NodeRec {
+    uint64_t start;
+    uint32_t deg;
+    uint32_t w32;
+};
+}  // namespace grape
+
 struct grape_graph {
     int device;
     uint32_t n;
     uint64_t m;
     uint64_t* off;        // u64[n+1]
-    uint32_t* col;        // u32[m], rows strictly increasing
+    uint32_t* col;        // u32[m], rows strictly increasing (allocation padded to whole sectors)
     void* cw;             // row-local inclusive weight prefix: u32[m] or u64[m]; NULL if unweighted
     uint32_t cw_bytes;    // 0, 4 or 8
+    grape::NodeRec* nodes;                       // [n]
+    uint32_t* col_fence[grape::kFenceLevels];    // col fence levels 1..3
+    void* cw_fence[grape::kFenceLevels];         // cw fence levels 1..3 (cw_bytes each)
     uint32_t flags;       // GRAPE_SYMMETRIC ...
     uint32_t max_degree;
     uint64_t max_row_weight;
@@ -44,6 +63,8 @@ struct WalkArgs {
 // node2vec == false -> first order.  Returns cudaGetLastError() of the launch.
 cudaError_t launch_walks(const grape_graph* g, const WalkArgs& a, bool node2vec,
                          const Thresholds& T, cudaStream_t stream);
+cudaError_t launch_walks_sm(const grape_graph* g, const WalkArgs& a, bool node2vec,
+                            const Thresholds& T, cudaStream_t stream);
 
 // graph.cu
 grape_status build_graph(uint32_t n, uint64_t m, const uint64_t* off, const uint32_t* col,

@@ -1,0 +1,280 @@
+// walk_common.cuh — device building blocks shared by the walk kernels (walk.cu,
+// walk_sm.cu): kernel parameters, cache-policy loads, sector scans, node
+// records and the staged row writer.  Internal to libgrape_walk.
+#pragma once
+#include <cstdint>
+#include <type_traits>
+#include "internal.h"
+#include "philox.cuh"
+
+namespace grape {
+namespace walk {
+
+
+constexpr uint32_t kPad = 0xFFFFFFFFu;
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+constexpr int kBlock = 256;
+#ifndef GRAPE_MIN_BLOCKS
+#define GRAPE_MIN_BLOCKS 4
+#endif
+constexpr int kMinBlocks = GRAPE_MIN_BLOCKS;   // 4 x 256 threads/SM -> <= 64 registers
+constexpr int NL = kFenceLevels;
+
+struct Unweighted {};
+
+template <typename T>
+struct Levels {
+    const T* a[NL + 1];   // a[0] = the array itself, a[1..NL] = its fence levels
+};
+
+template <typename CW>
+using CwStore = typename std::conditional<std::is_same<CW, Unweighted>::value, uint32_t, CW>::type;
+
+// Kernel parameters (constant bank; nothing here occupies registers until used).
+template <typename CW>
+struct Params {
+    const NodeRec* nodes;
+    Levels<uint32_t> col;
+    Levels<CwStore<CW>> cw;
+    uint32_t n;
+    const uint32_t* starts;
+    uint64_t num_walks;
+    uint64_t base;
+    uint32_t L;
+    uint32_t k0, k1;
+    uint32_t* out;
+    unsigned long long* steps_out;
+    // acceptance: u < T  <=>  u <= T - 1  (T in [1, 2^32], so T - 1 fits u32)
+    uint32_t tp_m1, t1_m1, lo_m1, hi_m1;
+    bool member_accepts;   // for u in [T_lo, T_hi): accepted iff (x in N(t)) == (T_1 > T_q)
+};
+
+__device__ __forceinline__ uint4 ldg_v4(const void* p)
+{
+    return __ldg(reinterpret_cast<const uint4*>(p));
+}
+
+// ---- L2 residency: the hot set (node records + fence levels,
+// tens of MB) is loaded with an evict_last policy so that the random stream of
+// cold leaf sectors (col / cw rows, hundreds of MB) cannot flush it; leaf loads
+// take GRAPE_LEAF_HINT (0: default, 1: evict_first, 2: evict_first and no L1
+// allocation).  Policies live in uniform registers (memory descriptors).
+#ifndef GRAPE_HOT_HINT
+#define GRAPE_HOT_HINT 1
+#endif
+#ifndef GRAPE_LEAF_HINT
+#define GRAPE_LEAF_HINT 1
+#endif
+enum Temp { kHot = 0, kLeaf = 1 };
+
+__device__ __forceinline__ uint64_t policy_evict_last()
+{
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_first()
+{
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+template <int TEMP>
+__device__ __forceinline__ uint32_t ld_u32(const uint32_t* p)
+{
+    uint32_t r;
+    if (TEMP == kHot && GRAPE_HOT_HINT == 1) {
+        asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(policy_evict_last()));
+    } else if (TEMP == kLeaf && GRAPE_LEAF_HINT == 1) {
+        asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(policy_evict_first()));
+    } else if (TEMP == kLeaf && GRAPE_LEAF_HINT == 2) {
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(policy_evict_first()));
+    } else {
+        r = __ldg(p);
+    }
+    return r;
+}
+
+template <int TEMP>
+__device__ __forceinline__ uint64_t ld_u64(const uint64_t* p)
+{
+    uint64_t r;
+    if (TEMP == kHot && GRAPE_HOT_HINT == 1) {
+        asm("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(policy_evict_last()));
+    } else if (TEMP == kLeaf && GRAPE_LEAF_HINT >= 1) {
+        asm("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(policy_evict_first()));
+    } else {
+        r = __ldg(p);
+    }
+    return r;
+}
+
+template <typename T, int TEMP>
+__device__ __forceinline__ T ld_elem(const T* p)
+{
+    if constexpr (sizeof(T) == 4) return ld_u32<TEMP>(p);
+    else return ld_u64<TEMP>(p);
+}
+
+// One aligned 32-byte sector in one 256-bit load (LDG.E.ENL2.256 on sm_100a).
+template <int TEMP>
+__device__ __forceinline__ void ld_sector(const void* p, uint32_t (&v)[8])
+{
+#define GRAPE_LD8(QUAL, POL)                                                                              \
+    asm("ld.global.nc" QUAL ".v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"                               \
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]) \
+        : "l"(p), "l"(POL))
+    if (TEMP == kHot && GRAPE_HOT_HINT == 1) {
+        GRAPE_LD8(".L2::cache_hint", policy_evict_last());
+    } else if (TEMP == kLeaf && GRAPE_LEAF_HINT == 1) {
+        GRAPE_LD8(".L2::cache_hint", policy_evict_first());
+    } else if (TEMP == kLeaf && GRAPE_LEAF_HINT == 2) {
+        GRAPE_LD8(".L1::no_allocate.L2::cache_hint", policy_evict_first());
+    } else {
+        asm("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+            : "l"(p));
+    }
+#undef GRAPE_LD8
+}
+
+// Number of entries j of the aligned 32-byte block `blk` of `arr` with index in
+// [a, b) and value < key; eq: whether one of them equals key.
+template <typename T, typename IDX, int TEMP>
+__device__ __forceinline__ uint32_t block_count_lt(const T* arr, IDX blk, IDX a, IDX b, T key, bool& eq)
+{
+    constexpr int B = 32 / sizeof(T);
+    const T* p = arr + (uint64_t)blk * B;
+    uint32_t w[8];
+    ld_sector<TEMP>(p, w);
+    T v[B];
+    if constexpr (sizeof(T) == 4) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = w[j];
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = ((uint64_t)w[2 * j + 1] << 32) | w[2 * j];
+    }
+    const int ja = (int)(a - blk * B), jb = (int)(b - blk * B);   // 0 <= ja < jb <= B
+    uint32_t cnt = 0;
+    bool e = false;
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+        const bool in = j >= ja && j < jb;
+        cnt += (in && v[j] < key) ? 1u : 0u;
+        e |= in && v[j] == key;
+    }
+    eq = e;
+    return cnt;
+}
+
+template <typename IDX>
+struct Node {
+    IDX start;
+    uint32_t deg, w32;
+};
+
+template <typename IDX>
+__device__ __forceinline__ Node<IDX> load_node(const NodeRec* nodes, uint32_t v)
+{
+    uint4 q;
+    if (GRAPE_HOT_HINT == 1)
+        asm("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+            : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w) : "l"(nodes + v), "l"(policy_evict_last()));
+    else
+        q = ldg_v4(nodes + v);
+    Node<IDX> r;
+    if constexpr (sizeof(IDX) == 8) r.start = ((uint64_t)q.y << 32) | q.x;
+    else r.start = q.x;
+    r.deg = q.z;
+    r.w32 = q.w;
+    return r;
+}
+
+__device__ __forceinline__ void st_cs_v4(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d)
+{
+    asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
+// Per-thread output staging: 8 u32 slots in shared memory (transposed, so the
+// 32 lanes of a warp hit 32 banks), flushed as one aligned 32-B sector.  Entry
+// s of a row goes to slot (phase + s) & 7, phase = the row's 4-B offset within
+// its 32-B sector, so a flush at slot 7 always ends a real sector of `out`.
+struct RowWriter {
+    uint32_t* slot;     // &smem[tid]; slot j at slot[j * kBlock]
+    uint32_t* row;      // &out[i * L]
+    uint32_t phase;     // (row address / 4) & 7
+    uint32_t first;     // first unflushed entry of the row
+
+    __device__ __forceinline__ void begin(uint32_t* row_)
+    {
+        row = row_;
+        phase = (uint32_t)(((uintptr_t)row_ >> 2) & 7);
+        first = 0;
+    }
+    __device__ __forceinline__ void put(uint32_t s, uint32_t x)
+    {
+        const uint32_t j = (phase + s) & 7;
+        slot[j * kBlock] = x;
+        if (j == 7) {
+            if (s >= first + 7) {   // the whole sector belongs to this row
+                uint32_t* p = row + s - 7;
+                st_cs_v4(p, slot[0], slot[kBlock], slot[2 * kBlock], slot[3 * kBlock]);
+                st_cs_v4(p + 4, slot[4 * kBlock], slot[5 * kBlock], slot[6 * kBlock], slot[7 * kBlock]);
+            } else {
+                for (uint32_t q = first; q <= s; ++q) row[q] = slot[((phase + q) & 7) * kBlock];
+            }
+            first = s + 1;
+        }
+    }
+    __device__ __forceinline__ void finish(uint32_t end)   // flush [first, end)
+    {
+        for (uint32_t q = first; q < end; ++q) row[q] = slot[((phase + q) & 7) * kBlock];
+    }
+};
+
+__device__ __forceinline__ void add_steps(unsigned long long* steps_out, unsigned long long mine)
+{
+    if (steps_out == nullptr) return;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(steps_out, mine);
+}
+
+template <typename T>
+Levels<T> levels_of(const void* base, void* const* fences)
+{
+    Levels<T> lv;
+    lv.a[0] = (const T*)base;
+    for (int l = 0; l < NL; ++l) lv.a[l + 1] = (const T*)fences[l];
+    return lv;
+}
+
+template <typename CW>
+Params<CW> make_params(const grape_graph* gg, const WalkArgs& a, const Thresholds& T)
+{
+    Params<CW> P{};
+    P.nodes = gg->nodes;
+    P.col = levels_of<uint32_t>(gg->col, (void* const*)gg->col_fence);
+    if constexpr (!std::is_same<CW, Unweighted>::value) P.cw = levels_of<CW>(gg->cw, gg->cw_fence);
+    P.n = gg->n;
+    P.starts = a.starts;
+    P.num_walks = a.num_walks;
+    P.base = a.walk_id_base;
+    P.L = a.L;
+    P.k0 = (uint32_t)a.seed;
+    P.k1 = (uint32_t)(a.seed >> 32);
+    P.out = a.out;
+    P.steps_out = a.steps_out;
+    const uint64_t lo = T.T1 < T.Tq ? T.T1 : T.Tq, hi = T.T1 < T.Tq ? T.Tq : T.T1;
+    P.tp_m1 = (uint32_t)(T.Tp - 1);
+    P.t1_m1 = (uint32_t)(T.T1 - 1);
+    P.lo_m1 = (uint32_t)(lo - 1);
+    P.hi_m1 = (uint32_t)(hi - 1);
+    P.member_accepts = T.T1 > T.Tq;
+    return P;
+}
+
+}  // namespace walk
+}  // namespace grape
