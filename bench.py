@@ -273,35 +273,49 @@ def run_ours(args):
                "d2h_bytes_per_step": int(W * L * 4 + 8), "steps_timed": e2e_steps,
                "path": "grape_walks_node2vec with pinned host starts/out (library-staged, chunked H2D/kernel/D2H)"}
 
-    # ---- CPU oracle baseline (rank 0, N = 1 only) and the roofline model
+    # ---- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None
-    att_per_step = None
-    if rank == 0 and not args.no_cpu:
-        g_cpu = g.to("cpu")
-        budget = args.cpu_budget if world == 1 else 2.0
-        s, secs, walks, cores, att = _oracle_sample(g_cpu, wk, budget)
-        if node2vec and s:
-            firsts = walks  # one first-order step per walk that moves (upper bound; all starts valid here)
-            att_per_step = (att + firsts) / s
-        if world == 1:
-            cpu = {"value": s / secs, "unit": "steps/s", "cores": cores, "kind": "oracle",
-                   "sample": f"first {walks} walks (wid 0..{walks - 1}) of the same workload, "
-                             f"{cores} threads, {secs:.1f} s"}
-    peak, peak_src = _peaks()
+    if rank == 0 and not args.no_cpu and world == 1:
+        s, secs, walks, cores, att = _oracle_sample(g.to("cpu"), wk, args.cpu_budget)
+        cpu = {"value": s / secs, "unit": "steps/s", "cores": cores, "kind": "oracle",
+               "sample": f"first {walks} walks (wid 0..{walks - 1}) of the same workload, "
+                         f"{cores} threads, {secs:.1f} s"}
+    # ---- roofline of the walk kernel: event counts from the counting
+    # build of the same kernel (grape_walks_stats, untimed), times the measured time.
     roof = None
     if rank == 0:
-        cwb = info["cw_bytes"]
-        A = att_per_step if att_per_step is not None else 1.0
-        # compulsory random-sector model: per realised step one 32-B sector for
-        # off[v..v+1], one for W_v (weighted), and per attempt one sector of the prefix row
-        # (weighted), one of col (proposal) and one of N(t) (membership); + 4 B of output.
-        per_step = 32 * (1 + (1 if cwb else 0)) + A * 32 * ((1 if cwb else 0) + 1 + (1 if node2vec else 0)) + 4
-        achieved = per_step * steps_per_launch / (avg_launch_ms / 1e3) / 1e9
+        _, ev = grape.walks_stats(dg, starts, L, node2vec=node2vec, p=wk["p"], q=wk["q"], seed=wk["seed"],
+                                  walk_id_base=base, out=out)
+        torch.cuda.synchronize(dev)
+        weighted = info["cw_bytes"] > 0
+        # compulsory random sectors: one per node record, one col sector per proposal,
+        # one prefix-row leaf sector per weighted proposal, one N(t) leaf sector per
+        # membership test; plus the streamed walk matrix (4 B/entry) and starts (4 B/walk).
+        rand_sectors = ev["node_loads"] + ev["attempts"] * (2 if weighted else 1) + ev["membership_tests"]
+        alg_bytes = 32 * rand_sectors + 4 * W * L + 4 * W
+        t_launch = avg_launch_ms / 1e3
+        peak, peak_src = _peaks()
+        traffic = args.traffic_per_launch
+        tfile = os.path.join(ROOT, "profiles", f"traffic_cfg{k}.json")
+        if traffic is None and os.path.exists(tfile):
+            traffic = json.load(open(tfile))["dram_bytes_per_launch"]
+        ceil = None
+        cfile = os.path.join(ROOT, "profiles", "gather_ceiling.json")
+        if os.path.exists(cfile):
+            ceil = json.load(open(cfile))["random_accesses_per_s"]
+        achieved = alg_bytes / t_launch / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": args.traffic_per_launch,
-                "kernel": "walk_kernel (node2vec)" if node2vec else "walk_kernel (first order)",
-                "bytes_per_step_model": per_step, "attempts_per_step": A, "peak_source": peak_src,
-                "avg_launch_ms": avg_launch_ms}
+                "traffic": traffic, "kernel": "walk_sm_kernel (grape_walks_node2vec)" if node2vec
+                else "walk_sm_kernel (grape_walks_first_order)",
+                "peak_source": peak_src, "avg_launch_ms": avg_launch_ms,
+                "algorithmic_bytes_per_launch": alg_bytes,
+                "bytes_per_step": alg_bytes / max(ev["steps"], 1),
+                "events_per_launch": ev,
+                "random_access": {"compulsory_sectors_per_step": rand_sectors / max(ev["steps"], 1),
+                                  "achieved_per_s": rand_sectors / t_launch,
+                                  "ceiling_per_s": ceil,
+                                  "frac": (rand_sectors / t_launch / ceil) if ceil else None,
+                                  "ceiling_source": "profiles/gather_ceiling.json"}}
     clocks = clk.summary()
     if rank == 0:
         line = {"metric": "random-walk steps/sec (node2vec 2nd-order)", "value": value, "unit": "steps/s",

@@ -156,6 +156,34 @@ grape_status grape_walks_node2vec(const grape_graph* g, const uint32_t* starts,
                                   uint32_t walk_length, double p, double q, uint64_t seed,
                                   uint32_t* out, uint64_t* steps_out, cudaStream_t stream);
 
+/*
+ * grape_walks_stats — diagnostics: run the same walks as grape_walks_first_order
+ * (node2vec = 0) or grape_walks_node2vec (node2vec = 1) with event counters
+ * compiled into the kernel, and return the counts.  `out` receives exactly the
+ * walk matrix the plain call writes (a parity check of the counting build).
+ * starts / out must be device buffers; the call is synchronous on `stream`.
+ * Used by bench.py to turn measured time into the roofline of DESIGN.md §7.
+ * Errors as grape_walks_node2vec; EINVAL if starts or out is host memory or
+ * stats is NULL.
+ */
+typedef struct {
+    uint64_t sector_loads;      /* 32-B sector loads issued, all kinds */
+    uint64_t node_loads;        /* node-record loads of the current node v (+ u64 W_v loads) */
+    uint64_t xnode_loads;       /* node-record loads of a proposal x (symmetric membership) */
+    uint64_t cw_probes;         /* sector probes of weight-prefix searches (proposals) */
+    uint64_t col_probes;        /* sector probes of membership searches */
+    uint64_t col_loads;         /* proposal loads col[i] */
+    uint64_t attempts;          /* proposals drawn (Philox draws) */
+    uint64_t membership_tests;  /* "x in N(t)" searches performed */
+    uint64_t start_loads;       /* walks started */
+    uint64_t steps;             /* realised transitions */
+} grape_walk_stats;
+
+grape_status grape_walks_stats(const grape_graph* g, const uint32_t* starts, uint64_t num_walks,
+                               uint64_t walk_id_base, uint32_t walk_length, int node2vec,
+                               double p, double q, uint64_t seed, uint32_t* out,
+                               grape_walk_stats* stats, cudaStream_t stream);
+
 /* Static string for a status code. */
 const char* grape_status_string(grape_status s);
 

@@ -151,7 +151,27 @@ def walks_node2vec(g: Graph, starts, L: int, p: float, q: float, *, seed: int = 
                   out, steps, stream)
 
 
+def walks_stats(g: Graph, starts, L: int, *, node2vec: bool, p: float = 1.0, q: float = 1.0,
+                seed: int = 42, walk_id_base: int = 0, out=None):
+    """grape_walks_stats: (walk matrix, dict of event counters) — diagnostics build of the
+    same kernel (device buffers only; synchronous)."""
+    st = _as_tensor(starts, torch.int32)
+    if not st.is_cuda:
+        raise ValueError("walks_stats needs device starts")
+    W = st.numel()
+    with torch.cuda.device(g.device):
+        if out is None:
+            out = torch.empty((W, L), dtype=torch.int32, device=st.device)
+        stats = _capi.WalkStats()
+        rc = _lib.grape_walks_stats(g.handle, st.data_ptr(), W, walk_id_base, L, int(node2vec), float(p),
+                                    float(q), seed, out.data_ptr(), ctypes.byref(stats),
+                                    ctypes.c_void_p(torch.cuda.current_stream(g.device).cuda_stream))
+    _capi.check(_lib, rc, "grape_walks_stats")
+    return out, {f: int(getattr(stats, f)) for f in _capi.STATS_FIELDS}
+
+
 # C-ABI names, for callers that mirror the header.
 grape_graph_from_csr = graph_from_csr
 grape_walks_first_order = walks_first_order
 grape_walks_node2vec = walks_node2vec
+grape_walks_stats = walks_stats

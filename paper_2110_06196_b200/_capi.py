@@ -20,7 +20,7 @@ GRAPE_PAD = 0xFFFFFFFF
 # Every entry point include/grape_walk.h declares (tests check the .so exports them all).
 EXPORTS = (
     "grape_graph_from_csr", "grape_graph_free", "grape_graph_get_info",
-    "grape_walks_first_order", "grape_walks_node2vec",
+    "grape_walks_first_order", "grape_walks_node2vec", "grape_walks_stats",
     "grape_status_string", "grape_last_error", "grape_version",
 )
 
@@ -37,6 +37,14 @@ class GraphInfo(ctypes.Structure):
         ("device_bytes", ctypes.c_uint64),
         ("device", ctypes.c_int),
     ]
+
+
+STATS_FIELDS = ("sector_loads", "node_loads", "xnode_loads", "cw_probes", "col_probes", "col_loads",
+                "attempts", "membership_tests", "start_loads", "steps")
+
+
+class WalkStats(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_uint64) for f in STATS_FIELDS]
 
 
 class GrapeError(RuntimeError):
@@ -65,6 +73,9 @@ def load(path: str | None = None) -> ctypes.CDLL:
     lib.grape_walks_first_order.restype = i32
     lib.grape_walks_node2vec.argtypes = [vp, vp, u64, u64, u32, dbl, dbl, u64, vp, vp, vp]
     lib.grape_walks_node2vec.restype = i32
+    lib.grape_walks_stats.argtypes = [vp, vp, u64, u64, u32, i32, dbl, dbl, u64, vp,
+                                      ctypes.POINTER(WalkStats), vp]
+    lib.grape_walks_stats.restype = i32
     lib.grape_status_string.argtypes = [i32]
     lib.grape_status_string.restype = ctypes.c_char_p
     lib.grape_last_error.argtypes = []

@@ -177,7 +177,7 @@ grape_status walks_common(const grape_graph* g, const uint32_t* starts, uint64_t
         set_error("starts and out must both be device or both be host memory");
         return GRAPE_EINVAL;
     }
-    WalkArgs a;
+    WalkArgs a{};
     a.starts = starts;
     a.num_walks = num_walks;
     a.walk_id_base = base;
@@ -278,6 +278,69 @@ grape_status grape_walks_node2vec(const grape_graph* g, const uint32_t* starts, 
 {
     return walks_common(g, starts, num_walks, walk_id_base, walk_length, true, p, q, seed, out,
                         steps_out, stream);
+}
+
+grape_status grape_walks_stats(const grape_graph* g, const uint32_t* starts, uint64_t num_walks,
+                               uint64_t walk_id_base, uint32_t walk_length, int node2vec, double p,
+                               double q, uint64_t seed, uint32_t* out, grape_walk_stats* stats,
+                               cudaStream_t stream)
+{
+    g_err[0] = 0;
+    if (g == nullptr || stats == nullptr || (num_walks > 0 && (starts == nullptr || out == nullptr))) {
+        set_error("graph, stats, starts and out must be non-NULL");
+        return GRAPE_EINVAL;
+    }
+    if (walk_length == 0) {
+        set_error("walk_length must be >= 1");
+        return GRAPE_EINVAL;
+    }
+    if (num_walks > (~0ull) / walk_length / 4) {
+        set_error("num_walks * walk_length overflows");
+        return GRAPE_EINVAL;
+    }
+    Thresholds T{1ull << 32, 1ull << 32, 1ull << 32};
+    if (node2vec && !node2vec_thresholds(p, q, &T)) return GRAPE_EINVAL;
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess) { cudaGetLastError(); cur = -1; }
+    if (cur != g->device) {
+        set_error("current device %d is not the graph's device %d", cur, g->device);
+        return GRAPE_EINVAL;
+    }
+    memset(stats, 0, sizeof(*stats));
+    if (num_walks == 0) return GRAPE_OK;
+    if (classify(starts) != Mem::Device || classify(out) != Mem::Device) {
+        set_error("grape_walks_stats needs device starts and out");
+        return GRAPE_EINVAL;
+    }
+    unsigned long long* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, sizeof(unsigned long long) * kStatsWords);
+    if (e != cudaSuccess) return cuda_fail(e, "stats buffer");
+    WalkArgs a{};
+    a.starts = starts;
+    a.num_walks = num_walks;
+    a.walk_id_base = walk_id_base;
+    a.L = walk_length;
+    a.seed = seed;
+    a.out = out;
+    a.stats = d;
+    e = cudaMemsetAsync(d, 0, sizeof(unsigned long long) * kStatsWords, stream);
+    if (e == cudaSuccess) e = launch_walks_sm(g, a, node2vec != 0, T, stream);
+    unsigned long long h[kStatsWords] = {0};
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    cudaFree(d);
+    if (e != cudaSuccess) return cuda_fail(e, "grape_walks_stats");
+    stats->sector_loads = h[0];
+    stats->node_loads = h[1];
+    stats->xnode_loads = h[2];
+    stats->cw_probes = h[3];
+    stats->col_probes = h[4];
+    stats->col_loads = h[5];
+    stats->attempts = h[6];
+    stats->membership_tests = h[7];
+    stats->start_loads = h[8];
+    stats->steps = h[9];
+    return GRAPE_OK;
 }
 
 const char* grape_status_string(grape_status s)

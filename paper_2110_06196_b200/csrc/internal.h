@@ -57,7 +57,9 @@ struct WalkArgs {
     uint64_t seed;
     uint32_t* out;
     unsigned long long* steps_out;   // device, may be NULL
+    unsigned long long* stats;       // device grape_walk_stats (as u64[kStatsWords]) or NULL
 };
+constexpr int kStatsWords = 10;
 
 // walk.cu: launch one walk kernel (device buffers) on `stream`.
 // node2vec == false -> first order.  Returns cudaGetLastError() of the launch.

@@ -36,6 +36,46 @@ __device__ __forceinline__ Draw philox_draw(uint32_t k0, uint32_t k1, uint64_t w
     return d;
 }
 
+// Round keys of Philox4x32-10 for a seed: rk[2r], rk[2r+1] = key + r * (W0, W1)
+// (mod 2^32), r = 0..9 — computed once on the host and passed in the kernel
+// parameters, so every round's XOR takes its key straight from the constant bank.
+struct RoundKeys {
+    uint32_t k[20];
+};
+
+inline RoundKeys philox_round_keys(uint64_t seed)
+{
+    RoundKeys rk;
+    uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+    for (int r = 0; r < 10; ++r) {
+        rk.k[2 * r] = k0;
+        rk.k[2 * r + 1] = k1;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return rk;
+}
+
+__device__ __forceinline__ Draw philox_draw_rk(const RoundKeys& rk, uint64_t wid, uint32_t step, uint32_t attempt)
+{
+    constexpr uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+    uint32_t c0 = (uint32_t)wid, c1 = (uint32_t)(wid >> 32), c2 = step, c3 = attempt;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = (uint64_t)M0 * c0, p1 = (uint64_t)M1 * c2;   // IMAD.WIDE.U32
+        const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ rk.k[2 * r];
+        const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ rk.k[2 * r + 1];
+        c1 = (uint32_t)p1;
+        c3 = (uint32_t)p0;
+        c0 = n0;
+        c2 = n2;
+    }
+    Draw d;
+    d.x64 = ((uint64_t)c1 << 32) | c0;
+    d.u = c2;
+    return d;
+}
+
 // floor(x64 * W / 2^64): the high word of the 128-bit product (§8(c) c8).
 __device__ __forceinline__ uint64_t bounded64(uint64_t x64, uint64_t W)
 {

@@ -231,7 +231,7 @@ cudaError_t launch_walks_structured(const grape_graph* g, const WalkArgs& a, boo
 }
 
 #ifndef GRAPE_WALKER
-#define GRAPE_WALKER 2
+#define GRAPE_WALKER 3
 #endif
 
 // The walker used by the C-ABI: 3 = convergent state machine (walk_sm.cu),

@@ -42,8 +42,10 @@ struct Params {
     uint64_t base;
     uint32_t L;
     uint32_t k0, k1;
+    RoundKeys rk;          // Philox round keys of the seed
     uint32_t* out;
     unsigned long long* steps_out;
+    unsigned long long* stats;   // diagnostics counters (grape_walks_stats) or NULL
     // acceptance: u < T  <=>  u <= T - 1  (T in [1, 2^32], so T - 1 fits u32)
     uint32_t tp_m1, t1_m1, lo_m1, hi_m1;
     bool member_accepts;   // for u in [T_lo, T_hi): accepted iff (x in N(t)) == (T_1 > T_q)
@@ -265,8 +267,10 @@ Params<CW> make_params(const grape_graph* gg, const WalkArgs& a, const Threshold
     P.L = a.L;
     P.k0 = (uint32_t)a.seed;
     P.k1 = (uint32_t)(a.seed >> 32);
+    P.rk = philox_round_keys(a.seed);
     P.out = a.out;
     P.steps_out = a.steps_out;
+    P.stats = a.stats;
     const uint64_t lo = T.T1 < T.Tq ? T.T1 : T.Tq, hi = T.T1 < T.Tq ? T.Tq : T.T1;
     P.tp_m1 = (uint32_t)(T.Tp - 1);
     P.t1_m1 = (uint32_t)(T.T1 - 1);

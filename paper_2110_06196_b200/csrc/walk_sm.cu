@@ -47,114 +47,45 @@ __device__ __forceinline__ void ld8(const uint32_t* p, uint32_t (&v)[8])
                  : "l"(p));
 }
 
-// Search over a fenced sorted row (walk_common.cuh Levels): "first i in [lo, hi)
-// with A[i] >= key".  State: the level being probed and the candidate range
-// [first, last] at that level (last = the default answer).  A probe loads the
-// sector holding the range's midpoint and either finds the answer inside it or
-// discards it; at levels below the top the range is one block, so one probe.
-template <typename IDX>
-struct Search {
-    IDX lo, hi;          // the row at level 0
-    IDX first, last;     // candidate range at level lvl
-    uint32_t lvl;
-    uint32_t is_col;     // 0: cw row (key = r + 1); 1: col row of t (key = x); 2: col row of x (key = t)
-};
-
-template <int LB, typename IDX>
-__device__ __forceinline__ IDX e_at(IDX hi, uint32_t l)
+// Lane-private count of the in-range entries of a u32 sector below key, and
+// whether one equals key (branch-free; ja < jb <= 8).
+__device__ __forceinline__ uint32_t sector_count_lt(const uint32_t (&w)[8], int ja, int jb, uint32_t key)
 {
-    IDX e = hi;
+    uint32_t lt = 0;
 #pragma unroll
-    for (uint32_t j = 0; j < (uint32_t)NL; ++j)
-        if (j < l) e = (e - 1) >> LB;
-    return e;
+    for (int q = 0; q < 8; ++q) lt |= (w[q] < key ? 1u : 0u) << q;
+    const uint32_t in = (0xFFu >> (8 - jb)) & (0xFFu << ja);
+    return __popc(lt & in);
 }
 
-// Highest level whose candidate range still spans more than one block, and its range.
-template <int LB, typename IDX>
-__device__ __forceinline__ void search_init(Search<IDX>& S, IDX lo, IDX hi, uint32_t is_col)
+__device__ __forceinline__ uint32_t sector_count_lt64(const uint32_t (&w)[8], int ja, int jb, uint64_t key, bool& eq)
 {
-    S.lo = lo;
-    S.hi = hi;
-    S.is_col = is_col;
-    IDX s = lo, e = hi;
-    uint32_t l = 0;
+    uint32_t lt = 0, ge = 0;
 #pragma unroll
-    for (int j = 0; j < NL; ++j) {
-        if (l == (uint32_t)j && (s >> LB) != ((e - 1) >> LB)) {
-            s >>= LB;
-            e = (e - 1) >> LB;
-            l = j + 1;
-        }
+    for (int q = 0; q < 4; ++q) {
+        const uint64_t val = ((uint64_t)w[2 * q + 1] << 32) | w[2 * q];
+        lt |= (val < key ? 1u : 0u) << q;
+        ge |= (val == key ? 1u : 0u) << q;
     }
-    S.lvl = l;
-    S.first = s;
-    S.last = e;
+    const uint32_t in = (0xFu >> (4 - jb)) & (0xFu << ja);
+    eq = (ge & in) != 0;
+    return __popc(lt & in);
 }
 
-template <typename IDX>
-__device__ __forceinline__ IDX search_mid(const Search<IDX>& S)
-{
-    return S.first + ((S.last - S.first) >> 1);
-}
+// STATS: count every event of the walk (grape_walks_stats; diagnostics build of
+// the same kernel — the timed path is compiled with STATS = false).
+enum : int { C_LOADS = 0, C_NODE, C_XNODE, C_CWPROBE, C_COLPROBE, C_COL, C_ATTEMPT, C_MEMB, C_START, C_STEPS };
 
-// One probe with the sector w (entries of width 4 or 8 bytes, B = 8 or 4 per
-// sector).  Returns true when the search is complete (k = answer at level 0,
-// eq = A[k] == key).
-template <typename T, int LB, typename IDX>
-__device__ __forceinline__ bool search_step(Search<IDX>& S, const uint32_t (&w)[8], T key, IDX& k, bool& eq)
-{
-    constexpr IDX B = IDX(1) << LB;
-    const IDX mid = search_mid(S);
-    const IDX sb = mid & ~(B - 1);
-    const IDX a = S.first > sb ? S.first : sb;
-    const IDX b = S.last < sb + B ? S.last : sb + B;
-    const int ja = (int)(a - sb), jb = (int)(b - sb);
-    uint32_t c = 0;
-    bool e = false;
-#pragma unroll
-    for (int j = 0; j < (int)B; ++j) {
-        T val;
-        if constexpr (sizeof(T) == 4) val = w[j];
-        else val = ((uint64_t)w[2 * j + 1] << 32) | w[2 * j];
-        const bool in = j >= ja && j < jb;
-        c += (in && val < key) ? 1u : 0u;
-        e |= in && val == key;
-    }
-    bool found = false;
-    IDX ans = 0;
-    if (c == (uint32_t)(b - a)) {
-        S.first = b;                       // every candidate here is < key
-        if (S.first == S.last) { ans = S.last; found = true; e = false; }
-    } else if (c == 0 && a > S.first) {
-        S.last = a;                        // answer is at or before a
-        if (S.first == S.last) { ans = a; found = true; }
-        e = false;
-    } else {
-        ans = a + c;                       // first entry >= key is in this sector
-        found = true;
-    }
-    if (!found) return false;
-    if (S.lvl == 0) {
-        k = ans;
-        eq = e;
-        return true;
-    }
-    // descend: the answer lies in block `ans` of the level below
-    const uint32_t l = S.lvl - 1;
-    const IDX sl = S.lo >> (LB * l);
-    const IDX el = e_at<LB, IDX>(S.hi, l);
-    S.lvl = l;
-    S.first = sl > ans * B ? sl : ans * B;
-    S.last = el < ans * B + B ? el : ans * B + B;
-    return false;
-}
-
-template <typename CW, typename IDX, bool NODE2VEC, bool NEED_MEMBER, bool SYM>
+template <typename CW, typename IDX, bool NODE2VEC, bool NEED_MEMBER, bool SYM, bool STATS>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) walk_sm_kernel(const __grid_constant__ Params<CW> P)
 {
+    uint32_t cnt[kStatsWords];
+    if (STATS) {
+#pragma unroll
+        for (int q = 0; q < kStatsWords; ++q) cnt[q] = 0;
+    }
     constexpr bool WEIGHTED = !std::is_same<CW, Unweighted>::value;
-    constexpr int CLB = sizeof(CwStore<CW>) == 8 ? 2 : 3;   // log2 entries per sector of cw
+    constexpr bool CW64 = WEIGHTED && sizeof(CwStore<CW>) == 8;
     using KeyT = CwStore<CW>;
     __shared__ uint32_t stage[8 * kBlock];
     RowWriter w;
@@ -163,59 +94,93 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) walk_sm_kernel(const __gri
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t st = i < P.num_walks ? ST_START : ST_DONE;
+    const void* nxt = P.starts + (i < P.num_walks ? i : 0);   // the address the next iteration loads
     unsigned long long steps = 0;
 
     uint32_t s = 0, a = 0, v = 0, t = kNone, x = 0, u = 0;
-    IDX vstart = 0, tstart = 0, ci = 0;
+    IDX vstart = 0, tstart = 0;
     uint32_t vdeg = 0, tdeg = 0;
     uint64_t vW = 0;
-    KeyT key = 0;
-    Search<IDX> S{};
+    KeyT key = 0;          // search key (cw: r + 1; col: x or t)
+    uint32_t sarr = 0;     // search array: 0 = cw, 1 = col
+    IDX slo = 0, shi = 0, sfirst = 0, slast = 0;
+    uint32_t slvl = 0;
 
     for (;;) {
         const bool active = st != ST_DONE;
         if (!__any_sync(0xffffffffu, active)) break;
-        // ---- 1. the one address this lane needs
-        const void* ea = P.starts;
-        if (st == ST_START) ea = P.starts + i;
-        else if (st == ST_NODE) ea = P.nodes + v;
-        else if (st == ST_XNODE) ea = P.nodes + x;
-        else if (st == ST_COL) ea = P.col.a[0] + ci;
-        else if (st == ST_WV) ea = P.cw.a[0] + (vstart + vdeg - 1);
-        else if (st == ST_SEARCH) {
-            const IDX mid = search_mid(S);
-            if (S.is_col) ea = P.col.a[S.lvl] + mid;
-            else ea = P.cw.a[S.lvl] + mid;
-        }
-        // ---- 2. one sector load for every active lane, issued by the whole warp
-        // together (independent thread scheduling would otherwise let divergent
-        // lane groups issue it one group at a time)
         __syncwarp();
         uint32_t sec[8];
-        if (active) ld8(sector_of(ea), sec);
-        const uint32_t j = word_of(ea);
-        // ---- 3. per-state extraction -> at most one action per lane
-        // actions: emit (accept x), draw (new attempt), fin (end of walk), memb (start membership search)
-        bool emit = false, draw = false, fin = false, memb = false;
+        if (active) ld8(sector_of(nxt), sec);
+        const uint32_t j = word_of(nxt);
+        if (STATS && active) {
+            ++cnt[C_LOADS];
+            cnt[C_NODE] += st == ST_NODE || st == ST_WV;
+            cnt[C_XNODE] += st == ST_XNODE;
+            cnt[C_CWPROBE] += st == ST_SEARCH && sarr == 0;
+            cnt[C_COLPROBE] += st == ST_SEARCH && sarr == 1;
+            cnt[C_COL] += st == ST_COL;
+            cnt[C_START] += st == ST_START;
+        }
+
+        // ---- per-state extraction; sets at most one action
+        bool emit = false, draw = false, fin = false, sinit = false;
+        IDX ilo = 0, ihi = 0;
         if (st == ST_SEARCH) {
-            IDX k = 0;
-            bool eq = false, done = false;
-            if (S.is_col) {
-                done = search_step<uint32_t, 3, IDX>(S, sec, S.is_col == 1 ? x : t, k, eq);
-            } else if constexpr (WEIGHTED) {
-                done = search_step<KeyT, CLB, IDX>(S, sec, key, k, eq);
+            const uint32_t lb = (CW64 && sarr == 0) ? 2 : 3;
+            const IDX B = IDX(1) << lb;
+            const IDX mid = sfirst + ((slast - sfirst) >> 1);
+            const IDX sb = mid & ~(B - 1);
+            const IDX lo_ = sfirst > sb ? sfirst : sb;
+            const IDX hi_ = slast < sb + B ? slast : sb + B;
+            bool eq = false;
+            uint32_t c;
+            if (CW64 && sarr == 0) {
+                c = sector_count_lt64(sec, (int)(lo_ - sb), (int)(hi_ - sb), (uint64_t)key, eq);
+            } else {
+                c = sector_count_lt(sec, (int)(lo_ - sb), (int)(hi_ - sb), (uint32_t)key);
+                // membership answer: the first entry >= key, if inside this sector, equals key?
+                if (sarr && c < (uint32_t)(hi_ - lo_)) eq = pick8(sec, (uint32_t)(lo_ - sb) + c) == (uint32_t)key;
             }
-            if (done) {
-                if (S.is_col) {
-                    emit = eq == P.member_accepts;   // u in [T_lo, T_hi): the class decides
-                    draw = !emit;
-                } else {
-                    ci = k;
-                    st = ST_COL;
+            bool found = false;
+            IDX ans = 0;
+            if (c == (uint32_t)(hi_ - lo_)) {        // every candidate here is < key
+                sfirst = hi_;
+                found = sfirst == slast;
+                ans = slast;
+                eq = false;
+            } else if (c == 0 && lo_ > sfirst) {      // the answer is at or before lo_
+                slast = lo_;
+                found = sfirst == slast;
+                ans = lo_;
+                eq = false;
+            } else {
+                ans = lo_ + c;
+                found = true;
+            }
+            if (found) {
+                if (slvl == 0) {
+                    if (sarr == 0) {
+                        st = ST_COL;                  // proposal index -> col
+                        nxt = P.col.a[0] + ans;
+                    } else {
+                        emit = eq == P.member_accepts;   // u in [T_lo, T_hi): the class decides
+                        draw = !emit;
+                    }
+                } else {                              // descend into block `ans` of level slvl - 1
+                    --slvl;
+                    const IDX sl = slo >> (lb * slvl);
+                    IDX el = shi;
+#pragma unroll
+                    for (uint32_t q = 0; q < (uint32_t)NL; ++q)
+                        if (q < slvl) el = (el - 1) >> lb;
+                    sfirst = sl > ans * B ? sl : ans * B;
+                    slast = el < ans * B + B ? el : ans * B + B;
                 }
             }
         } else if (st == ST_COL) {
             x = pick8(sec, j);
+            bool memb = false;
             if (!NODE2VEC || t == kNone) emit = true;
             else if (x == t) emit = u <= P.tp_m1;
             else if (!NEED_MEMBER) emit = u <= P.t1_m1;
@@ -223,6 +188,14 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) walk_sm_kernel(const __gri
             else if (u > P.hi_m1) emit = false;
             else memb = true;
             draw = !emit && !memb;
+            if (memb) {
+                if (SYM) {
+                    st = ST_XNODE;
+                    nxt = P.nodes + x;
+                } else {
+                    sinit = true; sarr = 1; key = (KeyT)x; ilo = tstart; ihi = tstart + tdeg;
+                }
+            }
         } else if (st == ST_NODE || st == ST_XNODE) {
             const bool hi4 = (j & 4) != 0;
             const uint32_t w0 = hi4 ? sec[4] : sec[0], w1 = hi4 ? sec[5] : sec[1];
@@ -237,13 +210,19 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) walk_sm_kernel(const __gri
                 vdeg = deg;
                 vW = w32;
                 a = 0;
-                if (deg == 0) fin = true;
-                else if (sizeof(KeyT) == 8 && WEIGHTED) st = ST_WV;
-                else draw = true;
-            } else {   // membership on the shorter row (GRAPE_SYMMETRIC): t in N(x) or x in N(t)
-                if (deg < tdeg) search_init<3, IDX>(S, start, start + deg, 2);
-                else search_init<3, IDX>(S, tstart, tstart + tdeg, 1);
-                st = ST_SEARCH;
+                if (deg == 0) {
+                    fin = true;
+                } else if (CW64) {
+                    st = ST_WV;
+                    nxt = P.cw.a[0] + (start + deg - 1);
+                } else {
+                    draw = true;
+                }
+            } else {   // GRAPE_SYMMETRIC: search the shorter row, t in N(x) or x in N(t)
+                sinit = true;
+                sarr = 1;
+                if (deg < tdeg) { key = (KeyT)t; ilo = start; ihi = start + deg; }
+                else { key = (KeyT)x; ilo = tstart; ihi = tstart + tdeg; }
             }
         } else if (st == ST_WV) {
             const uint32_t jj = j & 6;   // u64 entry: words jj, jj+1
@@ -253,24 +232,18 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) walk_sm_kernel(const __gri
             const uint32_t start = pick8(sec, j);
             w.begin(P.out + i * L);
             s = 0;
+            t = kNone;
             if (start < P.n) {
                 x = start;
-                v = kNone;
-                t = kNone;
-                emit = true;   // row[0] = start, then load its node record
+                emit = true;   // row[0] = start, then its node record
             } else {
                 fin = true;
             }
         }
-        // ---- 4. consolidated actions (each executed once per iteration)
-        if (memb) {
-            if (SYM) {
-                st = ST_XNODE;
-            } else {
-                search_init<3, IDX>(S, tstart, tstart + tdeg, 1);
-                st = ST_SEARCH;
-            }
-        }
+
+        // ---- consolidated actions (one call site each), entered by the whole warp at
+        // once so that each block is issued once per iteration, not once per lane group
+        __syncwarp();
         if (emit) {
             w.put(s, x);
             if (s > 0) {
@@ -279,49 +252,97 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) walk_sm_kernel(const __gri
             }
             v = x;
             ++s;
-            if (s == L) fin = true;
-            else st = ST_NODE;
+            if (s == L) {
+                fin = true;
+            } else {
+                st = ST_NODE;
+                nxt = P.nodes + x;
+            }
         }
         if (fin) {
             for (uint32_t q = s; q < L; ++q) w.put(q, kPad);
             w.finish(L);
             i += stride;
             st = i < P.num_walks ? ST_START : ST_DONE;
+            nxt = P.starts + (i < P.num_walks ? i : 0);
+        }
+        __syncwarp();
+        if (STATS) {
+            cnt[C_ATTEMPT] += draw;
+            cnt[C_MEMB] += sinit && sarr == 1;
         }
         if (draw) {
-            if (st != ST_NODE && st != ST_WV) ++a;   // rejected attempt (a new step starts at a = 0)
-            const Draw dr = philox_draw(P.k0, P.k1, P.base + i, s, a);
+            if (st != ST_NODE && st != ST_WV) ++a;   // a rejected attempt; a new step starts at 0
+            const Draw dr = philox_draw_rk(P.rk, P.base + i, s, a);
             u = dr.u;
             if constexpr (WEIGHTED) {
-                key = (KeyT)(bounded64(dr.x64, vW) + 1);   // first cw >= r + 1  <=>  cw > r
-                search_init<CLB, IDX>(S, vstart, vstart + vdeg, 0);
-                st = ST_SEARCH;
+                sinit = true; sarr = 0; key = (KeyT)(bounded64(dr.x64, vW) + 1);   // first cw >= r+1
+                ilo = vstart; ihi = vstart + vdeg;
             } else {
-                ci = vstart + (IDX)bounded64(dr.x64, vdeg);
                 st = ST_COL;
+                nxt = P.col.a[0] + (vstart + (IDX)bounded64(dr.x64, vdeg));
             }
+        }
+        __syncwarp();
+        if (sinit) {   // highest level whose range spans > 1 block; its range and first probe
+            const uint32_t lb = (CW64 && sarr == 0) ? 2 : 3;
+            slo = ilo; shi = ihi;
+            IDX sv = ilo, ev = ihi;
+            uint32_t l = 0;
+#pragma unroll
+            for (int q = 0; q < NL; ++q) {
+                if (l == (uint32_t)q && (sv >> lb) != ((ev - 1) >> lb)) {
+                    sv >>= lb;
+                    ev = (ev - 1) >> lb;
+                    l = q + 1;
+                }
+            }
+            slvl = l; sfirst = sv; slast = ev;
+            st = ST_SEARCH;
+        }
+        if (st == ST_SEARCH) {   // next probe address
+            const IDX mid = sfirst + ((slast - sfirst) >> 1);
+            if (sarr) nxt = P.col.a[slvl] + mid;
+            else nxt = P.cw.a[slvl] + mid;
         }
     }
     add_steps(P.steps_out, steps);
+    if (STATS) {
+        cnt[C_STEPS] = (uint32_t)steps;
+#pragma unroll
+        for (int q = 0; q < kStatsWords; ++q) {
+            unsigned long long c = cnt[q];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+            if ((threadIdx.x & 31) == 0) atomicAdd(P.stats + q, c);
+        }
+    }
+}
+
+template <typename CW, typename IDX, bool NODE2VEC, bool NEED_MEMBER, bool SYM, bool STATS>
+cudaError_t launch_sm_k(const grape_graph* gg, const WalkArgs& a, const Thresholds& T, cudaStream_t stream)
+{
+    const Params<CW> P = make_params<CW>(gg, a, T);
+    static int resident = 0;   // blocks per SM x SMs, queried once per process and instantiation
+    if (resident == 0) {
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, walk_sm_kernel<CW, IDX, NODE2VEC, NEED_MEMBER, SYM, STATS>, kBlock, 0);
+        resident = sms * (per_sm > 0 ? per_sm : 1);
+    }
+    uint64_t blocks = (a.num_walks + kBlock - 1) / kBlock;
+    if (blocks > (uint64_t)resident) blocks = resident;   // persistent: lanes loop over walks
+    walk_sm_kernel<CW, IDX, NODE2VEC, NEED_MEMBER, SYM, STATS><<<(unsigned)blocks, kBlock, 0, stream>>>(P);
+    return cudaGetLastError();
 }
 
 template <typename CW, typename IDX, bool NODE2VEC, bool NEED_MEMBER, bool SYM>
 cudaError_t launch_sm(const grape_graph* gg, const WalkArgs& a, const Thresholds& T, cudaStream_t stream)
 {
-    const Params<CW> P = make_params<CW>(gg, a, T);
-    static int resident = 0;   // blocks per SM x SMs, queried once per process
-    if (resident == 0) {
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, walk_sm_kernel<CW, IDX, NODE2VEC, NEED_MEMBER, SYM>,
-                                                      kBlock, 0);
-        resident = sms * (per_sm > 0 ? per_sm : 1);
-    }
-    uint64_t blocks = (a.num_walks + kBlock - 1) / kBlock;
-    if (blocks > (uint64_t)resident) blocks = resident;   // persistent: lanes loop over walks
-    walk_sm_kernel<CW, IDX, NODE2VEC, NEED_MEMBER, SYM><<<(unsigned)blocks, kBlock, 0, stream>>>(P);
-    return cudaGetLastError();
+    if (a.stats != nullptr) return launch_sm_k<CW, IDX, NODE2VEC, NEED_MEMBER, SYM, true>(gg, a, T, stream);
+    return launch_sm_k<CW, IDX, NODE2VEC, NEED_MEMBER, SYM, false>(gg, a, T, stream);
 }
 
 template <typename CW, typename IDX>

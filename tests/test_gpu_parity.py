@@ -223,3 +223,34 @@ def test_invalid_inputs_rejected(grape):
         grape.walks_node2vec(dg, st, 0, 1.0, 1.0)
     with pytest.raises(grape.GrapeError):   # host starts with a device out
         grape.walks_node2vec(dg, st.cpu(), 5, 1.0, 1.0, out=torch.empty(10, 5, dtype=torch.int32, device="cuda"))
+
+
+@pytest.mark.parametrize("mode,p,q,sym,weighted", [("node2vec", 0.5, 2.0, True, True), ("node2vec", 1.0, 0.25, False, False),
+                                                   ("first_order", 1, 1, True, True), ("node2vec", 2.0, 1.0, True, False)])
+def test_stats_build_matches_and_counts(grape, mode, p, q, sym, weighted):
+    """grape_walks_stats: the counting build writes the same walks; its attempt and
+    step counters equal the oracle's (attempts = draws of node2vec steps s >= 2
+    plus one draw per first-order / first step)."""
+    g = tiny_graph(31, 300, 0.03, directed=not sym, weighted=weighted)
+    dg = _dev_graph(grape, g)
+    starts = np.concatenate([np.arange(g.n), [g.n + 3]]).astype(np.uint32)
+    st = torch.as_tensor(starts.view(np.int32)).cuda()
+    plain = grape.walks_node2vec(dg, st, 40, p, q, seed=5) if mode == "node2vec" else \
+        grape.walks_first_order(dg, st, 40, seed=5)
+    out, stats = grape.walks_stats(dg, st, 40, node2vec=mode == "node2vec", p=p, q=q, seed=5)
+    torch.cuda.synchronize()
+    assert torch.equal(out, plain)
+    exp, esteps, eatt = _oracle(g).walks(starts, 40, mode=mode, p=p, q=q, seed=5, with_attempts=True)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), exp)
+    assert stats["steps"] == esteps
+    if mode == "node2vec" and not (p == 1 and q == 1):
+        first = int(np.sum(exp[:, 1] != PAD))   # walks that made their (first-order) first step
+        assert stats["attempts"] == eatt + first
+    else:
+        assert stats["attempts"] == esteps
+    assert stats["start_loads"] == len(starts)
+    assert stats["col_loads"] == stats["attempts"]
+    assert stats["sector_loads"] == (stats["node_loads"] + stats["xnode_loads"] + stats["cw_probes"] +
+                                     stats["col_probes"] + stats["col_loads"] + stats["start_loads"])
+    if not weighted:
+        assert stats["cw_probes"] == 0
