@@ -197,6 +197,7 @@ def run_reference(args):
 def run_ours(args):
     world, rank, local = _dist_setup(args)
     import paper_2110_06196_b200 as grape
+    from paper_2110_06196_b200.shard import reduce_step_timing, weak_scaling_range
     k = args.config
     wk = config_walks(k)
     dev = torch.device("cuda", local)
@@ -205,7 +206,7 @@ def run_ours(args):
     info = dg.info
     W = g.n * wk["walks_per_node"]
     L = wk["L"]
-    base = rank * W
+    base, _ = weak_scaling_range(W, rank, world)   # rank r: wids [r W, (r+1) W) of N x W walks
     starts = starts_per_node(g.n, wk["walks_per_node"], device=dev)
     out = torch.empty((W, L), dtype=torch.int32, device=dev)
     steps_ctr = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -240,8 +241,7 @@ def run_ours(args):
     kernel_ms = [a.elapsed_time(b) for a, b in ev]
     my_ms = float(sum(kernel_ms))
     my_steps = float(steps_ctr.item())
-    max_ms = _allreduce(my_ms, dist.ReduceOp.MAX, world)
-    tot_steps = _allreduce(my_steps, dist.ReduceOp.SUM, world)
+    max_ms, tot_steps = reduce_step_timing(my_ms, my_steps, world, device=dev)
     value = tot_steps / (max_ms / 1e3)
     steps_per_launch = my_steps / args.steps
     avg_launch_ms = my_ms / args.steps
