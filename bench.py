@@ -161,7 +161,7 @@ def _oracle_sample(g_cpu, wk, budget_s: float, first_wid: int = 0, cores: int | 
 
 
 def _workload_desc(k, g, wk, W):
-    return {"workload": f"BASELINE configs[{k - 1}]: {CONFIGS[k]['name']}", "graph": g.name,
+    return {"workload": f"BASELINE configs[{k - 1}]: {CONFIGS[k]['name']}", "mode": wk["mode"], "graph": g.name,
             "nodes": g.n, "arcs": g.m, "weighted": g.w is not None, "walks_per_gpu": W, "L": wk["L"],
             "p": wk["p"], "q": wk["q"], "seed": wk["seed"],
             "l2": "no flush: per-step output (W*L*4 B) and graph exceed the 126 MB L2"}
@@ -172,7 +172,7 @@ def run_reference(args):
     if rank != 0:
         return
     k = args.config
-    wk = config_walks(k)
+    wk = _walk_recipe(args)
     g = config_graph(k)
     W = g.n * wk["walks_per_node"]
     vals, total_steps, total_secs = [], 0, 0.0
@@ -194,12 +194,19 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def _walk_recipe(args):
+    wk = config_walks(args.config)
+    if args.mode:
+        wk["mode"] = args.mode
+    return wk
+
+
 def run_ours(args):
     world, rank, local = _dist_setup(args)
     import paper_2110_06196_b200 as grape
     from paper_2110_06196_b200.shard import reduce_step_timing, weak_scaling_range
     k = args.config
-    wk = config_walks(k)
+    wk = _walk_recipe(args)
     dev = torch.device("cuda", local)
     g = config_graph(k, device=dev)
     dg = grape.graph_from_csr(g.off, g.col, g.w, device=local, symmetric=g.symmetric)
@@ -318,7 +325,8 @@ def run_ours(args):
                                   "ceiling_source": "profiles/gather_ceiling.json"}}
     clocks = clk.summary()
     if rank == 0:
-        line = {"metric": "random-walk steps/sec (node2vec 2nd-order)", "value": value, "unit": "steps/s",
+        line = {"metric": "random-walk steps/sec (node2vec 2nd-order)" if node2vec else
+                "random-walk steps/sec (first-order)", "value": value, "unit": "steps/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32/u64 integer",
                 "data": "synthetic (seeded generator, graphgen/)", "config": _workload_desc(k, g, wk, W),
@@ -339,6 +347,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--mode", default=None, choices=["node2vec", "first_order"],
+                    help="override the config's walk mode (configs[4] names both)")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work per thread")
     ap.add_argument("--ref-budget", type=float, default=6.0)
     ap.add_argument("--traffic-per-launch", type=float, default=None,

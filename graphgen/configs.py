@@ -17,7 +17,7 @@ CONFIGS = {
     4: dict(name="cfg4_chunglu_50M_n2v_p2_q0.5", graph=dict(kind="chung_lu", n=50_000_000, m=1_000_000_000, weights=1000),
             mode="node2vec", p=2.0, q=0.5, walks_per_node=1, L=100, seed=42),
     5: dict(name="cfg5_rmat26_directed_n2v_p0.25_q4", graph=dict(kind="rmat", scale=26, ef=16, symmetric=False,
-                                                                weights=("geometric", 10.0)),
+                                                                weights=("geometric", 10.0), sinks=0.05),
             mode="node2vec", p=0.25, q=4.0, walks_per_node=2, L=64, seed=42),
 }
 
@@ -31,7 +31,7 @@ def config_graph(k: int, device="cpu", *, scale_down: int = 0):
         return chung_lu(n, m, seed=k, weights=g["weights"], device=device,
                         name=CONFIGS[k]["name"] + (f"/2^{scale_down}" if scale_down else ""))
     return rmat(g["scale"] - scale_down, g["ef"], seed=k, symmetric=g["symmetric"],
-                weights=g["weights"], device=device,
+                weights=g["weights"], device=device, sink_fraction=g.get("sinks"),
                 name=CONFIGS[k]["name"] + (f"/2^{scale_down}" if scale_down else ""))
 
 

@@ -93,6 +93,44 @@ def csr_from_arcs(n: int, src: torch.Tensor, dst: torch.Tensor) -> tuple[torch.T
     return off, col
 
 
+def _csr_from_sorted_keys(n: int, key: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+    """CSR of sorted unique arc keys src * n + dst."""
+    src = torch.div(key, n, rounding_mode="floor")
+    col = (key - src * n).to(torch.int32)
+    off = torch.zeros(n + 1, dtype=torch.int64, device=key.device)
+    off[1:] = torch.cumsum(torch.bincount(src, minlength=n), 0)
+    return off, col
+
+
+def _csr_symmetric(n: int, ckey: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+    """Symmetric CSR from sorted unique canonical keys a * n + b (a < b): every edge
+    gives arcs a->b and b->a.  The reversed keys are sorted once and merged by rank
+    (searchsorted), so no sort ever holds all 2m arcs."""
+    a = torch.div(ckey, n, rounding_mode="floor")
+    b = ckey - a * n
+    rkey = torch.sort(b * n + a).values
+    del a, b
+    m1 = ckey.numel()
+    col = torch.empty(2 * m1, dtype=torch.int32, device=ckey.device)
+    idx = torch.arange(m1, device=ckey.device)
+    pos = idx + torch.searchsorted(rkey, ckey)
+    col[pos] = (ckey % n).to(torch.int32)
+    pos = idx + torch.searchsorted(ckey, rkey)
+    col[pos] = (rkey % n).to(torch.int32)
+    del pos, idx
+    cnt = torch.bincount(torch.div(ckey, n, rounding_mode="floor"), minlength=n)
+    cnt += torch.bincount(torch.div(rkey, n, rounding_mode="floor"), minlength=n)
+    off = torch.zeros(n + 1, dtype=torch.int64, device=ckey.device)
+    off[1:] = torch.cumsum(cnt, 0)
+    return off, col
+
+
+def _arc_rows(off: torch.Tensor, lo: int, hi: int) -> torch.Tensor:
+    """Source node of arcs [lo, hi)."""
+    e = torch.arange(lo, hi, device=off.device, dtype=torch.int64)
+    return torch.searchsorted(off, e, right=True) - 1
+
+
 def _permutation(n: int, seed: int, device) -> torch.Tensor:
     """Seeded random permutation of [0, n): stable argsort of per-label hashes."""
     h = hash3(seed, 0x5045524D, torch.arange(n, device=device, dtype=torch.int64))
@@ -155,24 +193,22 @@ def chung_lu(n: int, m_target: int, *, seed: int, weights: int | None = None,
         keys.append(torch.minimum(a, b) * n + torch.maximum(a, b))
     key = torch.unique(torch.cat(keys), sorted=True)
     del keys
-    a = torch.div(key, n, rounding_mode="floor")
-    b = key - a * n
+    off, col = _csr_symmetric(n, key)
     del key
-    src = torch.cat([a, b])
-    dst = torch.cat([b, a])
-    del a, b
-    off, col = csr_from_arcs(n, src, dst)
-    del src, dst
     w = None
     if weights is not None:
-        rows = torch.repeat_interleave(torch.arange(n, device=device), off[1:] - off[:-1])
-        w = _sym_weights(n, rows, col.to(torch.int64), seed, "uniform", weights)
+        w = torch.empty_like(col)
+        m = col.numel()
+        for lo in range(0, m, chunk):
+            hi = min(m, lo + chunk)
+            w[lo:hi] = _sym_weights(n, _arc_rows(off, lo, hi), col[lo:hi].to(torch.int64), seed, "uniform",
+                                    weights)
     return CSR(n, off, col, w, True, name or f"chung_lu(n={n},m={m_target})")
 
 
 def rmat(scale: int, edge_factor: int, *, seed: int, a=0.57, b=0.19, c=0.19,
          symmetric: bool = True, weights=None, device="cpu", chunk: int = 1 << 25,
-         name: str = "") -> CSR:
+         sink_fraction: float | None = None, name: str = "") -> CSR:
     """R-MAT (Graph500-style quadrant recursion, no noise).
 
     ef * 2^scale samples; at each of `scale` levels one 32-bit draw u picks the
@@ -206,22 +242,63 @@ def rmat(scale: int, edge_factor: int, *, seed: int, a=0.57, b=0.19, c=0.19,
             keys.append(s * n + d)
     key = torch.unique(torch.cat(keys), sorted=True)
     del keys
-    s = torch.div(key, n, rounding_mode="floor")
-    d = key - s * n
-    del key
     if symmetric:
-        s, d = torch.cat([s, d]), torch.cat([d, s])
-    off, col = csr_from_arcs(n, s, d)
-    del s, d
+        off, col = _csr_symmetric(n, key)
+    else:
+        if sink_fraction is not None:
+            key = _fix_sinks(n, key, seed, sink_fraction)
+        off, col = _csr_from_sorted_keys(n, key)
+    del key
     w = None
     if weights is not None:
         kind, mean = weights
         assert kind == "geometric"
-        rows = torch.repeat_interleave(torch.arange(n, device=device), off[1:] - off[:-1])
-        cc = col.to(torch.int64)
-        ekey = (torch.minimum(rows, cc) * n + torch.maximum(rows, cc)) if symmetric else rows * n + cc
-        w = _geometric_weights(ekey, seed, mean)
+        w = torch.empty_like(col)
+        m = col.numel()
+        for lo in range(0, m, chunk):
+            hi = min(m, lo + chunk)
+            rows = _arc_rows(off, lo, hi)
+            cc = col[lo:hi].to(torch.int64)
+            ekey = (torch.minimum(rows, cc) * n + torch.maximum(rows, cc)) if symmetric else rows * n + cc
+            w[lo:hi] = _geometric_weights(ekey, seed, mean)
     return CSR(n, off, col, w, symmetric, name or f"rmat(scale={scale},ef={edge_factor})")
+
+
+def _fix_sinks(n: int, key: torch.Tensor, seed: int, fraction: float) -> torch.Tensor:
+    """Directed R-MAT leaves far more out-degree-0 nodes than BASELINE configs[4]'s
+    "~5% dead-end nodes".  Keep a seeded random subset of
+    round(fraction * n) of the natural sinks as sinks; give every other sink one
+    out-arc to col[j] for a uniformly drawn arc j (targets ∝ in-degree), redrawing
+    on a self-loop.  Returns the sorted keys with the new arcs merged in."""
+    device = key.device
+    src = torch.div(key, n, rounding_mode="floor")
+    deg = torch.bincount(src, minlength=n)
+    del src
+    sinks = torch.nonzero(deg == 0).flatten()
+    keep = int(round(fraction * n))
+    if sinks.numel() <= keep:
+        return key
+    order = torch.argsort(hash3(seed, 0x53494E4B, sinks), stable=True)
+    fix = torch.sort(sinks[order[keep:]]).values
+    m = key.numel()
+    tgt = torch.full_like(fix, -1)
+    for attempt in range(64):
+        todo = tgt < 0
+        if not bool(todo.any()):
+            break
+        h = hash3(seed, 0x54475400 + attempt, fix[todo])
+        j = (_hi32(h) * m) >> 32
+        t = key[j] % n
+        t = torch.where(t == fix[todo], torch.full_like(t, -1), t)
+        tgt[todo] = t
+    ok = tgt >= 0
+    new = torch.sort(fix[ok] * n + tgt[ok]).values
+    out = torch.empty(m + new.numel(), dtype=key.dtype, device=device)
+    idx = torch.arange(m, device=device)
+    out[idx + torch.searchsorted(new, key)] = key
+    idx = torch.arange(new.numel(), device=device)
+    out[idx + torch.searchsorted(key, new)] = new
+    return out
 
 
 def tiny_graph(seed: int, n: int, density: float, *, directed: bool = False,

@@ -166,34 +166,60 @@ def test_specialisation_identities(grape):
         assert torch.equal(x, y) and torch.equal(x, z)
 
 
-@pytest.mark.parametrize("k", [2])
-def test_full_size_config_sampled(grape, k):
-    """BASELINE configs[1] at full size, in bench.py's launch configuration (one
-    call over all walks): a seeded sample of walks recomputed by the oracle one
-    by one (the counter-based RNG makes walk i a function of (seed, wid) alone)."""
-    g = config_graph(k, device="cuda")
+FULL = [(2, "node2vec"), (3, "node2vec"), (4, "node2vec"), (5, "node2vec"), (5, "first_order")]
+
+
+@pytest.mark.parametrize("k,mode", FULL, ids=[f"cfg{k}-{m}" for k, m in FULL])
+def test_full_size_config_sampled(grape, k, mode):
+    """BASELINE configs at full size, in bench.py's launch configuration (one call
+    over all walks of the config): a seeded sample of walks — random wids, every
+    walk starting at one of the 50 highest-degree nodes, and (directed graphs)
+    walks from sinks — recomputed by the oracle one by one (the counter-based RNG
+    makes walk i a function of (seed, wid) alone); plus the step counter against
+    the matrix and invariants on the whole matrix."""
     wk = config_walks(k)
+    g = config_graph(k, device="cuda")
+    torch.cuda.empty_cache()
     dg = _dev_graph(grape, g)
     starts = starts_per_node(g.n, wk["walks_per_node"], device="cuda")
     steps = torch.zeros(1, dtype=torch.int64, device="cuda")
-    out = grape.walks_node2vec(dg, starts, wk["L"], wk["p"], wk["q"], seed=wk["seed"], steps=steps)
+    if mode == "node2vec":
+        out = grape.walks_node2vec(dg, starts, wk["L"], wk["p"], wk["q"], seed=wk["seed"], steps=steps)
+    else:
+        out = grape.walks_first_order(dg, starts, wk["L"], seed=wk["seed"], steps=steps)
     torch.cuda.synchronize()
-    o = _oracle(g.to("cpu"))
     W = starts.numel()
-    rng = np.random.default_rng(k)
-    # hubs and random walks: wids whose start is one of the 50 highest-degree nodes + random sample
-    deg = (g.off[1:] - g.off[:-1]).cpu()
-    hubs = torch.topk(deg, 50).indices.numpy()
-    sample = np.unique(np.concatenate([rng.integers(0, W, 1500), hubs, hubs + g.n, [0, W - 1]]))
-    host_out = out.cpu().numpy().view(np.uint32)
-    st_np = starts.cpu().numpy().view(np.uint32)
-    for i in sample:
-        exp, _ = o.walks(st_np[i:i + 1], wk["L"], mode=wk["mode"], p=wk["p"], q=wk["q"],
-                         seed=wk["seed"], base=int(i))
-        assert np.array_equal(host_out[i], exp[0]), i
-    # counter vs the matrix itself
-    realised = int(np.sum(host_out != PAD)) - int(np.sum(host_out[:, 0] != PAD))
+    # whole-matrix checks on the device: rows start at their start node, PAD only as a suffix
+    assert torch.equal(out[:, 0], starts)
+    pad = out == -1
+    assert not bool((pad[:, :-1] & ~pad[:, 1:]).any())
+    realised = int((~pad).sum().item()) - W
     assert realised == int(steps.item())
+    deg = (g.off[1:] - g.off[:-1])
+    hubs = torch.topk(deg, 50).indices.cpu().numpy()
+    sinks = torch.nonzero(deg == 0).flatten()[:20].cpu().numpy()
+    host_rows = {}
+    rng = np.random.default_rng(k)
+    sample = np.concatenate([rng.integers(0, W, 1500), hubs, [0, W - 1]])
+    if wk["walks_per_node"] > 1:
+        sample = np.concatenate([sample, hubs + g.n])
+    sample = np.unique(sample)
+    idx = torch.as_tensor(sample, device="cuda")
+    host_out = out[idx].cpu().numpy().view(np.uint32)
+    st_np = starts[idx].cpu().numpy().view(np.uint32)
+    del out, pad
+    dg.free()
+    gc = g.to("cpu")
+    del g
+    torch.cuda.empty_cache()
+    o = _oracle(gc)
+    for r, i in enumerate(sample):
+        exp, _ = o.walks(st_np[r:r + 1], wk["L"], mode=mode, p=wk["p"], q=wk["q"], seed=wk["seed"], base=int(i))
+        assert np.array_equal(host_out[r], exp[0]), int(i)
+    # walks that start at sinks (directed configs): [start, PAD, ...]
+    if len(sinks):
+        exp, st_ = o.walks(sinks.astype(np.uint32), wk["L"], mode=mode, p=wk["p"], q=wk["q"], seed=wk["seed"])
+        assert st_ == 0 and np.all(exp[:, 1:] == PAD)
 
 
 def test_invalid_inputs_rejected(grape):
