@@ -209,7 +209,7 @@ def run_ours(args):
     wk = _walk_recipe(args)
     dev = torch.device("cuda", local)
     g = config_graph(k, device=dev)
-    dg = grape.graph_from_csr(g.off, g.col, g.w, device=local, symmetric=g.symmetric)
+    dg = grape.graph_from_csr(g.off, g.col, g.w, device=local, symmetric=g.symmetric, tables=not args.no_tables)
     info = dg.info
     W = g.n * wk["walks_per_node"]
     L = wk["L"]
@@ -354,6 +354,7 @@ def main():
     ap.add_argument("--traffic-per-launch", type=float, default=None,
                     help="ncu dram bytes per launch of the walk kernel (from profiles/)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-tables", action="store_true", help="GRAPE_NO_TABLES: the v3 fenced-search walker")
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle baseline (profiling runs)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

@@ -62,7 +62,12 @@ enum {
      * (§8(c) c12).  Checked on the device unless GRAPE_SKIP_VALIDATION. */
     GRAPE_SYMMETRIC = 1u << 0,
     /* Skip the O(m) device validation of the CSR (trusted input). */
-    GRAPE_SKIP_VALIDATION = 1u << 1
+    GRAPE_SKIP_VALIDATION = 1u << 1,
+    /* Do not build the sampling tables (per-arc records with the
+     * reverse arc's interval, per-row guide tables, per-row edge hash sets;
+     * about 8-16 B + 16 B per arc).  Saves that memory; walks then run on the
+     * fenced-search walker (v3).  Results are identical either way. */
+    GRAPE_NO_TABLES = 1u << 2
 };
 
 typedef struct {
@@ -75,6 +80,9 @@ typedef struct {
     uint64_t max_row_weight;  /* max_v W_v (deg for unweighted) */
     uint64_t device_bytes;    /* device memory owned by the handle */
     int device;
+    uint32_t tables;          /* 1 if the sampling tables were built (v4 walker) */
+    uint32_t weights_symmetric; /* 1 if every arc with a reverse arc has its weight */
+    uint64_t table_bytes;     /* part of device_bytes held by the tables */
 } grape_graph_info;
 
 /*
@@ -89,7 +97,7 @@ typedef struct {
  *                (sorted, no duplicate arcs; "sorted vectors").
  *   weights      u32[m], every value >= 1, or NULL for an unweighted graph.
  *   device       CUDA device ordinal that will own the graph.
- *   flags        GRAPE_SYMMETRIC | GRAPE_SKIP_VALIDATION.
+ *   flags        GRAPE_SYMMETRIC | GRAPE_SKIP_VALIDATION | GRAPE_NO_TABLES.
  *   out          receives the handle.
  * The three arrays may be host (pageable or pinned) or device pointers; they
  * are copied, and the call is synchronous: the caller may free them on return.
@@ -172,11 +180,15 @@ typedef struct {
     uint64_t xnode_loads;       /* node-record loads of a proposal x (symmetric membership) */
     uint64_t cw_probes;         /* sector probes of weight-prefix searches (proposals) */
     uint64_t col_probes;        /* sector probes of membership searches */
-    uint64_t col_loads;         /* proposal loads col[i] */
+    uint64_t col_loads;         /* proposal loads: col[i] (v3) or arc records (v4, incl. guide-split scans) */
     uint64_t attempts;          /* proposals drawn (Philox draws) */
     uint64_t membership_tests;  /* "x in N(t)" searches performed */
     uint64_t start_loads;       /* walks started */
     uint64_t steps;             /* realised transitions */
+    /* v4 (tables) walker; zero on the v3 walker: */
+    uint64_t guide_loads;       /* guide-table entries read (weighted proposals) */
+    uint64_t hash_probes;       /* edge-hash sectors read by membership tests */
+    uint64_t alu_decisions;     /* attempts decided without reading the graph */
 } grape_walk_stats;
 
 grape_status grape_walks_stats(const grape_graph* g, const uint32_t* starts, uint64_t num_walks,

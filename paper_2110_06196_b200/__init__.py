@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import _capi
-from ._capi import (GRAPE_PAD, GRAPE_SYMMETRIC, GRAPE_SKIP_VALIDATION, GrapeError,  # noqa: F401
+from ._capi import (GRAPE_PAD, GRAPE_SYMMETRIC, GRAPE_SKIP_VALIDATION, GRAPE_NO_TABLES, GrapeError,  # noqa: F401
                     GRAPE_OK, GRAPE_EINVAL, GRAPE_ENOMEM, GRAPE_ECUDA)
 
 _lib = _capi.load()
@@ -85,15 +85,17 @@ class Graph:
 
 
 def graph_from_csr(row_offsets, col_indices, weights=None, *, device: int = 0,
-                   symmetric: bool = False, validate: bool = True) -> Graph:
+                   symmetric: bool = False, validate: bool = True, tables: bool = True) -> Graph:
     """grape_graph_from_csr: row_offsets u64/int64 [n+1], col_indices u32/int32 [m],
-    weights u32/int32 [m] >= 1 or None.  Host or device tensors / numpy arrays."""
+    weights u32/int32 [m] >= 1 or None.  Host or device tensors / numpy arrays.
+    tables=False passes GRAPE_NO_TABLES (v3 walker, less memory, same walks)."""
     off = _as_tensor(row_offsets, torch.int64)
     col = _as_tensor(col_indices, torch.int32)
     w = None if weights is None else _as_tensor(weights, torch.int32)
     n = off.numel() - 1
     m = col.numel()
-    flags = (GRAPE_SYMMETRIC if symmetric else 0) | (0 if validate else GRAPE_SKIP_VALIDATION)
+    flags = ((GRAPE_SYMMETRIC if symmetric else 0) | (0 if validate else GRAPE_SKIP_VALIDATION)
+             | (0 if tables else GRAPE_NO_TABLES))
     h = ctypes.c_void_p()
     st = _lib.grape_graph_from_csr(n, m, off.data_ptr(), col.data_ptr() if m else None,
                                    None if w is None else w.data_ptr(), device, flags, ctypes.byref(h))

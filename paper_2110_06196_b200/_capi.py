@@ -15,6 +15,7 @@ LIB_PATH = os.path.join(_HERE, "libgrape_walk.so")
 GRAPE_OK, GRAPE_EINVAL, GRAPE_ENOMEM, GRAPE_ECUDA = 0, 1, 2, 3
 GRAPE_SYMMETRIC = 1 << 0
 GRAPE_SKIP_VALIDATION = 1 << 1
+GRAPE_NO_TABLES = 1 << 2
 GRAPE_PAD = 0xFFFFFFFF
 
 # Every entry point include/grape_walk.h declares (tests check the .so exports them all).
@@ -36,11 +37,15 @@ class GraphInfo(ctypes.Structure):
         ("max_row_weight", ctypes.c_uint64),
         ("device_bytes", ctypes.c_uint64),
         ("device", ctypes.c_int),
+        ("tables", ctypes.c_uint32),
+        ("weights_symmetric", ctypes.c_uint32),
+        ("table_bytes", ctypes.c_uint64),
     ]
 
 
 STATS_FIELDS = ("sector_loads", "node_loads", "xnode_loads", "cw_probes", "col_probes", "col_loads",
-                "attempts", "membership_tests", "start_loads", "steps")
+                "attempts", "membership_tests", "start_loads", "steps", "guide_loads", "hash_probes",
+                "alu_decisions")
 
 
 class WalkStats(ctypes.Structure):

@@ -221,7 +221,7 @@ grape_status grape_graph_from_csr(uint32_t num_nodes, uint64_t num_arcs, const u
         set_error("num_nodes must be < 2^32 - 1 (0xFFFFFFFF is GRAPE_PAD)");
         return GRAPE_EINVAL;
     }
-    if (flags & ~(uint32_t)(GRAPE_SYMMETRIC | GRAPE_SKIP_VALIDATION)) {
+    if (flags & ~(uint32_t)(GRAPE_SYMMETRIC | GRAPE_SKIP_VALIDATION | GRAPE_NO_TABLES)) {
         set_error("unknown flags 0x%x", flags);
         return GRAPE_EINVAL;
     }
@@ -261,6 +261,9 @@ grape_status grape_graph_get_info(const grape_graph* g, grape_graph_info* info)
     info->max_row_weight = g->max_row_weight;
     info->device_bytes = g->device_bytes;
     info->device = g->device;
+    info->tables = g->tables ? 1u : 0u;
+    info->weights_symmetric = g->wsym ? 1u : 0u;
+    info->table_bytes = g->table_bytes;
     return GRAPE_OK;
 }
 
@@ -324,7 +327,7 @@ grape_status grape_walks_stats(const grape_graph* g, const uint32_t* starts, uin
     a.out = out;
     a.stats = d;
     e = cudaMemsetAsync(d, 0, sizeof(unsigned long long) * kStatsWords, stream);
-    if (e == cudaSuccess) e = launch_walks_sm(g, a, node2vec != 0, T, stream);
+    if (e == cudaSuccess) e = launch_walks(g, a, node2vec != 0, T, stream);
     unsigned long long h[kStatsWords] = {0};
     if (e == cudaSuccess) e = cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
@@ -340,6 +343,9 @@ grape_status grape_walks_stats(const grape_graph* g, const uint32_t* starts, uin
     stats->membership_tests = h[7];
     stats->start_loads = h[8];
     stats->steps = h[9];
+    stats->guide_loads = h[10];
+    stats->hash_probes = h[11];
+    stats->alu_decisions = h[12];
     return GRAPE_OK;
 }
 

@@ -193,6 +193,7 @@ void destroy_graph(grape_graph* g)
     cudaFree(g->col);
     cudaFree(g->cw);
     cudaFree(g->nodes);
+    destroy_tables(g);
     for (int l = 0; l < kFenceLevels; ++l) {
         cudaFree(g->col_fence[l]);
         cudaFree(g->cw_fence[l]);
@@ -210,7 +211,7 @@ grape_status build_graph(uint32_t n, uint64_t m, const uint64_t* off_in, const u
     g->device = device;
     g->n = n;
     g->m = m;
-    g->flags = flags & (GRAPE_SYMMETRIC);
+    g->flags = flags & (GRAPE_SYMMETRIC | GRAPE_NO_TABLES);
     uint32_t* w = nullptr;
     unsigned* d_bad = nullptr;
     unsigned long long* d_maxw = nullptr;
@@ -346,6 +347,11 @@ grape_status build_graph(uint32_t n, uint64_t m, const uint64_t* off_in, const u
         GRAPE_TRY_CUDA(cudaGetLastError(), "fence levels");
     }
     GRAPE_TRY_CUDA(cudaDeviceSynchronize(), "graph build");
+    if (!(flags & GRAPE_NO_TABLES)) {
+        st = build_tables(g);
+        if (st != GRAPE_OK) return fail(st);
+        GRAPE_TRY_CUDA(cudaDeviceSynchronize(), "table build");
+    }
     cudaFree(w);
     w = nullptr;
     cudaFree(d_bad);
@@ -353,9 +359,8 @@ grape_status build_graph(uint32_t n, uint64_t m, const uint64_t* off_in, const u
     cudaFree(d_maxdeg);
     d_bad = nullptr; d_maxw = nullptr; d_maxdeg = nullptr;
     g->device_bytes = (n + 1ull) * 8 + padded(m * 4) + (g->cw_bytes ? padded(m * g->cw_bytes) : 0) +
-                      (uint64_t)n * sizeof(NodeRec) + fence_bytes;
+                      (uint64_t)n * sizeof(NodeRec) + fence_bytes + g->table_bytes;
     *out = g;
-    (void)st;
     return GRAPE_OK;
 #undef GRAPE_TRY_ALLOC
 #undef GRAPE_TRY_CUDA

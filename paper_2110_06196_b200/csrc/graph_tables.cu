@@ -1,0 +1,213 @@
+// graph_tables.cu — sampling tables for the v4 walker, built
+// once per graph next to the CSR (not on the timed path).
+//
+// The rules of a walk (include/grape_walk.h) touch the graph in three ways per
+// attempt: the proposal index i = min{i : cw[off_v + i] > r}, the
+// proposal x = col[off_v + i], and the class of x — p if x == t,
+// 1 if x in N(t), q otherwise.  The tables answer each with one
+// sector read instead of a search, and never change a result:
+//
+//   rec    per arc e = (v -> x), arc order (16 B weighted / 8 B unweighted):
+//            weighted   {x, hi = cw[e], rlo, rhi}  [rlo, rhi) = the r-interval of
+//                       the reverse arc (x -> v) inside x's row, [0,0) if none
+//            unweighted {x, rev}   rev = index of v in N(x), or NONE
+//          With it the walker knows, at x coming from v, which draws propose
+//          x' == v (the "return" class p) without reading anything.
+//   guide  weighted rows only, B_v = 2 deg(v) entries at 2 off[v]: entry kb
+//          covers the x64 draws with floor(x64 * B_v / 2^64) = kb; it holds
+//          i_lo = the proposal index of the smallest such draw, and bit 31 set
+//          when the bucket's largest draw proposes a different index ("split";
+//          the walker then scans rec[i_lo..] comparing r with hi).  A guide
+//          table (Chen & Asau) for the inverse-CDF search of P:509-511.
+//   ehash  per-row set of N(v) for "x in N(t)": 2 deg(v) u32 slots at 2 off[v],
+//          linear probing from umulhi(fmix32(x), 2 deg(v)), empty = 0xFFFFFFFF
+//          (never a node id).  Load factor 1/2.
+// Index ranges: 2m < 2^32 - 64 (u32 arc and slot indices), max degree < 2^31 (guide bit
+// 31), row sums < 2^32 (u32 prefix).  Outside them the tables are not built and
+// the v3 walker (fenced searches) runs.
+#include <cstring>
+#include "internal.h"
+
+namespace grape {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;
+
+__host__ __device__ inline uint32_t fmix32(uint32_t h)
+{
+    h ^= h >> 16;
+    h *= 0x85EBCA6Bu;
+    h ^= h >> 13;
+    h *= 0xC2B2AE35u;
+    h ^= h >> 16;
+    return h;
+}
+
+// First index in [a, b) with col[j] >= key (b if none).
+__device__ inline uint64_t lower_bound_u32(const uint32_t* __restrict__ col, uint64_t a, uint64_t b, uint32_t key)
+{
+    while (a < b) {
+        const uint64_t mid = a + ((b - a) >> 1);
+        if (col[mid] < key) a = mid + 1; else b = mid;
+    }
+    return a;
+}
+
+// First index in [a, b) with cw[j] > key (b if none).
+__device__ inline uint64_t upper_bound_u32(const uint32_t* __restrict__ cw, uint64_t a, uint64_t b, uint32_t key)
+{
+    while (a < b) {
+        const uint64_t mid = a + ((b - a) >> 1);
+        if (cw[mid] <= key) a = mid + 1; else b = mid;
+    }
+    return a;
+}
+
+// One warp per row, lanes over the row's arcs.
+template <bool WEIGHTED>
+__global__ void build_records(const uint64_t* __restrict__ off, const uint32_t* __restrict__ col,
+                              const uint32_t* __restrict__ cw, uint32_t n, void* __restrict__ rec,
+                              unsigned* __restrict__ asym)
+{
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    bool bad = false;
+    for (uint64_t v = warp; v < n; v += nwarps) {
+        const uint64_t lo = off[v], hi = off[v + 1];
+        for (uint64_t e = lo + lane; e < hi; e += 32) {
+            const uint32_t x = col[e];
+            const uint64_t xa = off[x], xb = off[x + 1];
+            const uint64_t j = lower_bound_u32(col, xa, xb, (uint32_t)v);
+            const bool found = j < xb && col[j] == (uint32_t)v;
+            if (WEIGHTED) {
+                const uint32_t own_hi = cw[e];
+                const uint32_t own_w = own_hi - (e > lo ? cw[e - 1] : 0u);
+                uint32_t rlo = 0, rhi = 0;
+                if (found) {
+                    rlo = j > xa ? cw[j - 1] : 0u;
+                    rhi = cw[j];
+                    bad |= (rhi - rlo) != own_w;
+                }
+                reinterpret_cast<uint4*>(rec)[e] = make_uint4(x, own_hi, rlo, rhi);
+            } else {
+                reinterpret_cast<uint2*>(rec)[e] = make_uint2(x, found ? (uint32_t)(j - xa) : kNone);
+            }
+        }
+    }
+    if (WEIGHTED && bad) atomicOr(asym, 1u);
+}
+
+// Guide entries of one row per warp: bucket kb of B = 2 deg covers the draws
+// x64 in [ceil(kb 2^64 / B), ceil((kb+1) 2^64 / B)).  With 2^64 = Q B + R:
+// ceil(kb 2^64 / B) = kb Q + ceil(kb R / B)  (kb R < B^2 < 2^64).
+__global__ void build_guide(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cw, uint32_t n,
+                            uint32_t* __restrict__ guide)
+{
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t v = warp; v < n; v += nwarps) {
+        const uint64_t lo = off[v], hi = off[v + 1], deg = hi - lo;
+        if (deg == 0) continue;
+        const uint64_t B = 2 * deg;
+        const uint64_t W = cw[hi - 1];
+        uint64_t Q = ~0ull / B, R = ~0ull % B + 1;   // 2^64 = Q B + R, 0 <= R < B
+        if (R == B) { ++Q; R = 0; }
+        for (uint64_t kb = lane; kb < B; kb += 32) {
+            const uint64_t xmin = kb * Q + (kb * R + B - 1) / B;
+            const uint64_t xmax = kb + 1 == B ? ~0ull : (kb + 1) * Q + ((kb + 1) * R + B - 1) / B - 1;
+            const uint32_t rmin = (uint32_t)__umul64hi(xmin, W), rmax = (uint32_t)__umul64hi(xmax, W);
+            const uint64_t i = upper_bound_u32(cw, lo, hi, rmin) - lo;   // < deg since cw[hi-1] = W > rmin
+            const bool split = cw[lo + i] <= rmax;
+            guide[2 * lo + kb] = (uint32_t)i | (split ? 0x80000000u : 0u);
+        }
+    }
+}
+
+__global__ void build_ehash(const uint64_t* __restrict__ off, const uint32_t* __restrict__ col, uint32_t n,
+                            uint32_t* __restrict__ ehash)
+{
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t v = warp; v < n; v += nwarps) {
+        const uint64_t lo = off[v], hi = off[v + 1];
+        const uint64_t size = 2 * (hi - lo);
+        uint32_t* region = ehash + 2 * lo;
+        for (uint64_t e = lo + lane; e < hi; e += 32) {
+            const uint32_t x = col[e];
+            uint64_t k = ((uint64_t)fmix32(x) * size) >> 32;
+            while (atomicCAS(region + k, kEmpty, x) != kEmpty) k = k + 1 == size ? 0 : k + 1;
+        }
+    }
+}
+
+int rows_grid(uint64_t n)
+{
+    uint64_t blocks = (n + 7) / 8;
+    if (blocks < 1) blocks = 1;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    return (int)blocks;
+}
+
+uint64_t padded(uint64_t bytes) { return ((bytes + 31) / 32) * 32 + 32; }
+
+}  // namespace
+
+void destroy_tables(grape_graph* g)
+{
+    cudaFree(g->rec);
+    cudaFree(g->guide);
+    cudaFree(g->ehash);
+    g->rec = nullptr;
+    g->guide = nullptr;
+    g->ehash = nullptr;
+    g->tables = false;
+    g->table_bytes = 0;
+}
+
+grape_status build_tables(grape_graph* g)
+{
+    const uint64_t m = g->m;
+    const bool weighted = g->cw_bytes != 0;
+    if (2 * m >= (1ull << 32) - 64 || g->max_degree >= (1u << 31) || g->cw_bytes == 8) return GRAPE_OK;
+    cudaError_t e = cudaSuccess;
+    unsigned* d_asym = nullptr;
+    auto fail = [&](cudaError_t err, const char* what) {
+        cudaFree(d_asym);
+        destroy_tables(g);
+        return cuda_fail(err, what);
+    };
+    g->rec_bytes = weighted ? 16 : 8;
+    const uint64_t rec_b = padded(m * g->rec_bytes), guide_b = weighted ? padded(2 * m * 4) : 0,
+                   hash_b = padded(2 * m * 4);
+    if ((e = cudaMalloc(&g->rec, rec_b)) != cudaSuccess) return fail(e, "cudaMalloc arc records");
+    if (weighted && (e = cudaMalloc((void**)&g->guide, guide_b)) != cudaSuccess) return fail(e, "cudaMalloc guide");
+    if ((e = cudaMalloc((void**)&g->ehash, hash_b)) != cudaSuccess) return fail(e, "cudaMalloc edge hash");
+    if ((e = cudaMalloc((void**)&d_asym, 4)) != cudaSuccess) return fail(e, "cudaMalloc");
+    cudaMemset(d_asym, 0, 4);
+    cudaMemset(g->rec, 0, rec_b);
+    cudaMemset(g->ehash, 0xFF, hash_b);
+    if (weighted) cudaMemset(g->guide, 0, guide_b);
+    const int grid = rows_grid(g->n);
+    if (weighted) {
+        build_records<true><<<grid, kThreads>>>(g->off, g->col, (const uint32_t*)g->cw, g->n, g->rec, d_asym);
+        build_guide<<<grid, kThreads>>>(g->off, (const uint32_t*)g->cw, g->n, g->guide);
+    } else {
+        build_records<false><<<grid, kThreads>>>(g->off, g->col, nullptr, g->n, g->rec, d_asym);
+    }
+    build_ehash<<<grid, kThreads>>>(g->off, g->col, g->n, g->ehash);
+    if ((e = cudaGetLastError()) != cudaSuccess) return fail(e, "table kernels");
+    unsigned asym = 0;
+    if ((e = cudaMemcpy(&asym, d_asym, 4, cudaMemcpyDeviceToHost)) != cudaSuccess) return fail(e, "table build");
+    cudaFree(d_asym);
+    g->wsym = !weighted || asym == 0;
+    g->table_bytes = rec_b + guide_b + hash_b;
+    g->tables = true;
+    return GRAPE_OK;
+}
+
+}  // namespace grape

@@ -33,6 +33,15 @@ struct grape_graph {
     uint32_t* col_fence[grape::kFenceLevels];    // col fence levels 1..3
     void* cw_fence[grape::kFenceLevels];         // cw fence levels 1..3 (cw_bytes each)
     uint32_t flags;       // GRAPE_SYMMETRIC ...
+    // Sampling tables (graph_tables.cu), absent with GRAPE_NO_TABLES
+    // or when the graph exceeds their index ranges (then the v3 walker runs):
+    bool tables;          // rec / guide / ehash below are built
+    bool wsym;            // every arc with a reverse arc has the reverse's weight
+    uint32_t rec_bytes;   // 8 (unweighted {x, rev}) or 16 (weighted {x, hi, rlo, rhi})
+    void* rec;            // per-arc records, arc order
+    uint32_t* guide;      // weighted: 2*deg(v) guide entries per row at 2*off[v]
+    uint32_t* ehash;      // per-row linear-probing sets of N(v): 2*deg(v) slots at 2*off[v]
+    uint64_t table_bytes;
     uint32_t max_degree;
     uint64_t max_row_weight;
     uint64_t device_bytes;
@@ -59,12 +68,14 @@ struct WalkArgs {
     unsigned long long* steps_out;   // device, may be NULL
     unsigned long long* stats;       // device grape_walk_stats (as u64[kStatsWords]) or NULL
 };
-constexpr int kStatsWords = 10;
+constexpr int kStatsWords = 13;
 
 // walk.cu: launch one walk kernel (device buffers) on `stream`.
 // node2vec == false -> first order.  Returns cudaGetLastError() of the launch.
 cudaError_t launch_walks(const grape_graph* g, const WalkArgs& a, bool node2vec,
                          const Thresholds& T, cudaStream_t stream);
+cudaError_t launch_walks_tab(const grape_graph* g, const WalkArgs& a, bool node2vec,
+                             const Thresholds& T, cudaStream_t stream);
 cudaError_t launch_walks_sm(const grape_graph* g, const WalkArgs& a, bool node2vec,
                             const Thresholds& T, cudaStream_t stream);
 
@@ -72,5 +83,10 @@ cudaError_t launch_walks_sm(const grape_graph* g, const WalkArgs& a, bool node2v
 grape_status build_graph(uint32_t n, uint64_t m, const uint64_t* off, const uint32_t* col,
                          const uint32_t* w, int device, uint32_t flags, grape_graph** out);
 void destroy_graph(grape_graph* g);
+// graph_tables.cu: build rec / guide / ehash for a validated graph whose off,
+// col (and cw when weighted) are on the device.  Leaves g->tables false (and
+// returns GRAPE_OK) when the graph is outside the tables' index ranges.
+grape_status build_tables(grape_graph* g);
+void destroy_tables(grape_graph* g);
 
 }  // namespace grape

@@ -234,11 +234,14 @@ cudaError_t launch_walks_structured(const grape_graph* g, const WalkArgs& a, boo
 #define GRAPE_WALKER 3
 #endif
 
-// The walker used by the C-ABI: 3 = convergent state machine (walk_sm.cu),
-// 2 = structured thread-per-walk kernel (this file).  Both produce identical walks.
+// The walker used by the C-ABI: the v4 table walker (walk_tab.cu) when the
+// graph has its sampling tables; otherwise 3 = convergent state machine over
+// fenced searches (walk_sm.cu), 2 = structured thread-per-walk kernel (this
+// file).  All produce identical walks.
 cudaError_t launch_walks(const grape_graph* g, const WalkArgs& a, bool node2vec, const Thresholds& T,
                          cudaStream_t stream)
 {
+    if (g->tables) return launch_walks_tab(g, a, node2vec, T, stream);
     if (GRAPE_WALKER == 2) return launch_walks_structured(g, a, node2vec, T, stream);
     return launch_walks_sm(g, a, node2vec, T, stream);
 }

@@ -22,9 +22,9 @@ def grape():
     return grape
 
 
-def _dev_graph(grape, g: CSR, symmetric=None):
+def _dev_graph(grape, g: CSR, symmetric=None, tables=True):
     sym = g.symmetric if symmetric is None else symmetric
-    return grape.graph_from_csr(g.off, g.col, g.w, device=0, symmetric=sym)
+    return grape.graph_from_csr(g.off, g.col, g.w, device=0, symmetric=sym, tables=tables)
 
 
 def _run(grape, dg, starts, L, mode, p, q, seed, base=0):
@@ -42,12 +42,14 @@ def _oracle(g: CSR):
     return Oracle(*g.numpy())
 
 
-def test_cfg1_every_walk_bit_exact(grape):
+@pytest.mark.parametrize("tables", [True, False], ids=["v4-tables", "v3-fenced"])
+def test_cfg1_every_walk_bit_exact(grape, tables):
     """configs[0]: Chung-Lu 10k nodes, first-order, 1 walk/node, L=32, seed 42 — all walks."""
     g = config_graph(1)
     wk = config_walks(1)
     starts = starts_per_node(g.n, wk["walks_per_node"]).numpy().view(np.uint32)
-    dg = _dev_graph(grape, g)
+    dg = _dev_graph(grape, g, tables=tables)
+    assert dg.info["tables"] == int(tables)
     got, steps = _run(grape, dg, starts, wk["L"], wk["mode"], 1, 1, wk["seed"])
     exp, esteps = _oracle(g).walks(starts, wk["L"], mode=wk["mode"], seed=wk["seed"])
     assert np.array_equal(got, exp)
@@ -77,10 +79,11 @@ def test_fuzz_graphs_every_walk(grape, seed, n, dens, directed, weighted, mode, 
     o = _oracle(g)
     for L in (1, 2, 3, 17, 64):
         exp, esteps = o.walks(starts, L, mode=mode, p=p, q=q, seed=seed, base=3 * seed)
-        for sym in ([False, True] if not directed else [False]):
-            dg = _dev_graph(grape, g, symmetric=sym)
+        for sym, tables in ([(False, True), (True, True), (False, False), (True, False)] if not directed
+                            else [(False, True), (False, False)]):
+            dg = _dev_graph(grape, g, symmetric=sym, tables=tables)
             got, steps = _run(grape, dg, starts, L, mode, p, q, seed, base=3 * seed)
-            assert np.array_equal(got, exp), (L, sym)
+            assert np.array_equal(got, exp), (L, sym, tables)
             assert steps == esteps
 
 
@@ -93,6 +96,7 @@ def test_u64_prefix_path(grape):
     g.w = torch.from_numpy(w.view(np.int32))
     dg = _dev_graph(grape, g)
     assert dg.info["cw_bytes"] == 8
+    assert dg.info["tables"] == 0   # outside the tables' u32 prefix range: v3 walker
     starts = np.arange(g.n, dtype=np.uint32)
     for mode, p, q in [("first_order", 1, 1), ("node2vec", 0.5, 2.0), ("node2vec", 1.0, 0.25)]:
         got, steps = _run(grape, dg, starts, 50, mode, p, q, 11)
@@ -155,6 +159,7 @@ def test_specialisation_identities(grape):
     dn = _dev_graph(grape, g, symmetric=False)
     ones = CSR(g.n, g.off, g.col, torch.ones(g.m, dtype=torch.int32), True)
     dw = _dev_graph(grape, ones)
+    dv3 = _dev_graph(grape, g, tables=False)
     starts = starts_per_node(g.n, 1).cuda()
     a = grape.walks_node2vec(dg, starts, 32, 1.0, 1.0, seed=3)
     b = grape.walks_first_order(dg, starts, 32, seed=3)
@@ -163,7 +168,8 @@ def test_specialisation_identities(grape):
         x = grape.walks_node2vec(dg, starts, 32, p, q, seed=3)
         y = grape.walks_node2vec(dn, starts, 32, p, q, seed=3)   # no symmetric trick
         z = grape.walks_node2vec(dw, starts, 32, p, q, seed=3)   # weighted, all ones
-        assert torch.equal(x, y) and torch.equal(x, z)
+        v = grape.walks_node2vec(dv3, starts, 32, p, q, seed=3)  # fenced-search walker
+        assert torch.equal(x, y) and torch.equal(x, z) and torch.equal(x, v)
 
 
 FULL = [(2, "node2vec"), (3, "node2vec"), (4, "node2vec"), (5, "node2vec"), (5, "first_order")]
@@ -251,14 +257,16 @@ def test_invalid_inputs_rejected(grape):
         grape.walks_node2vec(dg, st.cpu(), 5, 1.0, 1.0, out=torch.empty(10, 5, dtype=torch.int32, device="cuda"))
 
 
+@pytest.mark.parametrize("tables", [True, False], ids=["v4-tables", "v3-fenced"])
 @pytest.mark.parametrize("mode,p,q,sym,weighted", [("node2vec", 0.5, 2.0, True, True), ("node2vec", 1.0, 0.25, False, False),
-                                                   ("first_order", 1, 1, True, True), ("node2vec", 2.0, 1.0, True, False)])
-def test_stats_build_matches_and_counts(grape, mode, p, q, sym, weighted):
+                                                   ("first_order", 1, 1, True, True), ("node2vec", 2.0, 1.0, True, False),
+                                                   ("node2vec", 0.25, 4.0, False, True)])
+def test_stats_build_matches_and_counts(grape, mode, p, q, sym, weighted, tables):
     """grape_walks_stats: the counting build writes the same walks; its attempt and
     step counters equal the oracle's (attempts = draws of node2vec steps s >= 2
     plus one draw per first-order / first step)."""
     g = tiny_graph(31, 300, 0.03, directed=not sym, weighted=weighted)
-    dg = _dev_graph(grape, g)
+    dg = _dev_graph(grape, g, tables=tables)
     starts = np.concatenate([np.arange(g.n), [g.n + 3]]).astype(np.uint32)
     st = torch.as_tensor(starts.view(np.int32)).cuda()
     plain = grape.walks_node2vec(dg, st, 40, p, q, seed=5) if mode == "node2vec" else \
@@ -275,8 +283,25 @@ def test_stats_build_matches_and_counts(grape, mode, p, q, sym, weighted):
     else:
         assert stats["attempts"] == esteps
     assert stats["start_loads"] == len(starts)
-    assert stats["col_loads"] == stats["attempts"]
-    assert stats["sector_loads"] == (stats["node_loads"] + stats["xnode_loads"] + stats["cw_probes"] +
-                                     stats["col_probes"] + stats["col_loads"] + stats["start_loads"])
-    if not weighted:
-        assert stats["cw_probes"] == 0
+    kinds = ("node_loads", "xnode_loads", "cw_probes", "col_probes", "col_loads", "start_loads",
+             "guide_loads", "hash_probes")
+    assert stats["sector_loads"] == sum(stats[k] for k in kinds)
+    if not tables:
+        assert stats["col_loads"] == stats["attempts"]
+        assert stats["guide_loads"] == stats["hash_probes"] == stats["alu_decisions"] == 0
+        if not weighted:
+            assert stats["cw_probes"] == 0
+    else:
+        # v4: an attempt either is decided from registers or reads its proposal once
+        # (one record; weighted: one guide entry unless deg = 1, plus split scans)
+        assert stats["xnode_loads"] == stats["cw_probes"] == stats["col_probes"] == 0
+        proposals = stats["attempts"] - stats["alu_decisions"]
+        assert 0 <= stats["alu_decisions"] <= stats["attempts"]
+        if weighted:
+            assert stats["guide_loads"] <= proposals <= stats["col_loads"]
+        else:
+            assert stats["col_loads"] == proposals and stats["guide_loads"] == 0
+        assert stats["hash_probes"] >= stats["membership_tests"]
+        assert stats["node_loads"] <= esteps + len(starts)
+        if mode == "node2vec" and p < min(1.0, q):
+            assert stats["alu_decisions"] > 0
