@@ -64,9 +64,11 @@ enum {
     /* Skip the O(m) device validation of the CSR (trusted input). */
     GRAPE_SKIP_VALIDATION = 1u << 1,
     /* Do not build the sampling tables (per-arc records with the
-     * reverse arc's interval, per-row guide tables, per-row edge hash sets;
-     * about 8-16 B + 16 B per arc).  Saves that memory; walks then run on the
-     * fenced-search walker (v3).  Results are identical either way. */
+     * reverse arc's interval and the head's node record, per-row guide tables,
+     * per-row edge hash sets: 16 + 8 B per arc unweighted, 32 + 8G + 8 B per
+     * arc weighted, G = 4, 2 or 1 chosen from free device memory; the CSR
+     * arrays are released once the tables exist).  Without them walks run on
+     * the fenced-search walker (v3).  Results are identical either way. */
     GRAPE_NO_TABLES = 1u << 2
 };
 
@@ -83,6 +85,7 @@ typedef struct {
     uint32_t tables;          /* 1 if the sampling tables were built (v4 walker) */
     uint32_t weights_symmetric; /* 1 if every arc with a reverse arc has its weight */
     uint64_t table_bytes;     /* part of device_bytes held by the tables */
+    uint32_t guide_factor;    /* weighted tables: guide buckets per arc (4, 2 or 1 by free memory) */
 } grape_graph_info;
 
 /*

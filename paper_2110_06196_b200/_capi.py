@@ -40,6 +40,7 @@ class GraphInfo(ctypes.Structure):
         ("tables", ctypes.c_uint32),
         ("weights_symmetric", ctypes.c_uint32),
         ("table_bytes", ctypes.c_uint64),
+        ("guide_factor", ctypes.c_uint32),
     ]
 
 

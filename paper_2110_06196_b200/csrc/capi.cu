@@ -264,6 +264,7 @@ grape_status grape_graph_get_info(const grape_graph* g, grape_graph_info* info)
     info->tables = g->tables ? 1u : 0u;
     info->weights_symmetric = g->wsym ? 1u : 0u;
     info->table_bytes = g->table_bytes;
+    info->guide_factor = g->guide_factor;
     return GRAPE_OK;
 }
 

@@ -352,14 +352,26 @@ grape_status build_graph(uint32_t n, uint64_t m, const uint64_t* off_in, const u
         if (st != GRAPE_OK) return fail(st);
         GRAPE_TRY_CUDA(cudaDeviceSynchronize(), "table build");
     }
+    if (g->tables) {   // the table walker reads only nodes / rec / guide / ehash
+        cudaFree(g->col);
+        cudaFree(g->cw);
+        g->col = nullptr;
+        g->cw = nullptr;
+        for (int l = 0; l < kFenceLevels; ++l) {
+            cudaFree(g->col_fence[l]);
+            cudaFree(g->cw_fence[l]);
+            g->col_fence[l] = nullptr;
+            g->cw_fence[l] = nullptr;
+        }
+    }
     cudaFree(w);
     w = nullptr;
     cudaFree(d_bad);
     cudaFree(d_maxw);
     cudaFree(d_maxdeg);
     d_bad = nullptr; d_maxw = nullptr; d_maxdeg = nullptr;
-    g->device_bytes = (n + 1ull) * 8 + padded(m * 4) + (g->cw_bytes ? padded(m * g->cw_bytes) : 0) +
-                      (uint64_t)n * sizeof(NodeRec) + fence_bytes + g->table_bytes;
+    g->device_bytes = (n + 1ull) * 8 + (uint64_t)n * sizeof(NodeRec) + g->table_bytes +
+                      (g->tables ? 0 : padded(m * 4) + (g->cw_bytes ? padded(m * g->cw_bytes) : 0) + fence_bytes);
     *out = g;
     return GRAPE_OK;
 #undef GRAPE_TRY_ALLOC

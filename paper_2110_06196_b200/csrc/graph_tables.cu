@@ -7,23 +7,29 @@
 // 1 if x in N(t), q otherwise.  The tables answer each with one
 // sector read instead of a search, and never change a result:
 //
-//   rec    per arc e = (v -> x), arc order (16 B weighted / 8 B unweighted):
-//            weighted   {x, hi = cw[e], rlo, rhi}  [rlo, rhi) = the r-interval of
-//                       the reverse arc (x -> v) inside x's row, [0,0) if none
-//            unweighted {x, rev}   rev = index of v in N(x), or NONE
+//   rec    per arc e = (v -> x), arc order, one aligned sector or half of one:
+//            weighted (32 B)   {x, hi = cw[e], rlo, rhi, off[x], deg x, W_x, lo = cw[e-1]}
+//                              [rlo, rhi) = the r-interval of the reverse arc (x -> v)
+//                              inside x's row, [0,0) if there is none
+//            unweighted (16 B) {x, rev, off[x], deg x}  rev = index of v in N(x) or NONE
 //          With it the walker knows, at x coming from v, which draws propose
-//          x' == v (the "return" class p) without reading anything.
-//   guide  weighted rows only, B_v = 2 deg(v) entries at 2 off[v]: entry kb
-//          covers the x64 draws with floor(x64 * B_v / 2^64) = kb; it holds
-//          i_lo = the proposal index of the smallest such draw, and bit 31 set
-//          when the bucket's largest draw proposes a different index ("split";
-//          the walker then scans rec[i_lo..] comparing r with hi).  A guide
-//          table (Chen & Asau) for the inverse-CDF search of P:509-511.
+//          x' == v (the "return" class p) without reading anything, and
+//          it has x's node record without a second read.
+//   guide  weighted rows only, B_v = G deg(v) 8-B entries at G off[v] (G = 4, 2
+//          or 1 by free memory): entry kb covers the x64 draws with
+//          floor(x64 * B_v / 2^64) = kb; it holds i_lo = the proposal index of
+//          the smallest such draw, and either the proposal col[i_lo] itself
+//          (every draw of the bucket proposes i_lo) or, for a "split" bucket,
+//          cw[i_lo] to settle i_lo vs i_lo + 1 by one compare (and a MULTI bit
+//          when the bucket spans more boundaries: the walker then scans the
+//          records comparing r with hi).  A guide table (Chen & Asau) for the
+//          inverse-CDF search of P:509-511.
 //   ehash  per-row set of N(v) for "x in N(t)": 2 deg(v) u32 slots at 2 off[v],
 //          linear probing from umulhi(fmix32(x), 2 deg(v)), empty = 0xFFFFFFFF
 //          (never a node id).  Load factor 1/2.
-// Index ranges: 2m < 2^32 - 64 (u32 arc and slot indices), max degree < 2^31 (guide bit
-// 31), row sums < 2^32 (u32 prefix).  Outside them the tables are not built and
+// Index ranges: 2m < 2^32 - 64 (u32 arc and slot indices), max degree < 2^29 (guide
+// bits 30-31, G deg < 2^32), row sums < 2^32 (u32 prefix).  When the tables are
+// built, col / cw / fences are released (graph.cu): nothing reads them after.  Outside them the tables are not built and
 // the v3 walker (fenced searches) runs.
 #include <cstring>
 #include "internal.h"
@@ -65,7 +71,9 @@ __device__ inline uint64_t upper_bound_u32(const uint32_t* __restrict__ cw, uint
     return a;
 }
 
-// One warp per row, lanes over the row's arcs.
+// One warp per row, lanes over the row's arcs.  Each record also carries the
+// node record of its head x (start, degree, W_x), so a walk that takes the arc
+// needs no separate node load.
 template <bool WEIGHTED>
 __global__ void build_records(const uint64_t* __restrict__ off, const uint32_t* __restrict__ col,
                               const uint32_t* __restrict__ cw, uint32_t n, void* __restrict__ rec,
@@ -84,27 +92,35 @@ __global__ void build_records(const uint64_t* __restrict__ off, const uint32_t* 
             const bool found = j < xb && col[j] == (uint32_t)v;
             if (WEIGHTED) {
                 const uint32_t own_hi = cw[e];
-                const uint32_t own_w = own_hi - (e > lo ? cw[e - 1] : 0u);
+                const uint32_t own_lo = e > lo ? cw[e - 1] : 0u;
                 uint32_t rlo = 0, rhi = 0;
                 if (found) {
                     rlo = j > xa ? cw[j - 1] : 0u;
                     rhi = cw[j];
-                    bad |= (rhi - rlo) != own_w;
+                    bad |= (rhi - rlo) != own_hi - own_lo;
                 }
-                reinterpret_cast<uint4*>(rec)[e] = make_uint4(x, own_hi, rlo, rhi);
+                const uint32_t xW = xb > xa ? cw[xb - 1] : 0u;
+                uint4* r = reinterpret_cast<uint4*>(rec) + 2 * e;
+                r[0] = make_uint4(x, own_hi, rlo, rhi);
+                r[1] = make_uint4((uint32_t)xa, (uint32_t)(xb - xa), xW, own_lo);
             } else {
-                reinterpret_cast<uint2*>(rec)[e] = make_uint2(x, found ? (uint32_t)(j - xa) : kNone);
+                reinterpret_cast<uint4*>(rec)[e] =
+                    make_uint4(x, found ? (uint32_t)(j - xa) : kNone, (uint32_t)xa, (uint32_t)(xb - xa));
             }
         }
     }
     if (WEIGHTED && bad) atomicOr(asym, 1u);
 }
 
-// Guide entries of one row per warp: bucket kb of B = 2 deg covers the draws
+// Guide entries of one row per warp: bucket kb of B = G deg covers the draws
 // x64 in [ceil(kb 2^64 / B), ceil((kb+1) 2^64 / B)).  With 2^64 = Q B + R:
 // ceil(kb 2^64 / B) = kb Q + ceil(kb R / B)  (kb R < B^2 < 2^64).
-__global__ void build_guide(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cw, uint32_t n,
-                            uint32_t* __restrict__ guide)
+// Entry {e0, e1}: e0 = i_lo | SPLIT (bit 31) | MULTI (bit 30), i_lo = the
+// proposal index of the bucket's smallest draw; unsplit: e1 = col[i_lo] (the
+// proposal itself); split: e1 = cw[i_lo], the upper end of i_lo's interval
+// (r < e1 -> i_lo, else i_lo + 1 unless MULTI: then scan the records).
+__global__ void build_guide(const uint64_t* __restrict__ off, const uint32_t* __restrict__ col,
+                            const uint32_t* __restrict__ cw, uint32_t n, uint32_t G, uint2* __restrict__ guide)
 {
     const unsigned lane = threadIdx.x & 31;
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -112,7 +128,7 @@ __global__ void build_guide(const uint64_t* __restrict__ off, const uint32_t* __
     for (uint64_t v = warp; v < n; v += nwarps) {
         const uint64_t lo = off[v], hi = off[v + 1], deg = hi - lo;
         if (deg == 0) continue;
-        const uint64_t B = 2 * deg;
+        const uint64_t B = G * deg;
         const uint64_t W = cw[hi - 1];
         uint64_t Q = ~0ull / B, R = ~0ull % B + 1;   // 2^64 = Q B + R, 0 <= R < B
         if (R == B) { ++Q; R = 0; }
@@ -122,7 +138,9 @@ __global__ void build_guide(const uint64_t* __restrict__ off, const uint32_t* __
             const uint32_t rmin = (uint32_t)__umul64hi(xmin, W), rmax = (uint32_t)__umul64hi(xmax, W);
             const uint64_t i = upper_bound_u32(cw, lo, hi, rmin) - lo;   // < deg since cw[hi-1] = W > rmin
             const bool split = cw[lo + i] <= rmax;
-            guide[2 * lo + kb] = (uint32_t)i | (split ? 0x80000000u : 0u);
+            const bool multi = split && cw[lo + i + 1] <= rmax;        // i + 1 < deg when split
+            guide[G * lo + kb] = make_uint2((uint32_t)i | (split ? 0x80000000u : 0u) | (multi ? 0x40000000u : 0u),
+                                            split ? cw[lo + i] : col[lo + i]);
         }
     }
 }
@@ -165,6 +183,7 @@ void destroy_tables(grape_graph* g)
     g->rec = nullptr;
     g->guide = nullptr;
     g->ehash = nullptr;
+    g->guide_factor = 0;
     g->tables = false;
     g->table_bytes = 0;
 }
@@ -173,7 +192,7 @@ grape_status build_tables(grape_graph* g)
 {
     const uint64_t m = g->m;
     const bool weighted = g->cw_bytes != 0;
-    if (2 * m >= (1ull << 32) - 64 || g->max_degree >= (1u << 31) || g->cw_bytes == 8) return GRAPE_OK;
+    if (2 * m >= (1ull << 32) - 64 || g->max_degree >= (1u << 29) || g->cw_bytes == 8) return GRAPE_OK;
     cudaError_t e = cudaSuccess;
     unsigned* d_asym = nullptr;
     auto fail = [&](cudaError_t err, const char* what) {
@@ -181,9 +200,25 @@ grape_status build_tables(grape_graph* g)
         destroy_tables(g);
         return cuda_fail(err, what);
     };
-    g->rec_bytes = weighted ? 16 : 8;
-    const uint64_t rec_b = padded(m * g->rec_bytes), guide_b = weighted ? padded(2 * m * 4) : 0,
-                   hash_b = padded(2 * m * 4);
+    g->rec_bytes = weighted ? 32 : 16;
+    const uint64_t rec_b = padded(m * g->rec_bytes), hash_b = padded(2 * m * 4);
+    // Guide factor G (buckets per arc): 4 / 2 / 1, the largest whose tables leave
+    // room on the device (the caller still needs its walk matrices); results do
+    // not depend on it, only the share of split buckets does.
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    uint32_t G = 0;
+    if (weighted) {
+        for (uint32_t c = 4; c >= 1; c >>= 1) {
+            const uint64_t need = rec_b + hash_b + padded(c * m * 8);
+            if (need <= (c == 1 ? 0.9 : 0.5) * (double)free_b) { G = c; break; }
+        }
+        if (G == 0) return GRAPE_OK;   // does not fit: v3 walker
+    } else if (rec_b + hash_b > 0.9 * (double)free_b) {
+        return GRAPE_OK;
+    }
+    g->guide_factor = G;
+    const uint64_t guide_b = weighted ? padded(G * m * 8) : 0;
     if ((e = cudaMalloc(&g->rec, rec_b)) != cudaSuccess) return fail(e, "cudaMalloc arc records");
     if (weighted && (e = cudaMalloc((void**)&g->guide, guide_b)) != cudaSuccess) return fail(e, "cudaMalloc guide");
     if ((e = cudaMalloc((void**)&g->ehash, hash_b)) != cudaSuccess) return fail(e, "cudaMalloc edge hash");
@@ -195,7 +230,7 @@ grape_status build_tables(grape_graph* g)
     const int grid = rows_grid(g->n);
     if (weighted) {
         build_records<true><<<grid, kThreads>>>(g->off, g->col, (const uint32_t*)g->cw, g->n, g->rec, d_asym);
-        build_guide<<<grid, kThreads>>>(g->off, (const uint32_t*)g->cw, g->n, g->guide);
+        build_guide<<<grid, kThreads>>>(g->off, g->col, (const uint32_t*)g->cw, g->n, G, (uint2*)g->guide);
     } else {
         build_records<false><<<grid, kThreads>>>(g->off, g->col, nullptr, g->n, g->rec, d_asym);
     }

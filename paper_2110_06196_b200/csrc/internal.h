@@ -37,9 +37,10 @@ struct grape_graph {
     // or when the graph exceeds their index ranges (then the v3 walker runs):
     bool tables;          // rec / guide / ehash below are built
     bool wsym;            // every arc with a reverse arc has the reverse's weight
-    uint32_t rec_bytes;   // 8 (unweighted {x, rev}) or 16 (weighted {x, hi, rlo, rhi})
+    uint32_t rec_bytes;   // 16 (unweighted) or 32 (weighted), graph_tables.cu
     void* rec;            // per-arc records, arc order
-    uint32_t* guide;      // weighted: 2*deg(v) guide entries per row at 2*off[v]
+    uint32_t* guide;      // weighted: G*deg(v) 8-B guide entries per row at G*off[v]
+    uint32_t guide_factor;   // G (buckets per arc) of the guide
     uint32_t* ehash;      // per-row linear-probing sets of N(v): 2*deg(v) slots at 2*off[v]
     uint64_t table_bytes;
     uint32_t max_degree;

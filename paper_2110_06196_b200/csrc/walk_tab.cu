@@ -32,24 +32,19 @@ namespace grape {
 namespace {
 using namespace walk;
 
-enum : uint32_t { ST_START = 0, ST_NODE, ST_GUIDE, ST_REC, ST_HASH, ST_DRAW, ST_DONE };
+enum : uint32_t { ST_START = 0, ST_NODE, ST_GUIDE, ST_REC, ST_HASH, ST_DRAW, ST_BACK, ST_DONE };
 
 constexpr uint32_t kEmptySlot = 0xFFFFFFFFu;
-// Inner (ALU) rounds per outer iteration before a lane that is still drawing
-// yields to the next round of loads (bounds the warp's divergent tail).
-#ifndef GRAPE_TAB_ALU_ROUNDS
-#define GRAPE_TAB_ALU_ROUNDS 4
-#endif
 #ifndef GRAPE_TAB_MIN_BLOCKS
-#define GRAPE_TAB_MIN_BLOCKS 3
+#define GRAPE_TAB_MIN_BLOCKS 4
 #endif
 
 struct TabParams {
     const NodeRec* nodes;
-    const uint32_t* col;      // first-order unweighted proposals
-    const void* rec;          // arc records (8 or 16 B)
-    const uint32_t* guide;
+    const void* rec;          // arc records (16 or 32 B)
+    const uint32_t* guide;    // 8-B entries
     const uint32_t* ehash;
+    uint32_t G;               // guide buckets per arc
     uint32_t n;
     const uint32_t* starts;
     uint64_t num_walks;
@@ -70,6 +65,15 @@ __device__ __forceinline__ uint32_t fmix32(uint32_t h)
     h *= 0xC2B2AE35u;
     h ^= h >> 16;
     return h;
+}
+
+// floor(x64 * w / 2^64) for w < 2^32 (§8(c) c8) from two 32x32 products:
+// x64 w = x_hi w 2^32 + x_lo w, and the dropped fraction of x_lo w / 2^32 never
+// carries across a multiple of 2^32.
+__device__ __forceinline__ uint32_t bounded32(uint64_t x64, uint32_t w)
+{
+    const uint64_t lo = ((uint64_t)(uint32_t)x64 * w) >> 32;
+    return (uint32_t)(((uint64_t)(uint32_t)(x64 >> 32) * w + lo) >> 32);
 }
 
 __device__ __forceinline__ uint32_t pick8(const uint32_t (&w)[8], uint32_t j)
@@ -99,13 +103,10 @@ __device__ __forceinline__ void ld8(const uint32_t* p, uint32_t (&v)[8])
 enum : int { C_LOADS = 0, C_NODE, C_XNODE, C_CWPROBE, C_COLPROBE, C_REC, C_ATTEMPT, C_MEMB, C_START, C_STEPS,
              C_GUIDE, C_HASH, C_ALU };
 
-// REC: 4 = first-order unweighted (col only), 8 = {x, rev}, 16 = {x, hi, rlo, rhi}.
-// WSYM: weighted graph whose reverse arcs carry equal weights, so the interval of
-// an arc taken forward is known from its reverse's width (needed after a return).
-template <int REC, bool NODE2VEC, bool NEED_MEMBER, bool WSYM, bool STATS>
+// WEIGHTED: 32-B records + guide; else 16-B records indexed by the draw.
+template <bool WEIGHTED, bool NODE2VEC, bool NEED_MEMBER, bool STATS>
 __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(const __grid_constant__ TabParams P)
 {
-    constexpr bool WEIGHTED = REC == 16;
     uint32_t cnt[kStatsWords];
     if (STATS) {
 #pragma unroll
@@ -124,17 +125,19 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
     uint32_t s = 0, a = 0;
     uint32_t vid = 0, vstart = 0, vdeg = 0, vW = 0;        // current node v
     uint32_t tid = kNone, tstart = 0, tdeg = 0, tW = 0;    // previous node t (kNone: first step)
-    uint32_t tlo = 0, thi = 0;    // proposal interval of t in v's row (r units); tlo > thi: unknown
+    uint32_t tlo = 0, thi = 0;    // proposal interval of t in v's row (r units; empty if no arc v -> t)
     uint32_t slo = 0, shi = 0;    // proposal interval of v in t's row (for a return v -> t)
     uint32_t u = 0, r = 0;        // pending attempt: acceptance draw, bounded proposal draw
-    uint32_t ri = 0;              // row-local record index being read
-    bool split = false;           // weighted: the guide bucket holds several candidates
-    uint32_t x = 0, nlo = 0, nhi = 0, nslo = 0, nshi = 0;   // proposal and its intervals
+    uint32_t ri = 0;              // row-local index of the proposal (record being read)
+    bool scan = false;            // weighted: compare r with the record's hi, advance if past it
+    bool acc = false;             // the attempt is accepted; the record is read for x's data
+    uint32_t x = 0;               // proposal
     uint32_t hk = 0;              // edge-hash slot (absolute index)
+    uint32_t hrev = 0, hxs = 0, hxd = 0;   // unweighted: x's record, kept across its membership test
 
     for (;;) {
-        const bool load = st < ST_DRAW;
         if (!__any_sync(0xffffffffu, st != ST_DONE)) break;
+        const bool load = st < ST_DRAW;
         __syncwarp();
         uint32_t sec[8];
         if (load) ld8(sector_of(nxt), sec);
@@ -148,66 +151,56 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
             cnt[C_HASH] += st == ST_HASH;
         }
 
-        // ---- interpret the sector; at most one action flag per lane
-        bool emit = false, fin = false, draw = st == ST_DRAW, decide = false;
+        // ---- interpret the sector
+        bool emit = false, back = st == ST_BACK, fin = false, draw = st == ST_DRAW, decide = false;
+        // the record of the taken arc (valid when emit): head x, its node record,
+        // the new T = [nlo, nhi) and S = [nslo, nshi)
+        uint32_t xs = 0, xd = 0, xw = 0, nlo = 0, nhi = 0, nslo = 0, nshi = 0;
         if (st == ST_REC) {
             bool found = true;
-            if constexpr (REC == 4) {
-                x = pick8(sec, j);
-            } else if constexpr (REC == 8) {
-                const uint32_t k = j & 6;
-                x = pick8(sec, k);
-                const uint32_t rev = pick8(sec, k + 1);
+            if constexpr (WEIGHTED) {
+                if (scan && r >= sec[1]) {   // past this record's interval: the next one
+                    found = false;
+                    ++ri;
+                    nxt = (const uint4*)P.rec + 2 * (vstart + ri);
+                }
+                x = sec[0];
+                nlo = sec[2]; nhi = sec[3];
+                xs = sec[4]; xd = sec[5]; xw = sec[6];
+                nslo = sec[7]; nshi = sec[1];
+            } else {
+                const bool h = (j & 4) != 0;
+                x = h ? sec[4] : sec[0];
+                const uint32_t rev = h ? sec[5] : sec[1];
+                xs = h ? sec[6] : sec[2];
+                xd = h ? sec[7] : sec[3];
+                xw = xd;
+                hrev = rev; hxs = xs; hxd = xd;
                 nlo = rev;
                 nhi = rev == kNone ? rev : rev + 1;   // [rev, rev+1), or the empty [NONE, NONE)
                 nslo = ri;
                 nshi = ri + 1;
-            } else {
-                // records k = 0, 1 of this sector; the target is k0 = j >> 2
-                const uint32_t k0 = j >> 2;
-                const uint32_t h0 = k0 ? sec[5] : sec[1];
-                uint32_t k = k0;
-                if (split && r >= h0) {
-                    if (k0 == 0 && r < sec[5]) {
-                        k = 1;
-                        ri += 1;
-                    } else {
-                        found = false;                 // continue with the next sector
-                        ri += 2 - k0;
-                        nxt = (const uint4*)P.rec + (vstart + ri);
-                    }
-                }
-                if (found) {
-                    const uint32_t b = k ? 4 : 0;
-                    x = k ? sec[4] : sec[0];
-                    const uint32_t hi = k ? sec[5] : sec[1];
-                    nlo = k ? sec[6] : sec[2];
-                    nhi = k ? sec[7] : sec[3];
-                    (void)b;
-                    if (WSYM) {
-                        nshi = hi;
-                        nslo = hi - (nhi - nlo);
-                    } else {
-                        nslo = 1;                      // unknown
-                        nshi = 0;
-                    }
-                }
             }
-            decide = found;
-        } else if (st == ST_NODE) {
-            const bool hi4 = (j & 4) != 0;
-            vstart = hi4 ? sec[4] : sec[0];
-            vdeg = hi4 ? sec[6] : sec[2];
-            vW = hi4 ? sec[7] : sec[3];
-            a = 0;
-            if (vdeg == 0) fin = true;
-            else draw = true;
+            if (found) {
+                if (acc) emit = true;
+                else decide = true;
+            }
         } else if (st == ST_GUIDE) {
-            const uint32_t e = pick8(sec, j);
-            ri = e & 0x7FFFFFFFu;
-            split = (e >> 31) != 0;
-            st = ST_REC;
-            nxt = (const uint4*)P.rec + (vstart + ri);
+            const uint32_t e0 = pick8(sec, j), e1 = pick8(sec, j | 1);   // 8-B entry at word j (even)
+            ri = e0 & 0x3FFFFFFFu;
+            if (e0 >> 31) {   // split bucket: r against the upper end of i_lo's interval
+                scan = false;
+                if (r >= e1) {
+                    ++ri;
+                    scan = (e0 >> 30) & 1;   // more boundaries: compare record by record
+                }
+                acc = false;
+                st = ST_REC;
+                nxt = (const uint4*)P.rec + 2 * (vstart + ri);
+            } else {          // the bucket proposes i_lo = e1 whatever the draw
+                x = e1;
+                decide = true;
+            }
         } else if (st == ST_HASH) {
             // slots [hk, min(sector end, region end)) of t's set
             const uint32_t sb = hk & ~7u;
@@ -223,141 +216,157 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
             const uint32_t in = (0xFFu >> (8 - e)) & (0xFFu << q0);
             if ((fm | em) & in) {
                 const bool member = (fm & in) != 0;
-                emit = member ? u <= P.t1_m1 : u <= P.tq_m1;
-                draw = !emit;
-                if (draw) ++a;
+                if (member ? u <= P.t1_m1 : u <= P.tq_m1) {
+                    if constexpr (WEIGHTED) {
+                        acc = true;   // read the record again for x's data
+                        scan = false;
+                        st = ST_REC;
+                        nxt = (const uint4*)P.rec + 2 * (vstart + ri);
+                    } else {          // the 16-B record was kept in registers
+                        emit = true;
+                        xs = hxs; xd = hxd; xw = hxd;
+                        nlo = hrev;
+                        nhi = hrev == kNone ? hrev : hrev + 1;
+                        nslo = ri;
+                        nshi = ri + 1;
+                    }
+                } else {
+                    draw = true;
+                    ++a;
+                }
             } else {
                 hk = sb + e == rend ? 2 * tstart : sb + e;
                 nxt = P.ehash + hk;
             }
+        } else if (st == ST_NODE) {   // start node
+            const bool h = (j & 4) != 0;
+            vstart = h ? sec[4] : sec[0];
+            vdeg = h ? sec[6] : sec[2];
+            vW = h ? sec[7] : sec[3];
+            a = 0;
+            if (vdeg == 0) fin = true;
+            else draw = true;
         } else if (st == ST_START) {
             const uint32_t start = pick8(sec, j);
             w.begin(P.out + i * L);
             s = 0;
             tid = kNone;
             if (start < P.n) {
-                x = start;
-                emit = true;
+                w.put(0, start);
+                vid = start;
+                s = 1;
+                if (L == 1) {
+                    fin = true;
+                } else {
+                    st = ST_NODE;
+                    nxt = P.nodes + start;
+                }
             } else {
                 fin = true;
             }
         }
-        if (decide) {   // x is known: the class of x, if it matters
-            if (!NODE2VEC || tid == kNone) {
-                emit = true;
-            } else {
+        if (decide) {   // x is known: its class, if it matters
+            bool ok = true, hash = false;
+            if (NODE2VEC && tid != kNone) {
                 const bool cp = u <= P.tp_m1, c1 = u <= P.t1_m1, cq = u <= P.tq_m1;
-                if (x == tid) emit = cp;
-                else if (!NEED_MEMBER || c1 == cq) emit = c1;
-                else {
-                    if (STATS) ++cnt[C_MEMB];
-                    st = ST_HASH;
-                    hk = 2 * tstart + (uint32_t)(((uint64_t)fmix32(x) * (2 * tdeg)) >> 32);
-                    nxt = P.ehash + hk;
-                }
-                draw = !emit && st != ST_HASH;
-                if (draw) ++a;
+                if (x == tid) ok = cp;
+                else if (!NEED_MEMBER || c1 == cq) ok = c1;
+                else hash = true;
+            }
+            if (hash) {
+                if (STATS) ++cnt[C_MEMB];
+                st = ST_HASH;
+                hk = 2 * tstart + (uint32_t)(((uint64_t)fmix32(x) * (2 * tdeg)) >> 32);
+                nxt = P.ehash + hk;
+            } else if (!ok) {
+                draw = true;
+                ++a;
+            } else if (st == ST_REC) {
+                emit = true;      // the record is in hand
+            } else {              // x came from the guide: read its record
+                acc = true;
+                scan = false;
+                st = ST_REC;
+                nxt = (const uint4*)P.rec + 2 * (vstart + ri);
             }
         }
 
-        // ---- ALU phase: emits, walk ends and draws until every lane has a load
-        // pending (or has drawn GRAPE_TAB_ALU_ROUNDS times)
-#pragma unroll 1
-        for (int round = 0;; ++round) {
-            if (!__any_sync(0xffffffffu, emit || fin || draw)) break;
-            __syncwarp();
-            if (emit) {   // x becomes row[s]; [nlo,nhi) / [nslo,nshi) are the new T / S
-                w.put(s, x);
-                if (s > 0) {
-                    ++steps;
-                    if (x == tid) {   // a return: v and t swap, t's record is in registers
-                        uint32_t q;
-                        q = vstart; vstart = tstart; tstart = q;
-                        q = vdeg; vdeg = tdeg; tdeg = q;
-                        q = vW; vW = tW; tW = q;
-                        tid = vid;
-                        vid = x;
-                        tlo = nlo; thi = nhi; slo = nslo; shi = nshi;
-                        a = 0;
-                        draw = s + 1 < L;
-                        st = ST_DRAW;
-                    } else {
-                        tid = vid; tstart = vstart; tdeg = vdeg; tW = vW;
-                        vid = x;
-                        tlo = nlo; thi = nhi; slo = nslo; shi = nshi;
-                        st = ST_NODE;
-                        nxt = P.nodes + x;
-                    }
+        // ---- the walk advances: from a record (emit) or by a register-decided
+        // return to t (back, decided by the previous iteration's draw)
+        __syncwarp();
+        if (emit || back) {
+            w.put(s, x);
+            ++steps;
+            if (emit) {
+                tid = vid; tstart = vstart; tdeg = vdeg; tW = vW;
+                vid = x; vstart = xs; vdeg = xd; vW = xw;
+                tlo = nlo; thi = nhi; slo = nslo; shi = nshi;
+            } else {   // x = t: v and t swap, and so do T and S
+                uint32_t q;
+                q = vstart; vstart = tstart; tstart = q;
+                q = vdeg; vdeg = tdeg; tdeg = q;
+                q = vW; vW = tW; tW = q;
+                q = vid; vid = tid; tid = q;
+                q = tlo; tlo = slo; slo = q;
+                q = thi; thi = shi; shi = q;
+            }
+            ++s;
+            a = 0;
+            fin = s == L || vdeg == 0;
+            draw = !fin;
+        }
+        if (fin) {
+            for (uint32_t q = s; q < L; ++q) w.put(q, kPad);
+            w.finish(L);
+            i += stride;
+            st = i < P.num_walks ? ST_START : ST_DONE;
+            nxt = P.starts + (i < P.num_walks ? i : 0);
+            draw = false;
+        }
+
+        // ---- one draw per lane per iteration: Philox, the band of u, and the
+        // decisions that need no read (§8(c) c12)
+        __syncwarp();
+        if (draw) {
+            if (STATS) ++cnt[C_ATTEMPT];
+            const Draw dr = philox_draw_rk(P.rk, P.base + i, s, a);
+            u = dr.u;
+            r = bounded32(dr.x64, vW);   // index (unweighted: vW = deg) or weight point
+            bool need_x = true, ret = false;
+            if (NODE2VEC && tid != kNone) {
+                const bool cp = u <= P.tp_m1, c1 = u <= P.t1_m1, cq = u <= P.tq_m1;
+                if (cp == c1 && c1 == cq) {
+                    need_x = cp;
+                } else if (c1 == cq && tlo <= thi) {   // only "x == t" matters, and it is known
+                    const bool is_t = r - tlo < thi - tlo;
+                    const bool ok = is_t ? cp : c1;
+                    need_x = ok && !is_t;
+                    ret = ok && is_t;
+                }
+                if (STATS) cnt[C_ALU] += !need_x;
+            }
+            acc = false;
+            scan = false;
+            if (ret) {          // return to t: emitted next iteration, no read
+                x = tid;
+                st = ST_BACK;
+            } else if (!need_x) {
+                ++a;            // rejected without reading the graph
+                st = ST_DRAW;
+            } else if constexpr (WEIGHTED) {
+                if (vdeg == 1) {
+                    ri = 0;
+                    st = ST_REC;
+                    nxt = (const uint4*)P.rec + 2 * vstart;
                 } else {
-                    vid = x;
-                    st = ST_NODE;
-                    nxt = P.nodes + x;
+                    const uint32_t kb = bounded32(dr.x64, P.G * vdeg);
+                    st = ST_GUIDE;
+                    nxt = (const uint2*)P.guide + ((uint64_t)P.G * vstart + kb);
                 }
-                ++s;
-                fin = s == L;
-                emit = false;
-            }
-            if (fin) {
-                for (uint32_t q = s; q < L; ++q) w.put(q, kPad);
-                w.finish(L);
-                i += stride;
-                st = i < P.num_walks ? ST_START : ST_DONE;
-                nxt = P.starts + (i < P.num_walks ? i : 0);
-                fin = false;
-                draw = false;
-            }
-            __syncwarp();
-            if (draw && round >= GRAPE_TAB_ALU_ROUNDS) {
-                st = ST_DRAW;   // keep drawing after the next round of loads
-                draw = false;
-            }
-            if (draw) {
-                if (STATS) ++cnt[C_ATTEMPT];
-                const Draw dr = philox_draw_rk(P.rk, P.base + i, s, a);
-                u = dr.u;
-                r = (uint32_t)bounded64(dr.x64, vW);   // index (unweighted: vW = deg) or weight point
-                bool need_x = true, back = false;
-                if (NODE2VEC && tid != kNone) {
-                    const bool cp = u <= P.tp_m1, c1 = u <= P.t1_m1, cq = u <= P.tq_m1;
-                    if (cp == c1 && c1 == cq) {
-                        need_x = cp;
-                    } else if (c1 == cq && tlo <= thi) {   // only "x == t" matters, and it is known
-                        const bool is_t = r - tlo < thi - tlo;
-                        const bool acc = is_t ? cp : c1;
-                        need_x = acc && !is_t;
-                        back = acc && is_t;
-                    }
-                    if (STATS) cnt[C_ALU] += !need_x;
-                }
-                if (back) {   // return to t: x = t, the new T / S are the old S / T
-                    x = tid;
-                    nlo = slo; nhi = shi; nslo = tlo; nshi = thi;
-                    emit = true;
-                    draw = false;
-                } else if (need_x) {
-                    draw = false;
-                    if constexpr (REC == 16) {
-                        if (vdeg == 1) {
-                            ri = 0;
-                            split = false;
-                            st = ST_REC;
-                            nxt = (const uint4*)P.rec + vstart;
-                        } else {
-                            const uint32_t kb = (uint32_t)__umul64hi(dr.x64, 2ull * vdeg);
-                            st = ST_GUIDE;
-                            nxt = P.guide + (2ull * vstart + kb);
-                        }
-                    } else if constexpr (REC == 8) {
-                        ri = r;
-                        st = ST_REC;
-                        nxt = (const uint2*)P.rec + (vstart + r);
-                    } else {
-                        st = ST_REC;
-                        nxt = P.col + (vstart + r);
-                    }
-                } else {
-                    ++a;   // rejected without reading the graph
-                }
+            } else {
+                ri = r;
+                st = ST_REC;
+                nxt = (const uint4*)P.rec + (vstart + r);
             }
         }
     }
@@ -374,15 +383,15 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
     }
 }
 
-template <int REC, bool NODE2VEC, bool NEED_MEMBER, bool WSYM, bool STATS>
+template <bool WEIGHTED, bool NODE2VEC, bool NEED_MEMBER, bool STATS>
 cudaError_t launch_k(const grape_graph* g, const WalkArgs& a, const Thresholds& T, cudaStream_t stream)
 {
     TabParams P{};
     P.nodes = g->nodes;
-    P.col = g->col;
     P.rec = g->rec;
     P.guide = g->guide;
     P.ehash = g->ehash;
+    P.G = g->guide_factor;
     P.n = g->n;
     P.starts = a.starts;
     P.num_walks = a.num_walks;
@@ -400,28 +409,30 @@ cudaError_t launch_k(const grape_graph* g, const WalkArgs& a, const Thresholds& 
         int dev = 0, sms = 0, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, walk_tab_kernel<REC, NODE2VEC, NEED_MEMBER, WSYM, STATS>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, walk_tab_kernel<WEIGHTED, NODE2VEC, NEED_MEMBER, STATS>,
                                                       kBlock, 0);
         resident = sms * (per_sm > 0 ? per_sm : 1);
     }
     uint64_t blocks = (a.num_walks + kBlock - 1) / kBlock;
     if (blocks > (uint64_t)resident) blocks = resident;
-    walk_tab_kernel<REC, NODE2VEC, NEED_MEMBER, WSYM, STATS><<<(unsigned)blocks, kBlock, 0, stream>>>(P);
+    walk_tab_kernel<WEIGHTED, NODE2VEC, NEED_MEMBER, STATS><<<(unsigned)blocks, kBlock, 0, stream>>>(P);
     return cudaGetLastError();
 }
 
-template <int REC, bool NODE2VEC, bool NEED_MEMBER, bool WSYM>
+template <bool WEIGHTED, bool NODE2VEC, bool NEED_MEMBER>
 cudaError_t launch_s(const grape_graph* g, const WalkArgs& a, const Thresholds& T, cudaStream_t stream)
 {
-    if (a.stats != nullptr) return launch_k<REC, NODE2VEC, NEED_MEMBER, WSYM, true>(g, a, T, stream);
-    return launch_k<REC, NODE2VEC, NEED_MEMBER, WSYM, false>(g, a, T, stream);
+    if (a.stats != nullptr) return launch_k<WEIGHTED, NODE2VEC, NEED_MEMBER, true>(g, a, T, stream);
+    return launch_k<WEIGHTED, NODE2VEC, NEED_MEMBER, false>(g, a, T, stream);
 }
 
-template <int REC, bool WSYM>
-cudaError_t dispatch_n2v(const grape_graph* g, const WalkArgs& a, const Thresholds& T, cudaStream_t stream)
+template <bool WEIGHTED>
+cudaError_t dispatch(const grape_graph* g, const WalkArgs& a, bool node2vec, const Thresholds& T,
+                     cudaStream_t stream)
 {
-    if (T.T1 != T.Tq) return launch_s<REC, true, true, WSYM>(g, a, T, stream);
-    return launch_s<REC, true, false, WSYM>(g, a, T, stream);
+    if (!node2vec || (T.Tp == T.T1 && T.T1 == T.Tq)) return launch_s<WEIGHTED, false, false>(g, a, T, stream);
+    if (T.T1 != T.Tq) return launch_s<WEIGHTED, true, true>(g, a, T, stream);
+    return launch_s<WEIGHTED, true, false>(g, a, T, stream);
 }
 
 }  // namespace
@@ -429,15 +440,8 @@ cudaError_t dispatch_n2v(const grape_graph* g, const WalkArgs& a, const Threshol
 cudaError_t launch_walks_tab(const grape_graph* g, const WalkArgs& a, bool node2vec, const Thresholds& T,
                              cudaStream_t stream)
 {
-    const bool weighted = g->cw_bytes != 0;
-    const bool first_order = !node2vec || (T.Tp == T.T1 && T.T1 == T.Tq);
-    if (first_order) {
-        if (weighted) return launch_s<16, false, false, false>(g, a, T, stream);
-        return launch_s<4, false, false, false>(g, a, T, stream);
-    }
-    if (!weighted) return dispatch_n2v<8, false>(g, a, T, stream);
-    if (g->wsym) return dispatch_n2v<16, true>(g, a, T, stream);
-    return dispatch_n2v<16, false>(g, a, T, stream);
+    if (g->cw_bytes != 0) return dispatch<true>(g, a, node2vec, T, stream);
+    return dispatch<false>(g, a, node2vec, T, stream);
 }
 
 }  // namespace grape

@@ -292,16 +292,19 @@ def test_stats_build_matches_and_counts(grape, mode, p, q, sym, weighted, tables
         if not weighted:
             assert stats["cw_probes"] == 0
     else:
-        # v4: an attempt either is decided from registers or reads its proposal once
-        # (one record; weighted: one guide entry unless deg = 1, plus split scans)
+        # v4: an attempt is decided from registers or reads its proposal: weighted,
+        # one guide entry (rows of degree > 1) and the record when it is needed;
+        # unweighted, the record; an accepted proposal whose membership test ran
+        # after the read re-reads its record.  Node records are read for starts only.
         assert stats["xnode_loads"] == stats["cw_probes"] == stats["col_probes"] == 0
         proposals = stats["attempts"] - stats["alu_decisions"]
         assert 0 <= stats["alu_decisions"] <= stats["attempts"]
         if weighted:
-            assert stats["guide_loads"] <= proposals <= stats["col_loads"]
+            assert stats["guide_loads"] <= proposals
         else:
-            assert stats["col_loads"] == proposals and stats["guide_loads"] == 0
+            assert stats["guide_loads"] == 0
+            assert proposals <= stats["col_loads"] <= proposals + stats["membership_tests"]
         assert stats["hash_probes"] >= stats["membership_tests"]
-        assert stats["node_loads"] <= esteps + len(starts)
+        assert stats["node_loads"] <= len(starts)
         if mode == "node2vec" and p < min(1.0, q):
             assert stats["alu_decisions"] > 0

@@ -61,6 +61,7 @@ def _check_all(grape, g, L=48, seeds=(3,), settings=SETTINGS, expect_wsym=None):
     assert d4.info["table_bytes"] > 0 and d3.info["table_bytes"] == 0
     if expect_wsym is not None:
         assert d4.info["weights_symmetric"] == int(expect_wsym)
+    assert d4.info["guide_factor"] == (4 if g.w is not None else 0)
     for seed in seeds:
         for mode, p, q in settings:
             exp, esteps = o.walks(starts, L, mode=mode, p=p, q=q, seed=seed, base=11)
