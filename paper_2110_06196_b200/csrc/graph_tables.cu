@@ -24,9 +24,11 @@
 //          when the bucket spans more boundaries: the walker then scans the
 //          records comparing r with hi).  A guide table (Chen & Asau) for the
 //          inverse-CDF search of P:509-511.
-//   ehash  per-row set of N(v) for "x in N(t)": 2 deg(v) u32 slots at 2 off[v],
-//          linear probing from umulhi(fmix32(x), 2 deg(v)), empty = 0xFFFFFFFF
-//          (never a node id).  Load factor 1/2.
+//   ehash  per-row set of N(v) for "x in N(t)": floor(deg v / 4) + 1 buckets of
+//          8 u32 slots (one sector each) from bucket floor(off[v] / 4) + v;
+//          bucketised linear probing from bucket floor(fmix32(x) nb / 2^32);
+//          empty = 0xFFFFFFFF (never a node id).  Load factor <= 1/2, so a
+//          lookup reads one sector unless its home bucket is full.
 // Index ranges: 2m < 2^32 - 64 (u32 arc and slot indices), max degree < 2^29 (guide
 // bits 30-31, G deg < 2^32), row sums < 2^32 (u32 prefix).  When the tables are
 // built, col / cw / fences are released (graph.cu): nothing reads them after.  Outside them the tables are not built and
@@ -145,6 +147,12 @@ __global__ void build_guide(const uint64_t* __restrict__ off, const uint32_t* __
     }
 }
 
+// Bucketised sets: row v owns the 8-slot buckets [B_v, B_v + nb_v), B_v =
+// floor(off[v] / 4) + v, nb_v = floor(deg v / 4) + 1 (>= 2 deg slots, disjoint
+// across rows, derivable from the node record).  x goes to the first empty slot
+// of bucket B_v + floor(fmix32(x) nb_v / 2^32), or of the next non-full bucket
+// (cyclically): a bucket that an item skipped is full forever (no deletions),
+// so a lookup may stop at the first bucket holding x or an empty slot.
 __global__ void build_ehash(const uint64_t* __restrict__ off, const uint32_t* __restrict__ col, uint32_t n,
                             uint32_t* __restrict__ ehash)
 {
@@ -153,12 +161,17 @@ __global__ void build_ehash(const uint64_t* __restrict__ off, const uint32_t* __
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t v = warp; v < n; v += nwarps) {
         const uint64_t lo = off[v], hi = off[v + 1];
-        const uint64_t size = 2 * (hi - lo);
-        uint32_t* region = ehash + 2 * lo;
+        const uint64_t base = (lo >> 2) + v, nb = ((hi - lo) >> 2) + 1;
         for (uint64_t e = lo + lane; e < hi; e += 32) {
             const uint32_t x = col[e];
-            uint64_t k = ((uint64_t)fmix32(x) * size) >> 32;
-            while (atomicCAS(region + k, kEmpty, x) != kEmpty) k = k + 1 == size ? 0 : k + 1;
+            uint64_t b = ((uint64_t)fmix32(x) * nb) >> 32;
+            for (;;) {
+                uint32_t* slot = ehash + 8 * (base + b);
+                int q = 0;
+                while (q < 8 && atomicCAS(slot + q, kEmpty, x) != kEmpty) ++q;
+                if (q < 8) break;
+                b = b + 1 == nb ? 0 : b + 1;
+            }
         }
     }
 }
@@ -192,7 +205,9 @@ grape_status build_tables(grape_graph* g)
 {
     const uint64_t m = g->m;
     const bool weighted = g->cw_bytes != 0;
-    if (2 * m >= (1ull << 32) - 64 || g->max_degree >= (1u << 29) || g->cw_bytes == 8) return GRAPE_OK;
+    if (2 * m >= (1ull << 32) - 64 || (m >> 2) + g->n + 2 >= (1ull << 32) || g->max_degree >= (1u << 29) ||
+        g->cw_bytes == 8)
+        return GRAPE_OK;
     cudaError_t e = cudaSuccess;
     unsigned* d_asym = nullptr;
     auto fail = [&](cudaError_t err, const char* what) {
@@ -201,7 +216,7 @@ grape_status build_tables(grape_graph* g)
         return cuda_fail(err, what);
     };
     g->rec_bytes = weighted ? 32 : 16;
-    const uint64_t rec_b = padded(m * g->rec_bytes), hash_b = padded(2 * m * 4);
+    const uint64_t rec_b = padded(m * g->rec_bytes), hash_b = padded(((m >> 2) + g->n + 1) * 32);
     // Guide factor G (buckets per arc): 4 / 2 / 1, the largest whose tables leave
     // room on the device (the caller still needs its walk matrices); results do
     // not depend on it, only the share of split buckets does.
@@ -211,7 +226,7 @@ grape_status build_tables(grape_graph* g)
     if (weighted) {
         for (uint32_t c = 4; c >= 1; c >>= 1) {
             const uint64_t need = rec_b + hash_b + padded(c * m * 8);
-            if (need <= (c == 1 ? 0.9 : 0.5) * (double)free_b) { G = c; break; }
+            if (c * m < (1ull << 32) && need <= (c == 1 ? 0.9 : 0.5) * (double)free_b) { G = c; break; }
         }
         if (G == 0) return GRAPE_OK;   // does not fit: v3 walker
     } else if (rec_b + hash_b > 0.9 * (double)free_b) {

@@ -10,7 +10,7 @@
 //   ST_GUIDE  guide entry of the draw's bucket    -> first candidate index
 //   ST_REC    arc record(s) {x, hi, rlo, rhi}     -> proposal x, and the reverse arc's
 //                                                   interval for the next step
-//   ST_HASH   one sector of t's edge-hash set     -> "x in N(t)"
+//   ST_HASH   one bucket of t's edge-hash set     -> "x in N(t)"
 // then an ALU-only phase (the inner loop) that may run several draws, emits and
 // walk ends without touching memory:
 //   * The three acceptance classes (thresholds §8(c) c9) split the
@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t st = i < P.num_walks ? ST_START : ST_DONE;
-    const void* nxt = P.starts + (i < P.num_walks ? i : 0);
+    uint32_t idx = 0;   // what the next load reads: NODE node id, GUIDE bucket, HASH bucket (REC: ri)
     unsigned long long steps = 0;
 
     uint32_t s = 0, a = 0;
@@ -132,7 +132,6 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
     bool scan = false;            // weighted: compare r with the record's hi, advance if past it
     bool acc = false;             // the attempt is accepted; the record is read for x's data
     uint32_t x = 0;               // proposal
-    uint32_t hk = 0;              // edge-hash slot (absolute index)
     uint32_t hrev = 0, hxs = 0, hxd = 0;   // unweighted: x's record, kept across its membership test
 
     for (;;) {
@@ -140,8 +139,23 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
         const bool load = st < ST_DRAW;
         __syncwarp();
         uint32_t sec[8];
-        if (load) ld8(sector_of(nxt), sec);
-        const uint32_t j = word_of(nxt);
+        uint32_t j;
+        {   // the one load of this iteration: a single address computation for every state
+            const bool rec = st == ST_REC, gd = st == ST_GUIDE, nd = st == ST_NODE;
+            const uint32_t mul = rec ? 1u : gd ? P.G : 0u;
+            uint64_t e = (uint64_t)mul * vstart + (rec ? ri : idx);
+            const char* b = rec ? (const char*)P.rec : gd ? (const char*)P.guide
+                          : nd ? (const char*)P.nodes : (const char*)P.ehash;
+            uint32_t sh = rec ? (WEIGHTED ? 5u : 4u) : gd ? 3u : nd ? 4u : 5u;
+            if (st == ST_START) {
+                b = (const char*)P.starts;
+                e = i;
+                sh = 2;
+            }
+            const char* addr = b + (e << sh);
+            if (load) ld8(sector_of(addr), sec);
+            j = word_of(addr);
+        }
         if (STATS && load) {
             ++cnt[C_LOADS];
             cnt[C_NODE] += st == ST_NODE;
@@ -162,7 +176,6 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                 if (scan && r >= sec[1]) {   // past this record's interval: the next one
                     found = false;
                     ++ri;
-                    nxt = (const uint4*)P.rec + 2 * (vstart + ri);
                 }
                 x = sec[0];
                 nlo = sec[2]; nhi = sec[3];
@@ -196,32 +209,23 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                 }
                 acc = false;
                 st = ST_REC;
-                nxt = (const uint4*)P.rec + 2 * (vstart + ri);
             } else {          // the bucket proposes i_lo = e1 whatever the draw
                 x = e1;
                 decide = true;
             }
-        } else if (st == ST_HASH) {
-            // slots [hk, min(sector end, region end)) of t's set
-            const uint32_t sb = hk & ~7u;
-            const uint32_t rend = 2 * (tstart + tdeg);
-            const uint32_t e = rend - sb < 8 ? rend - sb : 8;
-            const uint32_t q0 = hk - sb;
-            uint32_t fm = 0, em = 0;
+        } else if (st == ST_HASH) {   // one bucket (8 slots) of t's set
+            bool found = false, empty = false;
 #pragma unroll
-            for (uint32_t q = 0; q < 8; ++q) {
-                fm |= (sec[q] == x ? 1u : 0u) << q;
-                em |= (sec[q] == kEmptySlot ? 1u : 0u) << q;
+            for (int q = 0; q < 8; ++q) {
+                found |= sec[q] == x;
+                empty |= sec[q] == kEmptySlot;
             }
-            const uint32_t in = (0xFFu >> (8 - e)) & (0xFFu << q0);
-            if ((fm | em) & in) {
-                const bool member = (fm & in) != 0;
-                if (member ? u <= P.t1_m1 : u <= P.tq_m1) {
+            if (found || empty) {
+                if (found ? u <= P.t1_m1 : u <= P.tq_m1) {
                     if constexpr (WEIGHTED) {
                         acc = true;   // read the record again for x's data
                         scan = false;
                         st = ST_REC;
-                        nxt = (const uint4*)P.rec + 2 * (vstart + ri);
                     } else {          // the 16-B record was kept in registers
                         emit = true;
                         xs = hxs; xd = hxd; xw = hxd;
@@ -234,9 +238,9 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                     draw = true;
                     ++a;
                 }
-            } else {
-                hk = sb + e == rend ? 2 * tstart : sb + e;
-                nxt = P.ehash + hk;
+            } else {   // full bucket without x: the next one, cyclically within t's buckets
+                const uint32_t base = (tstart >> 2) + tid;
+                idx = idx + 1 == base + (tdeg >> 2) + 1 ? base : idx + 1;
             }
         } else if (st == ST_NODE) {   // start node
             const bool h = (j & 4) != 0;
@@ -259,7 +263,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                     fin = true;
                 } else {
                     st = ST_NODE;
-                    nxt = P.nodes + start;
+                    idx = start;
                 }
             } else {
                 fin = true;
@@ -275,9 +279,8 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
             }
             if (hash) {
                 if (STATS) ++cnt[C_MEMB];
-                st = ST_HASH;
-                hk = 2 * tstart + (uint32_t)(((uint64_t)fmix32(x) * (2 * tdeg)) >> 32);
-                nxt = P.ehash + hk;
+                st = ST_HASH;   // home bucket of x among t's floor(deg t / 4) + 1 buckets
+                idx = (tstart >> 2) + tid + (uint32_t)(((uint64_t)fmix32(x) * ((tdeg >> 2) + 1)) >> 32);
             } else if (!ok) {
                 draw = true;
                 ++a;
@@ -287,7 +290,6 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                 acc = true;
                 scan = false;
                 st = ST_REC;
-                nxt = (const uint4*)P.rec + 2 * (vstart + ri);
             }
         }
 
@@ -320,7 +322,6 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
             w.finish(L);
             i += stride;
             st = i < P.num_walks ? ST_START : ST_DONE;
-            nxt = P.starts + (i < P.num_walks ? i : 0);
             draw = false;
         }
 
@@ -357,16 +358,13 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                 if (vdeg == 1) {
                     ri = 0;
                     st = ST_REC;
-                    nxt = (const uint4*)P.rec + 2 * vstart;
                 } else {
-                    const uint32_t kb = bounded32(dr.x64, P.G * vdeg);
+                    idx = bounded32(dr.x64, P.G * vdeg);   // guide bucket
                     st = ST_GUIDE;
-                    nxt = (const uint2*)P.guide + ((uint64_t)P.G * vstart + kb);
                 }
             } else {
                 ri = r;
                 st = ST_REC;
-                nxt = (const uint4*)P.rec + (vstart + r);
             }
         }
     }
