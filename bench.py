@@ -194,6 +194,12 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def _parse_layout(spec: str):
+    if not spec:
+        return None
+    return {k: int(float(v)) for k, v in (kv.split("=") for kv in spec.split(","))}
+
+
 def _walk_recipe(args):
     wk = config_walks(args.config)
     if args.mode:
@@ -209,7 +215,11 @@ def run_ours(args):
     wk = _walk_recipe(args)
     dev = torch.device("cuda", local)
     g = config_graph(k, device=dev)
-    dg = grape.graph_from_csr(g.off, g.col, g.w, device=local, symmetric=g.symmetric, tables=not args.no_tables)
+    torch.cuda.empty_cache()   # the generator's temporaries: room for the graph's tables
+    dg = grape.graph_from_csr(g.off, g.col, g.w, device=local, symmetric=g.symmetric, tables=not args.no_tables,
+                              layout=_parse_layout(args.layout))
+    g = g.to("cpu")            # the library holds its own copy; free the device CSR for the walk matrix
+    torch.cuda.empty_cache()
     info = dg.info
     W = g.n * wk["walks_per_node"]
     L = wk["L"]
@@ -283,7 +293,7 @@ def run_ours(args):
     # ---- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and not args.no_cpu and world == 1:
-        s, secs, walks, cores, att = _oracle_sample(g.to("cpu"), wk, args.cpu_budget)
+        s, secs, walks, cores, att = _oracle_sample(g, wk, args.cpu_budget)
         cpu = {"value": s / secs, "unit": "steps/s", "cores": cores, "kind": "oracle",
                "sample": f"first {walks} walks (wid 0..{walks - 1}) of the same workload, "
                          f"{cores} threads, {secs:.1f} s"}
@@ -295,25 +305,37 @@ def run_ours(args):
                                   walk_id_base=base, out=out)
         torch.cuda.synchronize(dev)
         weighted = info["cw_bytes"] > 0
-        # compulsory random sectors: one per node record, one col sector per proposal,
-        # one prefix-row leaf sector per weighted proposal, one N(t) leaf sector per
-        # membership test; plus the streamed walk matrix (4 B/entry) and starts (4 B/walk).
-        rand_sectors = ev["node_loads"] + ev["attempts"] * (2 if weighted else 1) + ev["membership_tests"]
+        if info.get("tables"):
+            # table walker: every read is one random 32-B sector that the
+            # rules force given the tables — the node record of a start, one guide entry
+            # or record per proposal whose x matters, the record of a taken arc, one
+            # edge-hash bucket per membership probe; attempts decided from registers
+            # read nothing.  (starts are read sequentially; counted as sectors too.)
+            rand_sectors = ev["sector_loads"]
+        else:
+            # fenced-search walker: one sector per node record, one col sector per
+            # proposal (+ one prefix leaf if weighted), one N(t) leaf per membership test
+            rand_sectors = ev["node_loads"] + ev["attempts"] * (2 if weighted else 1) + ev["membership_tests"]
         alg_bytes = 32 * rand_sectors + 4 * W * L + 4 * W
         t_launch = avg_launch_ms / 1e3
         peak, peak_src = _peaks()
         traffic = args.traffic_per_launch
         tfile = os.path.join(ROOT, "profiles", f"traffic_cfg{k}.json")
+        kname = "walk_tab_kernel" if info.get("tables") else "walk_sm_kernel"
         if traffic is None and os.path.exists(tfile):
-            traffic = json.load(open(tfile))["dram_bytes_per_launch"]
+            tj = json.load(open(tfile))
+            # only a capture of the same kernel and walk mode counts
+            if kname in tj.get("kernel", "") and tj.get("mode", wk["mode"]) == wk["mode"]:
+                traffic = tj["dram_bytes_per_launch"]
         ceil = None
         cfile = os.path.join(ROOT, "profiles", "gather_ceiling.json")
         if os.path.exists(cfile):
             ceil = json.load(open(cfile))["random_accesses_per_s"]
         achieved = alg_bytes / t_launch / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": "walk_sm_kernel (grape_walks_node2vec)" if node2vec
-                else "walk_sm_kernel (grape_walks_first_order)",
+                "traffic": traffic,
+                "kernel": ("walk_tab_kernel" if info.get("tables") else "walk_sm_kernel") +
+                          (" (grape_walks_node2vec)" if node2vec else " (grape_walks_first_order)"),
                 "peak_source": peak_src, "avg_launch_ms": avg_launch_ms,
                 "algorithmic_bytes_per_launch": alg_bytes,
                 "bytes_per_step": alg_bytes / max(ev["steps"], 1),
@@ -333,7 +355,9 @@ def run_ours(args):
                 "gpu_launches": args.steps, "realised_steps_per_gpu_step": steps_per_launch,
                 "nominal_steps_per_gpu_step": W * (L - 1), "wall_s_timed": t_wall,
                 "clocks": clocks, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-                "graph_device_bytes": info["device_bytes"]}
+                "graph_device_bytes": info["device_bytes"],
+                "graph_layout": {k_: info.get(k_) for k_ in ("tables", "guide_bytes", "guide_factor",
+                                                              "weights_symmetric", "table_bytes")}}
         print(json.dumps(line), flush=True)
     dg.free()
     if world > 1:
@@ -355,6 +379,8 @@ def main():
                     help="ncu dram bytes per launch of the walk kernel (from profiles/)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-tables", action="store_true", help="GRAPE_NO_TABLES: the v3 fenced-search walker")
+    ap.add_argument("--layout", default="", help="force table layout fields, e.g. "
+                    "record_bytes=16,guide_bytes=8,guide_factor=1,hash_h=6 (grape_table_options)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle baseline (profiling runs)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

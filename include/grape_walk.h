@@ -72,6 +72,25 @@ enum {
     GRAPE_NO_TABLES = 1u << 2
 };
 
+/*
+ * Sampling-table layout for grape_graph_from_csr_opts.  Every
+ * field 0 = automatic.  The automatic choice takes the first layout, in order
+ * of fewest reads per step, whose tables fit both the free device memory
+ * (leaving 10% of it) and table_budget_bytes (default 68e9 minus the node
+ * records: B200's random-gather rate collapses beyond ~68 GB of randomly read
+ * memory).  Forced values that do not fit give GRAPE_ENOMEM.
+ * The layout never changes a walk.
+ */
+typedef struct {
+    uint64_t table_budget_bytes; /* cap on rec + guide + hash bytes; 0 = automatic */
+    uint32_t record_bytes;       /* weighted: 32 (with the head's node record) or 16;
+                                    unweighted: 16 or 8 */
+    uint32_t guide_bytes;        /* weighted: 32 (unsplit buckets hold the record; needs
+                                    32-B records) or 8 */
+    uint32_t guide_factor;       /* weighted: guide buckets per arc, 1, 2 or 4 */
+    uint32_t hash_h;             /* edge-hash: one 8-slot bucket per H arcs (+1 per row), 4 or 6 */
+} grape_table_options;
+
 typedef struct {
     uint32_t num_nodes;
     uint64_t num_arcs;
@@ -86,6 +105,9 @@ typedef struct {
     uint32_t weights_symmetric; /* 1 if every arc with a reverse arc has its weight */
     uint64_t table_bytes;     /* part of device_bytes held by the tables */
     uint32_t guide_factor;    /* weighted tables: guide buckets per arc (4, 2 or 1 by free memory) */
+    uint32_t guide_bytes;     /* weighted tables: 32 (entries of unsplit buckets hold the record) or 8 */
+    uint32_t record_bytes;    /* tables: bytes per arc record */
+    uint32_t hash_h;          /* tables: arcs per edge-hash bucket (4 or 6) */
 } grape_graph_info;
 
 /*
@@ -115,6 +137,13 @@ grape_status grape_graph_from_csr(uint32_t num_nodes, uint64_t num_arcs,
                                   const uint64_t* row_offsets, const uint32_t* col_indices,
                                   const uint32_t* weights, int device, uint32_t flags,
                                   grape_graph** out);
+
+/* As grape_graph_from_csr, with the sampling-table layout given by *opts
+ * (NULL = automatic).  EINVAL for a field outside its listed values. */
+grape_status grape_graph_from_csr_opts(uint32_t num_nodes, uint64_t num_arcs,
+                                       const uint64_t* row_offsets, const uint32_t* col_indices,
+                                       const uint32_t* weights, int device, uint32_t flags,
+                                       const grape_table_options* opts, grape_graph** out);
 
 /* Synchronises the owning device, then frees the handle.  NULL is a no-op. */
 grape_status grape_graph_free(grape_graph* g);

@@ -85,10 +85,13 @@ class Graph:
 
 
 def graph_from_csr(row_offsets, col_indices, weights=None, *, device: int = 0,
-                   symmetric: bool = False, validate: bool = True, tables: bool = True) -> Graph:
+                   symmetric: bool = False, validate: bool = True, tables: bool = True,
+                   layout: dict | None = None) -> Graph:
     """grape_graph_from_csr: row_offsets u64/int64 [n+1], col_indices u32/int32 [m],
     weights u32/int32 [m] >= 1 or None.  Host or device tensors / numpy arrays.
-    tables=False passes GRAPE_NO_TABLES (v3 walker, less memory, same walks)."""
+    tables=False passes GRAPE_NO_TABLES (v3 walker, less memory, same walks);
+    layout: grape_table_options fields (table_budget_bytes, record_bytes, guide_bytes,
+    guide_factor, hash_h) to force parts of the table layout (grape_graph_from_csr_opts)."""
     off = _as_tensor(row_offsets, torch.int64)
     col = _as_tensor(col_indices, torch.int32)
     w = None if weights is None else _as_tensor(weights, torch.int32)
@@ -97,8 +100,12 @@ def graph_from_csr(row_offsets, col_indices, weights=None, *, device: int = 0,
     flags = ((GRAPE_SYMMETRIC if symmetric else 0) | (0 if validate else GRAPE_SKIP_VALIDATION)
              | (0 if tables else GRAPE_NO_TABLES))
     h = ctypes.c_void_p()
-    st = _lib.grape_graph_from_csr(n, m, off.data_ptr(), col.data_ptr() if m else None,
-                                   None if w is None else w.data_ptr(), device, flags, ctypes.byref(h))
+    opts = None
+    if layout:
+        opts = _capi.TableOptions(**layout)
+    st = _lib.grape_graph_from_csr_opts(n, m, off.data_ptr(), col.data_ptr() if m else None,
+                                        None if w is None else w.data_ptr(), device, flags,
+                                        None if opts is None else ctypes.byref(opts), ctypes.byref(h))
     _capi.check(_lib, st, "grape_graph_from_csr")
     return Graph(h.value, device)
 

@@ -20,7 +20,7 @@ GRAPE_PAD = 0xFFFFFFFF
 
 # Every entry point include/grape_walk.h declares (tests check the .so exports them all).
 EXPORTS = (
-    "grape_graph_from_csr", "grape_graph_free", "grape_graph_get_info",
+    "grape_graph_from_csr", "grape_graph_from_csr_opts", "grape_graph_free", "grape_graph_get_info",
     "grape_walks_first_order", "grape_walks_node2vec", "grape_walks_stats",
     "grape_status_string", "grape_last_error", "grape_version",
 )
@@ -41,6 +41,19 @@ class GraphInfo(ctypes.Structure):
         ("weights_symmetric", ctypes.c_uint32),
         ("table_bytes", ctypes.c_uint64),
         ("guide_factor", ctypes.c_uint32),
+        ("guide_bytes", ctypes.c_uint32),
+        ("record_bytes", ctypes.c_uint32),
+        ("hash_h", ctypes.c_uint32),
+    ]
+
+
+class TableOptions(ctypes.Structure):
+    _fields_ = [
+        ("table_budget_bytes", ctypes.c_uint64),
+        ("record_bytes", ctypes.c_uint32),
+        ("guide_bytes", ctypes.c_uint32),
+        ("guide_factor", ctypes.c_uint32),
+        ("hash_h", ctypes.c_uint32),
     ]
 
 
@@ -71,6 +84,9 @@ def load(path: str | None = None) -> ctypes.CDLL:
     vp, u32, u64, i32, dbl = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int, ctypes.c_double
     lib.grape_graph_from_csr.argtypes = [u32, u64, vp, vp, vp, i32, u32, ctypes.POINTER(vp)]
     lib.grape_graph_from_csr.restype = i32
+    lib.grape_graph_from_csr_opts.argtypes = [u32, u64, vp, vp, vp, i32, u32, ctypes.POINTER(TableOptions),
+                                              ctypes.POINTER(vp)]
+    lib.grape_graph_from_csr_opts.restype = i32
     lib.grape_graph_free.argtypes = [vp]
     lib.grape_graph_free.restype = i32
     lib.grape_graph_get_info.argtypes = [vp, ctypes.POINTER(GraphInfo)]

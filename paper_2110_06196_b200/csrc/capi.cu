@@ -203,9 +203,9 @@ using namespace grape;
 
 extern "C" {
 
-grape_status grape_graph_from_csr(uint32_t num_nodes, uint64_t num_arcs, const uint64_t* row_offsets,
-                                  const uint32_t* col_indices, const uint32_t* weights, int device,
-                                  uint32_t flags, grape_graph** out)
+grape_status grape_graph_from_csr_opts(uint32_t num_nodes, uint64_t num_arcs, const uint64_t* row_offsets,
+                                       const uint32_t* col_indices, const uint32_t* weights, int device,
+                                       uint32_t flags, const grape_table_options* opts, grape_graph** out)
 {
     g_err[0] = 0;
     if (out == nullptr) {
@@ -232,7 +232,30 @@ grape_status grape_graph_from_csr(uint32_t num_nodes, uint64_t num_arcs, const u
         set_error("device %d out of range (%d devices)", device, ndev);
         return GRAPE_EINVAL;
     }
-    return build_graph(num_nodes, num_arcs, row_offsets, col_indices, weights, device, flags, out);
+    grape_table_options o{};
+    if (opts != nullptr) {
+        o = *opts;
+        const bool w = weights != nullptr;
+        const uint32_t rb = o.record_bytes;
+        const bool rec_ok = rb == 0 || (w ? (rb == 32 || rb == 16) : (rb == 16 || rb == 8));
+        const bool gb_ok = o.guide_bytes == 0 || o.guide_bytes == 32 || o.guide_bytes == 8;
+        const bool g_ok = o.guide_factor == 0 || o.guide_factor == 1 || o.guide_factor == 2 || o.guide_factor == 4;
+        const bool h_ok = o.hash_h == 0 || o.hash_h == 4 || o.hash_h == 6;
+        if (!rec_ok || !gb_ok || !g_ok || !h_ok || (!w && (o.guide_bytes || o.guide_factor)) ||
+            (o.guide_bytes == 32 && rb == 16)) {
+            set_error("grape_table_options: a field is outside its allowed values for this graph");
+            return GRAPE_EINVAL;
+        }
+    }
+    return build_graph(num_nodes, num_arcs, row_offsets, col_indices, weights, device, flags, o, out);
+}
+
+grape_status grape_graph_from_csr(uint32_t num_nodes, uint64_t num_arcs, const uint64_t* row_offsets,
+                                  const uint32_t* col_indices, const uint32_t* weights, int device,
+                                  uint32_t flags, grape_graph** out)
+{
+    return grape_graph_from_csr_opts(num_nodes, num_arcs, row_offsets, col_indices, weights, device, flags,
+                                     nullptr, out);
 }
 
 grape_status grape_graph_free(grape_graph* g)
@@ -265,6 +288,9 @@ grape_status grape_graph_get_info(const grape_graph* g, grape_graph_info* info)
     info->weights_symmetric = g->wsym ? 1u : 0u;
     info->table_bytes = g->table_bytes;
     info->guide_factor = g->guide_factor;
+    info->guide_bytes = g->guide_bytes;
+    info->record_bytes = g->tables ? g->rec_bytes : 0;
+    info->hash_h = g->hash_h;
     return GRAPE_OK;
 }
 

@@ -202,7 +202,8 @@ void destroy_graph(grape_graph* g)
 }
 
 grape_status build_graph(uint32_t n, uint64_t m, const uint64_t* off_in, const uint32_t* col_in,
-                         const uint32_t* w_in, int device, uint32_t flags, grape_graph** out)
+                         const uint32_t* w_in, int device, uint32_t flags, const grape_table_options& opts,
+                         grape_graph** out)
 {
     DeviceGuard guard(device);
     cudaError_t e = cudaGetLastError();  // clear stale errors
@@ -316,6 +317,21 @@ grape_status build_graph(uint32_t n, uint64_t m, const uint64_t* off_in, const u
         else
             build_nodes<uint32_t><<<gn, 256>>>(g->off, nullptr, n, g->nodes);
         GRAPE_TRY_CUDA(cudaGetLastError(), "node records");
+    }
+    GRAPE_TRY_CUDA(cudaDeviceSynchronize(), "graph build");
+    cudaFree(w);   // the prefix sums hold everything the walkers need from the weights
+    w = nullptr;
+    if (!(flags & GRAPE_NO_TABLES)) {
+        st = build_tables(g, opts);
+        if (st != GRAPE_OK) return fail(st);
+        GRAPE_TRY_CUDA(cudaDeviceSynchronize(), "table build");
+    }
+    if (g->tables) {   // the table walker reads only nodes / rec / guide / ehash
+        cudaFree(g->col);
+        cudaFree(g->cw);
+        g->col = nullptr;
+        g->cw = nullptr;
+    } else {           // fence levels for the v3 walker
         fence_bytes = 0;
         uint64_t len = m;
         for (int l = 0; l < kFenceLevels; ++l) {
@@ -345,27 +361,8 @@ grape_status build_graph(uint32_t n, uint64_t m, const uint64_t* off_in, const u
             }
         }
         GRAPE_TRY_CUDA(cudaGetLastError(), "fence levels");
+        GRAPE_TRY_CUDA(cudaDeviceSynchronize(), "fence levels");
     }
-    GRAPE_TRY_CUDA(cudaDeviceSynchronize(), "graph build");
-    if (!(flags & GRAPE_NO_TABLES)) {
-        st = build_tables(g);
-        if (st != GRAPE_OK) return fail(st);
-        GRAPE_TRY_CUDA(cudaDeviceSynchronize(), "table build");
-    }
-    if (g->tables) {   // the table walker reads only nodes / rec / guide / ehash
-        cudaFree(g->col);
-        cudaFree(g->cw);
-        g->col = nullptr;
-        g->cw = nullptr;
-        for (int l = 0; l < kFenceLevels; ++l) {
-            cudaFree(g->col_fence[l]);
-            cudaFree(g->cw_fence[l]);
-            g->col_fence[l] = nullptr;
-            g->cw_fence[l] = nullptr;
-        }
-    }
-    cudaFree(w);
-    w = nullptr;
     cudaFree(d_bad);
     cudaFree(d_maxw);
     cudaFree(d_maxdeg);

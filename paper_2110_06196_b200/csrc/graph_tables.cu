@@ -15,8 +15,9 @@
 //          With it the walker knows, at x coming from v, which draws propose
 //          x' == v (the "return" class p) without reading anything, and
 //          it has x's node record without a second read.
-//   guide  weighted rows only, B_v = G deg(v) 8-B entries at G off[v] (G = 4, 2
-//          or 1 by free memory): entry kb covers the x64 draws with
+//   guide  weighted rows only, B_v = G deg(v) entries at G off[v] (G = 4, 2 or 1,
+//          32-B "fat" or 8-B "slim" entries, by free memory; a fat entry of an
+//          unsplit bucket is a copy of the record): entry kb covers the x64 draws with
 //          floor(x64 * B_v / 2^64) = kb; it holds i_lo = the proposal index of
 //          the smallest such draw, and either the proposal col[i_lo] itself
 //          (every draw of the bucket proposes i_lo) or, for a "split" bucket,
@@ -33,6 +34,7 @@
 // bits 30-31, G deg < 2^32), row sums < 2^32 (u32 prefix).  When the tables are
 // built, col / cw / fences are released (graph.cu): nothing reads them after.  Outside them the tables are not built and
 // the v3 walker (fenced searches) runs.
+#include <algorithm>
 #include <cstring>
 #include "internal.h"
 
@@ -76,7 +78,7 @@ __device__ inline uint64_t upper_bound_u32(const uint32_t* __restrict__ cw, uint
 // One warp per row, lanes over the row's arcs.  Each record also carries the
 // node record of its head x (start, degree, W_x), so a walk that takes the arc
 // needs no separate node load.
-template <bool WEIGHTED>
+template <bool WEIGHTED, bool COMPACT>
 __global__ void build_records(const uint64_t* __restrict__ off, const uint32_t* __restrict__ col,
                               const uint32_t* __restrict__ cw, uint32_t n, void* __restrict__ rec,
                               unsigned* __restrict__ asym)
@@ -101,13 +103,20 @@ __global__ void build_records(const uint64_t* __restrict__ off, const uint32_t* 
                     rhi = cw[j];
                     bad |= (rhi - rlo) != own_hi - own_lo;
                 }
-                const uint32_t xW = xb > xa ? cw[xb - 1] : 0u;
-                uint4* r = reinterpret_cast<uint4*>(rec) + 2 * e;
-                r[0] = make_uint4(x, own_hi, rlo, rhi);
-                r[1] = make_uint4((uint32_t)xa, (uint32_t)(xb - xa), xW, own_lo);
+                if (COMPACT) {
+                    reinterpret_cast<uint4*>(rec)[e] = make_uint4(x, own_hi, rlo, rhi);
+                } else {
+                    const uint32_t xW = xb > xa ? cw[xb - 1] : 0u;
+                    uint4* r = reinterpret_cast<uint4*>(rec) + 2 * e;
+                    r[0] = make_uint4(x, own_hi, rlo, rhi);
+                    r[1] = make_uint4((uint32_t)xa, (uint32_t)(xb - xa), xW, own_lo);
+                }
             } else {
-                reinterpret_cast<uint4*>(rec)[e] =
-                    make_uint4(x, found ? (uint32_t)(j - xa) : kNone, (uint32_t)xa, (uint32_t)(xb - xa));
+                const uint32_t rev = found ? (uint32_t)(j - xa) : kNone;
+                if (COMPACT)
+                    reinterpret_cast<uint2*>(rec)[e] = make_uint2(x, rev);
+                else
+                    reinterpret_cast<uint4*>(rec)[e] = make_uint4(x, rev, (uint32_t)xa, (uint32_t)(xb - xa));
             }
         }
     }
@@ -147,25 +156,62 @@ __global__ void build_guide(const uint64_t* __restrict__ off, const uint32_t* __
     }
 }
 
+// Fat guide (32-B entries, one sector): an unsplit bucket holds a copy of the
+// record of its proposal i_lo (so a proposal from it needs no other read), with
+// bits 30-31 of word 5 (the degree of x, < 2^29) clear; a split bucket holds
+// {i_lo, cw[i_lo], 0, 0, 0, SPLIT | MULTI<<30, 0, 0}.
+__global__ void build_guide_fat(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cw, uint32_t n,
+                                uint32_t G, const uint4* __restrict__ rec, uint4* __restrict__ guide)
+{
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t v = warp; v < n; v += nwarps) {
+        const uint64_t lo = off[v], hi = off[v + 1], deg = hi - lo;
+        if (deg == 0) continue;
+        const uint64_t B = G * deg;
+        const uint64_t W = cw[hi - 1];
+        uint64_t Q = ~0ull / B, R = ~0ull % B + 1;
+        if (R == B) { ++Q; R = 0; }
+        for (uint64_t kb = lane; kb < B; kb += 32) {
+            const uint64_t xmin = kb * Q + (kb * R + B - 1) / B;
+            const uint64_t xmax = kb + 1 == B ? ~0ull : (kb + 1) * Q + ((kb + 1) * R + B - 1) / B - 1;
+            const uint32_t rmin = (uint32_t)__umul64hi(xmin, W), rmax = (uint32_t)__umul64hi(xmax, W);
+            const uint64_t i = upper_bound_u32(cw, lo, hi, rmin) - lo;
+            const bool split = cw[lo + i] <= rmax;
+            const bool multi = split && cw[lo + i + 1] <= rmax;
+            uint4* d = guide + 2 * (G * lo + kb);
+            if (split) {
+                d[0] = make_uint4((uint32_t)i, cw[lo + i], 0u, 0u);
+                d[1] = make_uint4(0u, 0x80000000u | (multi ? 0x40000000u : 0u), 0u, 0u);
+            } else {
+                d[0] = rec[2 * (lo + i)];
+                d[1] = rec[2 * (lo + i) + 1];
+            }
+        }
+    }
+}
+
 // Bucketised sets: row v owns the 8-slot buckets [B_v, B_v + nb_v), B_v =
-// floor(off[v] / 4) + v, nb_v = floor(deg v / 4) + 1 (>= 2 deg slots, disjoint
-// across rows, derivable from the node record).  x goes to the first empty slot
+// floor(off[v] / H) + v, nb_v = floor(deg v / H) + 1, H = 4 (load <= 1/2) or 6
+// (<= 3/4): disjoint across rows since floor((a + d) / H) - floor(a / H) >=
+// floor(d / H), and derivable from the node record.  x goes to the first empty slot
 // of bucket B_v + floor(fmix32(x) nb_v / 2^32), or of the next non-full bucket
 // (cyclically): a bucket that an item skipped is full forever (no deletions),
 // so a lookup may stop at the first bucket holding x or an empty slot.
 __global__ void build_ehash(const uint64_t* __restrict__ off, const uint32_t* __restrict__ col, uint32_t n,
-                            uint32_t* __restrict__ ehash)
+                            uint32_t H, uint32_t* __restrict__ ehash)
 {
     const unsigned lane = threadIdx.x & 31;
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t v = warp; v < n; v += nwarps) {
         const uint64_t lo = off[v], hi = off[v + 1];
-        const uint64_t base = (lo >> 2) + v, nb = ((hi - lo) >> 2) + 1;
+        const uint64_t base = lo / H + v, nb = (hi - lo) / H + 1;
         for (uint64_t e = lo + lane; e < hi; e += 32) {
             const uint32_t x = col[e];
             uint64_t b = ((uint64_t)fmix32(x) * nb) >> 32;
-            for (;;) {
+            for (uint64_t tries = 0; tries < nb; ++tries) {   // nb * 8 slots >= deg + 1 > items: ends
                 uint32_t* slot = ehash + 8 * (base + b);
                 int q = 0;
                 while (q < 8 && atomicCAS(slot + q, kEmpty, x) != kEmpty) ++q;
@@ -197,15 +243,24 @@ void destroy_tables(grape_graph* g)
     g->guide = nullptr;
     g->ehash = nullptr;
     g->guide_factor = 0;
+    g->guide_bytes = 0;
+    g->hash_h = 0;
+    g->compact = false;
     g->tables = false;
     g->table_bytes = 0;
 }
 
-grape_status build_tables(grape_graph* g)
+// Random-sector gather rate falls off a cliff once the randomly read footprint
+// exceeds ~68 GB on B200 (36 G sectors/s up to 68 GB, 28 at 80 GB, 10.5 at 128 GB;
+// tools/gather_footprint.cu, profiles/gather_footprint.txt; page size does not
+// move it, tools/gather_vmm.cu).  The layout is chosen to stay below it.
+constexpr double kReachBytes = 68e9;
+
+grape_status build_tables(grape_graph* g, const grape_table_options& o)
 {
-    const uint64_t m = g->m;
+    const uint64_t m = g->m, n = g->n;
     const bool weighted = g->cw_bytes != 0;
-    if (2 * m >= (1ull << 32) - 64 || (m >> 2) + g->n + 2 >= (1ull << 32) || g->max_degree >= (1u << 29) ||
+    if (2 * m >= (1ull << 32) - 64 || (m >> 2) + n + 2 >= (1ull << 32) || g->max_degree >= (1u << 29) ||
         g->cw_bytes == 8)
         return GRAPE_OK;
     cudaError_t e = cudaSuccess;
@@ -215,25 +270,70 @@ grape_status build_tables(grape_graph* g)
         destroy_tables(g);
         return cuda_fail(err, what);
     };
-    g->rec_bytes = weighted ? 32 : 16;
-    const uint64_t rec_b = padded(m * g->rec_bytes), hash_b = padded(((m >> 2) + g->n + 1) * 32);
-    // Guide factor G (buckets per arc): 4 / 2 / 1, the largest whose tables leave
-    // room on the device (the caller still needs its walk matrices); results do
-    // not depend on it, only the share of split buckets does.
+    // Layout, in order of preference (fewest reads per step first): records
+    // with the head's node record (32 / 16 B) or compact (16 / 8 B, the head's
+    // node record read separately); fat (32-B) or slim (8-B) guide entries with
+    // G = 4 / 2 / 1 buckets per arc; edge-hash load 1/2 (H = 4) or 3/4 (H = 6).
+    // The first that fits both the device (leaving 10% free: the caller still
+    // needs its walk matrices) and the gather reach wins (grape_table_options
+    // may force any part).  Results do not depend on the choice; the number and
+    // spread of the reads do.
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
-    uint32_t G = 0;
-    if (weighted) {
-        for (uint32_t c = 4; c >= 1; c >>= 1) {
-            const uint64_t need = rec_b + hash_b + padded(c * m * 8);
-            if (c * m < (1ull << 32) && need <= (c == 1 ? 0.9 : 0.5) * (double)free_b) { G = c; break; }
+    const double base_b = (double)(n + 1) * 8 + (double)n * sizeof(NodeRec);
+    const double cap = o.table_budget_bytes ? (double)o.table_budget_bytes : kReachBytes - base_b;
+    const double budget = std::min((double)free_b - 0.1 * (double)total_b, cap);
+    struct Choice { uint32_t rec, gb, G, H; };
+    Choice c{0, 0, 0, 0};
+    auto size_of = [&](const Choice& k) {
+        return (double)padded(m * k.rec) + (double)padded(((m / k.H) + n + 1) * 32) +
+               (weighted ? (double)padded((uint64_t)k.G * m * k.gb) : 0.0);
+    };
+    auto allowed = [&](const Choice& k) {
+        return (!o.record_bytes || o.record_bytes == k.rec) && (!o.guide_bytes || o.guide_bytes == k.gb) &&
+               (!o.guide_factor || o.guide_factor == k.G) && (!o.hash_h || o.hash_h == k.H);
+    };
+    bool found = false, any_allowed = false;
+    const uint32_t recs_w[2] = {32u, 16u}, recs_u[2] = {16u, 8u};
+    const uint32_t gbs_w[2] = {32u, 8u}, gbs_u[1] = {0u};
+    const uint32_t Gs_w[3] = {4u, 2u, 1u}, Gs_u[1] = {0u};
+    const uint32_t Hs[2] = {4u, 6u};
+    const uint32_t* recs = weighted ? recs_w : recs_u;
+    const uint32_t* gbs = weighted ? gbs_w : gbs_u;
+    const uint32_t* Gs = weighted ? Gs_w : Gs_u;
+    const int ngb = weighted ? 2 : 1, nG = weighted ? 3 : 1;
+    for (int hi = 0; hi < 2; ++hi) {
+        for (int ri = 0; ri < 2; ++ri) {
+            for (int gi = 0; gi < ngb; ++gi) {
+                if (gbs[gi] == 32 && recs[ri] != 32) continue;   // fat entries copy full records
+                for (int fi = 0; fi < nG; ++fi) {
+                    const Choice k{recs[ri], gbs[gi], Gs[fi], Hs[hi]};
+                    if (found || !allowed(k)) continue;
+                    any_allowed = true;
+                    if ((!weighted || (uint64_t)k.G * m < (1ull << 32)) && size_of(k) <= budget) {
+                        c = k;
+                        found = true;
+                    }
+                }
+            }
         }
-        if (G == 0) return GRAPE_OK;   // does not fit: v3 walker
-    } else if (rec_b + hash_b > 0.9 * (double)free_b) {
-        return GRAPE_OK;
     }
-    g->guide_factor = G;
-    const uint64_t guide_b = weighted ? padded(G * m * 8) : 0;
+    const bool forced = o.record_bytes || o.guide_bytes || o.guide_factor || o.hash_h;
+    if (!found) {
+        if (forced && any_allowed) {
+            set_error("the requested table layout does not fit (%.3g bytes available)", budget);
+            return GRAPE_ENOMEM;
+        }
+        return GRAPE_OK;   // does not fit: v3 walker
+    }
+    g->rec_bytes = c.rec;
+    g->compact = weighted ? c.rec == 16 : c.rec == 8;
+    g->guide_factor = c.G;
+    g->guide_bytes = c.gb;
+    g->hash_h = c.H;
+    const uint64_t rec_b = padded(m * c.rec), hash_b = padded(((m / c.H) + n + 1) * 32);
+    const uint64_t guide_b = weighted ? padded((uint64_t)c.G * m * c.gb) : 0;
+    const uint32_t G = c.G, gbytes = c.gb;
     if ((e = cudaMalloc(&g->rec, rec_b)) != cudaSuccess) return fail(e, "cudaMalloc arc records");
     if (weighted && (e = cudaMalloc((void**)&g->guide, guide_b)) != cudaSuccess) return fail(e, "cudaMalloc guide");
     if ((e = cudaMalloc((void**)&g->ehash, hash_b)) != cudaSuccess) return fail(e, "cudaMalloc edge hash");
@@ -244,12 +344,22 @@ grape_status build_tables(grape_graph* g)
     if (weighted) cudaMemset(g->guide, 0, guide_b);
     const int grid = rows_grid(g->n);
     if (weighted) {
-        build_records<true><<<grid, kThreads>>>(g->off, g->col, (const uint32_t*)g->cw, g->n, g->rec, d_asym);
-        build_guide<<<grid, kThreads>>>(g->off, g->col, (const uint32_t*)g->cw, g->n, G, (uint2*)g->guide);
+        if (g->compact)
+            build_records<true, true><<<grid, kThreads>>>(g->off, g->col, (const uint32_t*)g->cw, g->n, g->rec, d_asym);
+        else
+            build_records<true, false><<<grid, kThreads>>>(g->off, g->col, (const uint32_t*)g->cw, g->n, g->rec, d_asym);
+        if (gbytes == 32)
+            build_guide_fat<<<grid, kThreads>>>(g->off, (const uint32_t*)g->cw, g->n, G, (const uint4*)g->rec,
+                                                (uint4*)g->guide);
+        else
+            build_guide<<<grid, kThreads>>>(g->off, g->col, (const uint32_t*)g->cw, g->n, G, (uint2*)g->guide);
     } else {
-        build_records<false><<<grid, kThreads>>>(g->off, g->col, nullptr, g->n, g->rec, d_asym);
+        if (g->compact)
+            build_records<false, true><<<grid, kThreads>>>(g->off, g->col, nullptr, g->n, g->rec, d_asym);
+        else
+            build_records<false, false><<<grid, kThreads>>>(g->off, g->col, nullptr, g->n, g->rec, d_asym);
     }
-    build_ehash<<<grid, kThreads>>>(g->off, g->col, g->n, g->ehash);
+    build_ehash<<<grid, kThreads>>>(g->off, g->col, g->n, g->hash_h, g->ehash);
     if ((e = cudaGetLastError()) != cudaSuccess) return fail(e, "table kernels");
     unsigned asym = 0;
     if ((e = cudaMemcpy(&asym, d_asym, 4, cudaMemcpyDeviceToHost)) != cudaSuccess) return fail(e, "table build");

@@ -37,10 +37,13 @@ struct grape_graph {
     // or when the graph exceeds their index ranges (then the v3 walker runs):
     bool tables;          // rec / guide / ehash below are built
     bool wsym;            // every arc with a reverse arc has the reverse's weight
-    uint32_t rec_bytes;   // 16 (unweighted) or 32 (weighted), graph_tables.cu
+    uint32_t rec_bytes;   // 32 / 16 (weighted: full / compact), 16 / 8 (unweighted), graph_tables.cu
     void* rec;            // per-arc records, arc order
     uint32_t* guide;      // weighted: G*deg(v) 8-B guide entries per row at G*off[v]
     uint32_t guide_factor;   // G (buckets per arc) of the guide
+    uint32_t guide_bytes;    // 32 (fat: unsplit buckets hold a record copy) or 8 (slim)
+    uint32_t hash_h;         // edge-hash buckets: floor(deg / H) + 1 per row (H = 4 or 6)
+    bool compact;            // records without the head's node record (16 B weighted / 8 B)
     uint32_t* ehash;      // per-row linear-probing sets of N(v): 2*deg(v) slots at 2*off[v]
     uint64_t table_bytes;
     uint32_t max_degree;
@@ -82,12 +85,13 @@ cudaError_t launch_walks_sm(const grape_graph* g, const WalkArgs& a, bool node2v
 
 // graph.cu
 grape_status build_graph(uint32_t n, uint64_t m, const uint64_t* off, const uint32_t* col,
-                         const uint32_t* w, int device, uint32_t flags, grape_graph** out);
+                         const uint32_t* w, int device, uint32_t flags, const grape_table_options& opts,
+                         grape_graph** out);
 void destroy_graph(grape_graph* g);
 // graph_tables.cu: build rec / guide / ehash for a validated graph whose off,
 // col (and cw when weighted) are on the device.  Leaves g->tables false (and
 // returns GRAPE_OK) when the graph is outside the tables' index ranges.
-grape_status build_tables(grape_graph* g);
+grape_status build_tables(grape_graph* g, const grape_table_options& opts);
 void destroy_tables(grape_graph* g);
 
 }  // namespace grape

@@ -35,6 +35,9 @@ using namespace walk;
 enum : uint32_t { ST_START = 0, ST_NODE, ST_GUIDE, ST_REC, ST_HASH, ST_DRAW, ST_BACK, ST_DONE };
 
 constexpr uint32_t kEmptySlot = 0xFFFFFFFFu;
+#ifndef GRAPE_TAB_DRAWS
+#define GRAPE_TAB_DRAWS 2
+#endif
 #ifndef GRAPE_TAB_MIN_BLOCKS
 #define GRAPE_TAB_MIN_BLOCKS 4
 #endif
@@ -45,6 +48,8 @@ struct TabParams {
     const uint32_t* guide;    // 8-B entries
     const uint32_t* ehash;
     uint32_t G;               // guide buckets per arc
+    uint32_t h_mul, h_shift;  // floor(v / H) = umulhi(v, h_mul) >> h_shift (edge-hash buckets)
+    bool wsym;                // weighted: reverse arcs carry equal weights
     uint32_t n;
     const uint32_t* starts;
     uint64_t num_walks;
@@ -104,7 +109,7 @@ enum : int { C_LOADS = 0, C_NODE, C_XNODE, C_CWPROBE, C_COLPROBE, C_REC, C_ATTEM
              C_GUIDE, C_HASH, C_ALU };
 
 // WEIGHTED: 32-B records + guide; else 16-B records indexed by the draw.
-template <bool WEIGHTED, bool NODE2VEC, bool NEED_MEMBER, bool STATS>
+template <bool WEIGHTED, bool FAT, bool COMPACT, bool NODE2VEC, bool NEED_MEMBER, bool STATS>
 __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(const __grid_constant__ TabParams P)
 {
     uint32_t cnt[kStatsWords];
@@ -119,7 +124,10 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t st = i < P.num_walks ? ST_START : ST_DONE;
-    uint32_t idx = 0;   // what the next load reads: NODE node id, GUIDE bucket, HASH bucket (REC: ri)
+    auto divH = [&](uint32_t v) { return __umulhi(v, P.h_mul) >> P.h_shift; };   // floor(v / H)
+    uint32_t idx = 0;   // what the next load reads: NODE node id, GUIDE bucket (REC: ri, HASH: hb)
+    uint32_t hb = 0;    // edge-hash bucket (absolute index)
+    bool gsrc = false;  // fat guide: the proposal's record is the guide entry idx
     unsigned long long steps = 0;
 
     uint32_t s = 0, a = 0;
@@ -143,10 +151,11 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
         {   // the one load of this iteration: a single address computation for every state
             const bool rec = st == ST_REC, gd = st == ST_GUIDE, nd = st == ST_NODE;
             const uint32_t mul = rec ? 1u : gd ? P.G : 0u;
-            uint64_t e = (uint64_t)mul * vstart + (rec ? ri : idx);
+            uint64_t e = (uint64_t)mul * vstart + (rec ? ri : st == ST_HASH ? hb : idx);
             const char* b = rec ? (const char*)P.rec : gd ? (const char*)P.guide
                           : nd ? (const char*)P.nodes : (const char*)P.ehash;
-            uint32_t sh = rec ? (WEIGHTED ? 5u : 4u) : gd ? 3u : nd ? 4u : 5u;
+            constexpr uint32_t RSH = (WEIGHTED ? 5u : 4u) - (COMPACT ? 1u : 0u);   // log2 record bytes
+            uint32_t sh = rec ? RSH : gd ? (FAT ? 5u : 3u) : nd ? 4u : 5u;
             if (st == ST_START) {
                 b = (const char*)P.starts;
                 e = i;
@@ -170,9 +179,24 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
         // the record of the taken arc (valid when emit): head x, its node record,
         // the new T = [nlo, nhi) and S = [nslo, nshi)
         uint32_t xs = 0, xd = 0, xw = 0, nlo = 0, nhi = 0, nslo = 0, nshi = 0;
+        bool have_rec = false;   // the sector in hand is x's record
         if (st == ST_REC) {
+            have_rec = true;
             bool found = true;
-            if constexpr (WEIGHTED) {
+            if constexpr (WEIGHTED && COMPACT) {   // 16-B {x, hi, rlo, rhi} at word j (0 or 4)
+                const bool h = (j & 4) != 0;
+                const uint32_t hi = h ? sec[5] : sec[1];
+                if (scan && r >= hi) {   // past this record's interval: the next one
+                    found = false;
+                    ++ri;
+                }
+                x = h ? sec[4] : sec[0];
+                nlo = h ? sec[6] : sec[2];
+                nhi = h ? sec[7] : sec[3];
+                nshi = hi;
+                nslo = P.wsym ? hi - (nhi - nlo) : 1u;   // [1, 0): unknown (asymmetric weights)
+                if (!P.wsym) nshi = 0;
+            } else if constexpr (WEIGHTED) {
                 if (scan && r >= sec[1]) {   // past this record's interval: the next one
                     found = false;
                     ++ri;
@@ -181,6 +205,14 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                 nlo = sec[2]; nhi = sec[3];
                 xs = sec[4]; xd = sec[5]; xw = sec[6];
                 nslo = sec[7]; nshi = sec[1];
+            } else if constexpr (COMPACT) {   // 8-B {x, rev} at word j (even)
+                x = pick8(sec, j);
+                const uint32_t rev = pick8(sec, j | 1);
+                hrev = rev;
+                nlo = rev;
+                nhi = rev == kNone ? rev : rev + 1;
+                nslo = ri;
+                nshi = ri + 1;
             } else {
                 const bool h = (j & 4) != 0;
                 x = h ? sec[4] : sec[0];
@@ -199,9 +231,19 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                 else decide = true;
             }
         } else if (st == ST_GUIDE) {
-            const uint32_t e0 = pick8(sec, j), e1 = pick8(sec, j | 1);   // 8-B entry at word j (even)
-            ri = e0 & 0x3FFFFFFFu;
-            if (e0 >> 31) {   // split bucket: r against the upper end of i_lo's interval
+            uint32_t e0, e1;
+            bool split;
+            if constexpr (FAT) {   // unsplit: a record copy; split: {i_lo, cw[i_lo], .., flags in word 5}
+                split = (sec[5] >> 31) != 0;
+                e0 = sec[0] | (sec[5] & 0xC0000000u);
+                e1 = sec[1];
+            } else {
+                e0 = pick8(sec, j);   // 8-B entry at word j (even)
+                e1 = pick8(sec, j | 1);
+                split = (e0 >> 31) != 0;
+            }
+            if (split) {      // split bucket: r against the upper end of i_lo's interval
+                ri = e0 & 0x3FFFFFFFu;
                 scan = false;
                 if (r >= e1) {
                     ++ri;
@@ -209,7 +251,17 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                 }
                 acc = false;
                 st = ST_REC;
+            } else if constexpr (FAT) {   // the bucket's proposal, with its whole record
+                have_rec = true;
+                gsrc = true;
+                x = sec[0];
+                nlo = sec[2]; nhi = sec[3];
+                xs = sec[4]; xd = sec[5]; xw = sec[6];
+                nslo = sec[7]; nshi = sec[1];
+                if (acc) emit = true;
+                else decide = true;
             } else {          // the bucket proposes i_lo = e1 whatever the draw
+                ri = e0 & 0x3FFFFFFFu;
                 x = e1;
                 decide = true;
             }
@@ -225,10 +277,10 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                     if constexpr (WEIGHTED) {
                         acc = true;   // read the record again for x's data
                         scan = false;
-                        st = ST_REC;
-                    } else {          // the 16-B record was kept in registers
+                        st = gsrc ? ST_GUIDE : ST_REC;
+                    } else {          // the record was kept in registers
                         emit = true;
-                        xs = hxs; xd = hxd; xw = hxd;
+                        xs = hxs; xd = hxd; xw = hxd;   // (compact: unused, x's node record is read)
                         nlo = hrev;
                         nhi = hrev == kNone ? hrev : hrev + 1;
                         nslo = ri;
@@ -239,8 +291,8 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                     ++a;
                 }
             } else {   // full bucket without x: the next one, cyclically within t's buckets
-                const uint32_t base = (tstart >> 2) + tid;
-                idx = idx + 1 == base + (tdeg >> 2) + 1 ? base : idx + 1;
+                const uint32_t base = divH(tstart) + tid;
+                hb = hb + 1 == base + divH(tdeg) + 1 ? base : hb + 1;
             }
         } else if (st == ST_NODE) {   // start node
             const bool h = (j & 4) != 0;
@@ -279,12 +331,12 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
             }
             if (hash) {
                 if (STATS) ++cnt[C_MEMB];
-                st = ST_HASH;   // home bucket of x among t's floor(deg t / 4) + 1 buckets
-                idx = (tstart >> 2) + tid + (uint32_t)(((uint64_t)fmix32(x) * ((tdeg >> 2) + 1)) >> 32);
+                st = ST_HASH;   // home bucket of x among t's floor(deg t / H) + 1 buckets
+                hb = divH(tstart) + tid + (uint32_t)(((uint64_t)fmix32(x) * (divH(tdeg) + 1)) >> 32);
             } else if (!ok) {
                 draw = true;
                 ++a;
-            } else if (st == ST_REC) {
+            } else if (have_rec) {
                 emit = true;      // the record is in hand
             } else {              // x came from the guide: read its record
                 acc = true;
@@ -299,9 +351,19 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
         if (emit || back) {
             w.put(s, x);
             ++steps;
-            if (emit) {
+            bool need_node = false;
+            if (emit && !(COMPACT && x == tid)) {
                 tid = vid; tstart = vstart; tdeg = vdeg; tW = vW;
-                vid = x; vstart = xs; vdeg = xd; vW = xw;
+                vid = x;
+                if constexpr (COMPACT) need_node = true;   // x's node record: next iteration
+                else { vstart = xs; vdeg = xd; vW = xw; }
+                tlo = nlo; thi = nhi; slo = nslo; shi = nshi;
+            } else if (emit) {   // compact record of a return: t's node record is in registers
+                uint32_t q;
+                q = vstart; vstart = tstart; tstart = q;
+                q = vdeg; vdeg = tdeg; tdeg = q;
+                q = vW; vW = tW; tW = q;
+                q = vid; vid = tid; tid = q;
                 tlo = nlo; thi = nhi; slo = nslo; shi = nshi;
             } else {   // x = t: v and t swap, and so do T and S
                 uint32_t q;
@@ -314,8 +376,16 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
             }
             ++s;
             a = 0;
-            fin = s == L || vdeg == 0;
-            draw = !fin;
+            if (need_node) {
+                fin = s == L;
+                if (!fin) {
+                    st = ST_NODE;
+                    idx = x;
+                }
+            } else {
+                fin = s == L || vdeg == 0;
+                draw = !fin;
+            }
         }
         if (fin) {
             for (uint32_t q = s; q < L; ++q) w.put(q, kPad);
@@ -325,48 +395,73 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
             draw = false;
         }
 
-        // ---- one draw per lane per iteration: Philox, the band of u, and the
-        // decisions that need no read (§8(c) c12)
-        __syncwarp();
-        if (draw) {
-            if (STATS) ++cnt[C_ATTEMPT];
-            const Draw dr = philox_draw_rk(P.rk, P.base + i, s, a);
-            u = dr.u;
-            r = bounded32(dr.x64, vW);   // index (unweighted: vW = deg) or weight point
-            bool need_x = true, ret = false;
-            if (NODE2VEC && tid != kNone) {
-                const bool cp = u <= P.tp_m1, c1 = u <= P.t1_m1, cq = u <= P.tq_m1;
-                if (cp == c1 && c1 == cq) {
-                    need_x = cp;
-                } else if (c1 == cq && tlo <= thi) {   // only "x == t" matters, and it is known
-                    const bool is_t = r - tlo < thi - tlo;
-                    const bool ok = is_t ? cp : c1;
-                    need_x = ok && !is_t;
-                    ret = ok && is_t;
+        // ---- draws: Philox, the band of u, and the decisions that need no read
+        // (§8(c) c12).  A lane whose attempt is decided from registers draws again
+        // in the same iteration, up to GRAPE_TAB_DRAWS draws; a register-decided
+        // return x = t is emitted on the spot when another draw follows it.
+#pragma unroll 1
+        for (int k = 0; k < GRAPE_TAB_DRAWS; ++k) {
+            __syncwarp();
+            if (!__any_sync(0xffffffffu, draw)) break;
+            if (draw) {
+                if (STATS) ++cnt[C_ATTEMPT];
+                const Draw dr = philox_draw_rk(P.rk, P.base + i, s, a);
+                u = dr.u;
+                r = bounded32(dr.x64, vW);   // index (unweighted: vW = deg) or weight point
+                bool need_x = true, ret = false;
+                if (NODE2VEC && tid != kNone) {
+                    const bool cp = u <= P.tp_m1, c1 = u <= P.t1_m1, cq = u <= P.tq_m1;
+                    if (cp == c1 && c1 == cq) {
+                        need_x = cp;
+                    } else if (c1 == cq && tlo <= thi) {   // only "x == t" matters, and it is known
+                        const bool is_t = r - tlo < thi - tlo;
+                        const bool ok = is_t ? cp : c1;
+                        need_x = ok && !is_t;
+                        ret = ok && is_t;
+                    }
+                    if (STATS) cnt[C_ALU] += !need_x;
                 }
-                if (STATS) cnt[C_ALU] += !need_x;
-            }
-            acc = false;
-            scan = false;
-            if (ret) {          // return to t: emitted next iteration, no read
-                x = tid;
-                st = ST_BACK;
-            } else if (!need_x) {
-                ++a;            // rejected without reading the graph
-                st = ST_DRAW;
-            } else if constexpr (WEIGHTED) {
-                if (vdeg == 1) {
-                    ri = 0;
-                    st = ST_REC;
+                acc = false;
+                scan = false;
+                gsrc = false;
+                draw = false;
+                if (ret) {          // return to t, no read
+                    if (k + 1 < GRAPE_TAB_DRAWS && s + 1 < L) {   // emit now; t's row is not empty
+                        w.put(s, tid);
+                        ++steps;
+                        uint32_t q;
+                        q = vstart; vstart = tstart; tstart = q;
+                        q = vdeg; vdeg = tdeg; tdeg = q;
+                        q = vW; vW = tW; tW = q;
+                        q = vid; vid = tid; tid = q;
+                        q = tlo; tlo = slo; slo = q;
+                        q = thi; thi = shi; shi = q;
+                        ++s;
+                        a = 0;
+                        draw = true;
+                    } else {        // emitted next iteration
+                        x = tid;
+                    }
+                    st = ST_BACK;
+                } else if (!need_x) {
+                    ++a;            // rejected without reading the graph
+                    st = ST_DRAW;
+                    draw = true;
+                } else if constexpr (WEIGHTED) {
+                    if (vdeg == 1) {
+                        ri = 0;
+                        st = ST_REC;
+                    } else {
+                        idx = bounded32(dr.x64, P.G * vdeg);   // guide bucket
+                        st = ST_GUIDE;
+                    }
                 } else {
-                    idx = bounded32(dr.x64, P.G * vdeg);   // guide bucket
-                    st = ST_GUIDE;
+                    ri = r;
+                    st = ST_REC;
                 }
-            } else {
-                ri = r;
-                st = ST_REC;
             }
         }
+        if (draw) st = ST_DRAW;   // still drawing: no load next iteration
     }
     add_steps(P.steps_out, steps);
     if (STATS) {
@@ -381,7 +476,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
     }
 }
 
-template <bool WEIGHTED, bool NODE2VEC, bool NEED_MEMBER, bool STATS>
+template <bool WEIGHTED, bool FAT, bool COMPACT, bool NODE2VEC, bool NEED_MEMBER, bool STATS>
 cudaError_t launch_k(const grape_graph* g, const WalkArgs& a, const Thresholds& T, cudaStream_t stream)
 {
     TabParams P{};
@@ -390,6 +485,9 @@ cudaError_t launch_k(const grape_graph* g, const WalkArgs& a, const Thresholds& 
     P.guide = g->guide;
     P.ehash = g->ehash;
     P.G = g->guide_factor;
+    if (g->hash_h == 6) { P.h_mul = 0xAAAAAAABu; P.h_shift = 2; }   // floor(v/6) = umulhi(v, ceil(2^34/6)) >> 2
+    else { P.h_mul = 0x40000000u; P.h_shift = 0; }                  // floor(v/4)
+    P.wsym = g->wsym;
     P.n = g->n;
     P.starts = a.starts;
     P.num_walks = a.num_walks;
@@ -407,30 +505,31 @@ cudaError_t launch_k(const grape_graph* g, const WalkArgs& a, const Thresholds& 
         int dev = 0, sms = 0, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, walk_tab_kernel<WEIGHTED, NODE2VEC, NEED_MEMBER, STATS>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, walk_tab_kernel<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, STATS>,
                                                       kBlock, 0);
         resident = sms * (per_sm > 0 ? per_sm : 1);
     }
     uint64_t blocks = (a.num_walks + kBlock - 1) / kBlock;
     if (blocks > (uint64_t)resident) blocks = resident;
-    walk_tab_kernel<WEIGHTED, NODE2VEC, NEED_MEMBER, STATS><<<(unsigned)blocks, kBlock, 0, stream>>>(P);
+    walk_tab_kernel<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, STATS><<<(unsigned)blocks, kBlock, 0, stream>>>(P);
     return cudaGetLastError();
 }
 
-template <bool WEIGHTED, bool NODE2VEC, bool NEED_MEMBER>
+template <bool WEIGHTED, bool FAT, bool COMPACT, bool NODE2VEC, bool NEED_MEMBER>
 cudaError_t launch_s(const grape_graph* g, const WalkArgs& a, const Thresholds& T, cudaStream_t stream)
 {
-    if (a.stats != nullptr) return launch_k<WEIGHTED, NODE2VEC, NEED_MEMBER, true>(g, a, T, stream);
-    return launch_k<WEIGHTED, NODE2VEC, NEED_MEMBER, false>(g, a, T, stream);
+    if (a.stats != nullptr) return launch_k<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, true>(g, a, T, stream);
+    return launch_k<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, false>(g, a, T, stream);
 }
 
-template <bool WEIGHTED>
+template <bool WEIGHTED, bool FAT, bool COMPACT>
 cudaError_t dispatch(const grape_graph* g, const WalkArgs& a, bool node2vec, const Thresholds& T,
                      cudaStream_t stream)
 {
-    if (!node2vec || (T.Tp == T.T1 && T.T1 == T.Tq)) return launch_s<WEIGHTED, false, false>(g, a, T, stream);
-    if (T.T1 != T.Tq) return launch_s<WEIGHTED, true, true>(g, a, T, stream);
-    return launch_s<WEIGHTED, true, false>(g, a, T, stream);
+    if (!node2vec || (T.Tp == T.T1 && T.T1 == T.Tq))
+        return launch_s<WEIGHTED, FAT, COMPACT, false, false>(g, a, T, stream);
+    if (T.T1 != T.Tq) return launch_s<WEIGHTED, FAT, COMPACT, true, true>(g, a, T, stream);
+    return launch_s<WEIGHTED, FAT, COMPACT, true, false>(g, a, T, stream);
 }
 
 }  // namespace
@@ -438,8 +537,13 @@ cudaError_t dispatch(const grape_graph* g, const WalkArgs& a, bool node2vec, con
 cudaError_t launch_walks_tab(const grape_graph* g, const WalkArgs& a, bool node2vec, const Thresholds& T,
                              cudaStream_t stream)
 {
-    if (g->cw_bytes != 0) return dispatch<true>(g, a, node2vec, T, stream);
-    return dispatch<false>(g, a, node2vec, T, stream);
+    if (g->cw_bytes == 0) {
+        if (g->compact) return dispatch<false, false, true>(g, a, node2vec, T, stream);
+        return dispatch<false, false, false>(g, a, node2vec, T, stream);
+    }
+    if (g->compact) return dispatch<true, false, true>(g, a, node2vec, T, stream);
+    if (g->guide_bytes == 32) return dispatch<true, true, false>(g, a, node2vec, T, stream);
+    return dispatch<true, false, false>(g, a, node2vec, T, stream);
 }
 
 }  // namespace grape

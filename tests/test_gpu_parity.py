@@ -22,9 +22,18 @@ def grape():
     return grape
 
 
+LAYOUTS = {   # forced table layouts (grape_table_options), weighted / unweighted
+    "slim": ({"guide_bytes": 8, "guide_factor": 2}, {"record_bytes": 16}),
+    "compact": ({"record_bytes": 16, "guide_bytes": 8, "guide_factor": 1, "hash_h": 6},
+                {"record_bytes": 8, "hash_h": 6}),
+}
+
+
 def _dev_graph(grape, g: CSR, symmetric=None, tables=True):
+    """tables: True (automatic layout), False (GRAPE_NO_TABLES: v3 walker) or a LAYOUTS key."""
     sym = g.symmetric if symmetric is None else symmetric
-    return grape.graph_from_csr(g.off, g.col, g.w, device=0, symmetric=sym, tables=tables)
+    layout = LAYOUTS[tables][0 if g.w is not None else 1] if isinstance(tables, str) else None
+    return grape.graph_from_csr(g.off, g.col, g.w, device=0, symmetric=sym, tables=bool(tables), layout=layout)
 
 
 def _run(grape, dg, starts, L, mode, p, q, seed, base=0):
@@ -79,8 +88,8 @@ def test_fuzz_graphs_every_walk(grape, seed, n, dens, directed, weighted, mode, 
     o = _oracle(g)
     for L in (1, 2, 3, 17, 64):
         exp, esteps = o.walks(starts, L, mode=mode, p=p, q=q, seed=seed, base=3 * seed)
-        for sym, tables in ([(False, True), (True, True), (False, False), (True, False)] if not directed
-                            else [(False, True), (False, False)]):
+        for sym, tables in ([(False, True), (True, "slim"), (False, "compact"), (False, False), (True, False)]
+                            if not directed else [(False, True), (False, "slim"), (False, "compact"), (False, False)]):
             dg = _dev_graph(grape, g, symmetric=sym, tables=tables)
             got, steps = _run(grape, dg, starts, L, mode, p, q, seed, base=3 * seed)
             assert np.array_equal(got, exp), (L, sym, tables)
@@ -257,7 +266,8 @@ def test_invalid_inputs_rejected(grape):
         grape.walks_node2vec(dg, st.cpu(), 5, 1.0, 1.0, out=torch.empty(10, 5, dtype=torch.int32, device="cuda"))
 
 
-@pytest.mark.parametrize("tables", [True, False], ids=["v4-tables", "v3-fenced"])
+@pytest.mark.parametrize("tables", [True, "slim", "compact", False], ids=["v4-tables", "v4-slim", "v4-compact",
+                                                                         "v3-fenced"])
 @pytest.mark.parametrize("mode,p,q,sym,weighted", [("node2vec", 0.5, 2.0, True, True), ("node2vec", 1.0, 0.25, False, False),
                                                    ("first_order", 1, 1, True, True), ("node2vec", 2.0, 1.0, True, False),
                                                    ("node2vec", 0.25, 4.0, False, True)])
@@ -286,7 +296,7 @@ def test_stats_build_matches_and_counts(grape, mode, p, q, sym, weighted, tables
     kinds = ("node_loads", "xnode_loads", "cw_probes", "col_probes", "col_loads", "start_loads",
              "guide_loads", "hash_probes")
     assert stats["sector_loads"] == sum(stats[k] for k in kinds)
-    if not tables:
+    if tables is False:
         assert stats["col_loads"] == stats["attempts"]
         assert stats["guide_loads"] == stats["hash_probes"] == stats["alu_decisions"] == 0
         if not weighted:
@@ -299,12 +309,15 @@ def test_stats_build_matches_and_counts(grape, mode, p, q, sym, weighted, tables
         assert stats["xnode_loads"] == stats["cw_probes"] == stats["col_probes"] == 0
         proposals = stats["attempts"] - stats["alu_decisions"]
         assert 0 <= stats["alu_decisions"] <= stats["attempts"]
-        if weighted:
-            assert stats["guide_loads"] <= proposals
+        if weighted:   # (fat guide: an accepted proposal re-reads its guide entry after a membership test)
+            assert stats["guide_loads"] <= proposals + stats["membership_tests"]
         else:
             assert stats["guide_loads"] == 0
             assert proposals <= stats["col_loads"] <= proposals + stats["membership_tests"]
         assert stats["hash_probes"] >= stats["membership_tests"]
-        assert stats["node_loads"] <= len(starts)
+        if tables != "compact":
+            assert stats["node_loads"] <= len(starts)
+        else:
+            assert stats["node_loads"] <= len(starts) + esteps
         if mode == "node2vec" and p < min(1.0, q):
             assert stats["alu_decisions"] > 0

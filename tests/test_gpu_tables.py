@@ -51,21 +51,34 @@ def _undirected(n, pairs, wfun=None, asym=False, seed=0):
     return _csr(n, src, dst, w, symmetric=True)
 
 
+LAYOUTS_W = [None, {"guide_bytes": 32, "guide_factor": 1}, {"guide_bytes": 8, "guide_factor": 4},
+             {"record_bytes": 16, "guide_factor": 2}, {"record_bytes": 16, "guide_factor": 1, "hash_h": 6}]
+LAYOUTS_U = [None, {"record_bytes": 8}, {"record_bytes": 16, "hash_h": 6}]
+
+
 def _check_all(grape, g, L=48, seeds=(3,), settings=SETTINGS, expect_wsym=None):
+    """Every walk of every setting on every table layout (and the v3 walker) == oracle."""
     o = Oracle(*g.numpy())
     starts = np.concatenate([np.arange(g.n), np.arange(g.n)[::-1], [g.n]]).astype(np.uint32)
     st = torch.as_tensor(starts.view(np.int32)).cuda()
-    d4 = grape.graph_from_csr(g.off, g.col, g.w, device=0, symmetric=g.symmetric)
+    graphs = []
+    for lay in (LAYOUTS_W if g.w is not None else LAYOUTS_U):
+        d = grape.graph_from_csr(g.off, g.col, g.w, device=0, symmetric=g.symmetric, layout=lay)
+        assert d.info["tables"] == 1 and d.info["table_bytes"] > 0
+        for k, v in (lay or {}).items():
+            assert d.info[k] == v, (k, d.info)
+        if lay is None and g.w is not None:   # small graph: the richest layout
+            assert (d.info["record_bytes"], d.info["guide_bytes"], d.info["guide_factor"]) == (32, 32, 4)
+        if expect_wsym is not None:
+            assert d.info["weights_symmetric"] == int(expect_wsym)
+        graphs.append(d)
     d3 = grape.graph_from_csr(g.off, g.col, g.w, device=0, symmetric=g.symmetric, tables=False)
-    assert d4.info["tables"] == 1 and d3.info["tables"] == 0
-    assert d4.info["table_bytes"] > 0 and d3.info["table_bytes"] == 0
-    if expect_wsym is not None:
-        assert d4.info["weights_symmetric"] == int(expect_wsym)
-    assert d4.info["guide_factor"] == (4 if g.w is not None else 0)
+    assert d3.info["tables"] == 0 and d3.info["table_bytes"] == 0
+    graphs.append(d3)
     for seed in seeds:
         for mode, p, q in settings:
             exp, esteps = o.walks(starts, L, mode=mode, p=p, q=q, seed=seed, base=11)
-            for dg in (d4, d3):
+            for dg in graphs:
                 steps = torch.zeros(1, dtype=torch.int64, device="cuda")
                 if mode == "first_order":
                     out = grape.walks_first_order(dg, st, L, seed=seed, walk_id_base=11, steps=steps)
@@ -73,10 +86,27 @@ def _check_all(grape, g, L=48, seeds=(3,), settings=SETTINGS, expect_wsym=None):
                     out = grape.walks_node2vec(dg, st, L, p, q, seed=seed, walk_id_base=11, steps=steps)
                 torch.cuda.synchronize()
                 got = out.cpu().numpy().view(np.uint32)
-                assert np.array_equal(got, exp), (mode, p, q, seed, dg.info["tables"])
+                assert np.array_equal(got, exp), (mode, p, q, seed, dg.info)
                 assert int(steps.item()) == esteps
-    d4.free()
-    d3.free()
+    for d in graphs:
+        d.free()
+
+
+def test_layout_options_rejected_or_enforced(grape):
+    g = _undirected(20, [(i, i + 1) for i in range(19)] + [(0, 10), (3, 17)], lambda r, k: r.integers(1, 9, k))
+    for bad in ({"record_bytes": 8}, {"guide_bytes": 16}, {"guide_factor": 3}, {"hash_h": 5},
+                {"record_bytes": 16, "guide_bytes": 32}):
+        with pytest.raises(grape.GrapeError) as ei:
+            grape.graph_from_csr(g.off, g.col, g.w, device=0, layout=bad)
+        assert ei.value.status == grape.GRAPE_EINVAL
+    with pytest.raises(grape.GrapeError) as ei:   # a forced layout that cannot fit the budget
+        grape.graph_from_csr(g.off, g.col, g.w, device=0, layout={"record_bytes": 32, "table_budget_bytes": 64})
+    assert ei.value.status == grape.GRAPE_ENOMEM
+    tiny = grape.graph_from_csr(g.off, g.col, g.w, device=0, layout={"table_budget_bytes": 64})
+    assert tiny.info["tables"] == 0   # automatic layout that does not fit: v3 walker
+    u = _undirected(20, [(0, 1), (1, 2)])
+    with pytest.raises(grape.GrapeError):
+        grape.graph_from_csr(u.off, u.col, None, device=0, layout={"guide_factor": 2})
 
 
 def test_guide_split_buckets_heavy_tailed_weights(grape):
