@@ -327,10 +327,23 @@ def run_ours(args):
             # only a capture of the same kernel and walk mode counts
             if kname in tj.get("kernel", "") and tj.get("mode", wk["mode"]) == wk["mode"]:
                 traffic = tj["dram_bytes_per_launch"]
-        ceil = None
-        cfile = os.path.join(ROOT, "profiles", "gather_ceiling.json")
+        # random-sector ceiling at this graph's randomly read footprint (measured,
+        # profiles/gather_footprint.json; linear interpolation in footprint)
+        ceil, ceil_src = None, None
+        cfile = os.path.join(ROOT, "profiles", "gather_footprint.json")
         if os.path.exists(cfile):
-            ceil = json.load(open(cfile))["random_accesses_per_s"]
+            tab = json.load(open(cfile))["footprint_gb_vs_rate"]
+            fp = info["device_bytes"] / 1e9
+            xs, ys = [t[0] for t in tab], [t[1] for t in tab]
+            if fp <= xs[0]:
+                rate = ys[0]
+            elif fp >= xs[-1]:
+                rate = ys[-1]
+            else:
+                k_ = next(j for j in range(1, len(xs)) if xs[j] >= fp)
+                rate = ys[k_ - 1] + (ys[k_] - ys[k_ - 1]) * (fp - xs[k_ - 1]) / (xs[k_] - xs[k_ - 1])
+            ceil = rate * 1e9
+            ceil_src = f"profiles/gather_footprint.json at {fp:.1f} GB"
         achieved = alg_bytes / t_launch / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic,
@@ -344,7 +357,7 @@ def run_ours(args):
                                   "achieved_per_s": rand_sectors / t_launch,
                                   "ceiling_per_s": ceil,
                                   "frac": (rand_sectors / t_launch / ceil) if ceil else None,
-                                  "ceiling_source": "profiles/gather_ceiling.json"}}
+                                  "ceiling_source": ceil_src}}
     clocks = clk.summary()
     if rank == 0:
         line = {"metric": "random-walk steps/sec (node2vec 2nd-order)" if node2vec else

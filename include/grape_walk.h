@@ -87,7 +87,7 @@ typedef struct {
                                     unweighted: 16 or 8 */
     uint32_t guide_bytes;        /* weighted: 32 (unsplit buckets hold the record; needs
                                     32-B records) or 8 */
-    uint32_t guide_factor;       /* weighted: guide buckets per arc, 1, 2 or 4 */
+    uint32_t guide_factor;       /* weighted: guide buckets per arc, 1, 2, 4, 8 or 16 */
     uint32_t hash_h;             /* edge-hash: one 8-slot bucket per H arcs (+1 per row), 4 or 6 */
 } grape_table_options;
 
@@ -104,7 +104,7 @@ typedef struct {
     uint32_t tables;          /* 1 if the sampling tables were built (v4 walker) */
     uint32_t weights_symmetric; /* 1 if every arc with a reverse arc has its weight */
     uint64_t table_bytes;     /* part of device_bytes held by the tables */
-    uint32_t guide_factor;    /* weighted tables: guide buckets per arc (4, 2 or 1 by free memory) */
+    uint32_t guide_factor;    /* weighted tables: guide buckets per arc (16 ... 1) */
     uint32_t guide_bytes;     /* weighted tables: 32 (entries of unsplit buckets hold the record) or 8 */
     uint32_t record_bytes;    /* tables: bytes per arc record */
     uint32_t hash_h;          /* tables: arcs per edge-hash bucket (4 or 6) */

@@ -239,7 +239,8 @@ grape_status grape_graph_from_csr_opts(uint32_t num_nodes, uint64_t num_arcs, co
         const uint32_t rb = o.record_bytes;
         const bool rec_ok = rb == 0 || (w ? (rb == 32 || rb == 16) : (rb == 16 || rb == 8));
         const bool gb_ok = o.guide_bytes == 0 || o.guide_bytes == 32 || o.guide_bytes == 8;
-        const bool g_ok = o.guide_factor == 0 || o.guide_factor == 1 || o.guide_factor == 2 || o.guide_factor == 4;
+        const bool g_ok = o.guide_factor == 0 || o.guide_factor == 1 || o.guide_factor == 2 || o.guide_factor == 4 ||
+                          o.guide_factor == 8 || o.guide_factor == 16;
         const bool h_ok = o.hash_h == 0 || o.hash_h == 4 || o.hash_h == 6;
         if (!rec_ok || !gb_ok || !g_ok || !h_ok || (!w && (o.guide_bytes || o.guide_factor)) ||
             (o.guide_bytes == 32 && rb == 16)) {

@@ -273,7 +273,7 @@ grape_status build_tables(grape_graph* g, const grape_table_options& o)
     // Layout, in order of preference (fewest reads per step first): records
     // with the head's node record (32 / 16 B) or compact (16 / 8 B, the head's
     // node record read separately); fat (32-B) or slim (8-B) guide entries with
-    // G = 4 / 2 / 1 buckets per arc; edge-hash load 1/2 (H = 4) or 3/4 (H = 6).
+    // G = 16 / 8 / 4 / 2 / 1 buckets per arc; edge-hash load 1/2 (H = 4) or 3/4 (H = 6).
     // The first that fits both the device (leaving 10% free: the caller still
     // needs its walk matrices) and the gather reach wins (grape_table_options
     // may force any part).  Results do not depend on the choice; the number and
@@ -296,12 +296,12 @@ grape_status build_tables(grape_graph* g, const grape_table_options& o)
     bool found = false, any_allowed = false;
     const uint32_t recs_w[2] = {32u, 16u}, recs_u[2] = {16u, 8u};
     const uint32_t gbs_w[2] = {32u, 8u}, gbs_u[1] = {0u};
-    const uint32_t Gs_w[3] = {4u, 2u, 1u}, Gs_u[1] = {0u};
+    const uint32_t Gs_w[5] = {16u, 8u, 4u, 2u, 1u}, Gs_u[1] = {0u};
     const uint32_t Hs[2] = {4u, 6u};
     const uint32_t* recs = weighted ? recs_w : recs_u;
     const uint32_t* gbs = weighted ? gbs_w : gbs_u;
     const uint32_t* Gs = weighted ? Gs_w : Gs_u;
-    const int ngb = weighted ? 2 : 1, nG = weighted ? 3 : 1;
+    const int ngb = weighted ? 2 : 1, nG = weighted ? 5 : 1;
     for (int hi = 0; hi < 2; ++hi) {
         for (int ri = 0; ri < 2; ++ri) {
             for (int gi = 0; gi < ngb; ++gi) {
@@ -310,7 +310,8 @@ grape_status build_tables(grape_graph* g, const grape_table_options& o)
                     const Choice k{recs[ri], gbs[gi], Gs[fi], Hs[hi]};
                     if (found || !allowed(k)) continue;
                     any_allowed = true;
-                    if ((!weighted || (uint64_t)k.G * m < (1ull << 32)) && size_of(k) <= budget) {
+                    if ((!weighted || ((uint64_t)k.G * m < (1ull << 32) && (uint64_t)k.G * g->max_degree < (1ull << 32))) &&
+                        size_of(k) <= budget) {
                         c = k;
                         found = true;
                     }

@@ -52,6 +52,7 @@ def _undirected(n, pairs, wfun=None, asym=False, seed=0):
 
 
 LAYOUTS_W = [None, {"guide_bytes": 32, "guide_factor": 1}, {"guide_bytes": 8, "guide_factor": 4},
+             {"guide_bytes": 32, "guide_factor": 8},
              {"record_bytes": 16, "guide_factor": 2}, {"record_bytes": 16, "guide_factor": 1, "hash_h": 6}]
 LAYOUTS_U = [None, {"record_bytes": 8}, {"record_bytes": 16, "hash_h": 6}]
 
@@ -68,7 +69,7 @@ def _check_all(grape, g, L=48, seeds=(3,), settings=SETTINGS, expect_wsym=None):
         for k, v in (lay or {}).items():
             assert d.info[k] == v, (k, d.info)
         if lay is None and g.w is not None:   # small graph: the richest layout
-            assert (d.info["record_bytes"], d.info["guide_bytes"], d.info["guide_factor"]) == (32, 32, 4)
+            assert (d.info["record_bytes"], d.info["guide_bytes"], d.info["guide_factor"]) == (32, 32, 16)
         if expect_wsym is not None:
             assert d.info["weights_symmetric"] == int(expect_wsym)
         graphs.append(d)

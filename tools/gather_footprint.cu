@@ -41,6 +41,25 @@ int main(int argc, char** argv) {
     fill<<<148 * 16, 256>>>(a, bytes / 4);
     CK(cudaDeviceSynchronize());
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    if (argc > 2) {   // occupancy sweep at one footprint: resident threads per SM
+        double fp = atof(argv[2]);
+        uint64_t nsec = (uint64_t)(fp * 1e9) / 32;
+        printf("footprint %.1f GB: threads/SM  mlp1_Gsec/s  mlp2_Gsec/s\n", fp);
+        for (int bps : {1, 2, 3, 4, 6, 8}) {
+            double r[2];
+            int mi = 0;
+            for (int mlp : {1, 2}) {
+                int blocks = 148 * bps, it = 64;
+                auto fn = [&] { if (mlp == 1) chase<1><<<blocks, 256>>>(a, nsec, it, sink); else chase<2><<<blocks, 256>>>(a, nsec, it, sink); };
+                fn(); CK(cudaDeviceSynchronize());
+                cudaEventRecord(e0); fn(); cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
+                float ms; cudaEventElapsedTime(&ms, e0, e1);
+                r[mi++] = (double)blocks * 256 * it * mlp / ms / 1e6;
+            }
+            printf("%10d %12.2f %12.2f\n", bps * 256, r[0], r[1]);
+        }
+        return 0;
+    }
     double fps[] = {0.5, 1, 2, 4, 8, 16, 32, 48, 56, 60, 64, 66, 68, 70, 72, 76, 80, 96, 128};
     printf("footprint_GB  mlp1_Gsec/s  mlp4_Gsec/s\n");
     for (double fp : fps) {
