@@ -25,4 +25,5 @@ from .oracle import (  # noqa: F401
     first_order_steps,
     node2vec_steps,
     philox4x32_10,
+    suss,
 )

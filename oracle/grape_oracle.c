@@ -323,3 +323,132 @@ int oracle_node2vec_steps(const uint64_t* off, const uint32_t* col, const uint64
         x_out[k] = oracle_node2vec_step(off, col, cw, T, seed, wid0 + k, s, t, v, &att_out[k]);
     return 0;
 }
+
+/* ---------------------------------------------------------------------------
+ * Approximated walks with Sorted Unique Sub-Sampling (SUSS) — SURVEY.md §8(f)
+ * row f1; §4.3.3 "Approximated random walks" and Fig. 3
+ * (P:110-116).  Readings (f1-*):
+ *   - degree threshold k = d_T >= 1.  At a node v with deg(v) = n <= k the step
+ *     is exactly the exact step ("if degree(v) <= d_T the step is exactly
+ *     the exact-walk step").
+ *   - n > k: SUSS "divides the range into k uniformly spaced buckets and
+ *     then randomly samples a value in each bucket": bucket b = [lo_b, lo_{b+1}),
+ *     lo_b = floor(b n / k) (the index range is [0, n): §8(c) c15 garble "[0,n]"),
+ *     candidate index c_b = lo_b + BOUNDED(h_b, lo_{b+1} - lo_b); the k candidates
+ *     are sorted and distinct by construction.
+ *   - the subsample is drawn once per step ("the sub-sampling is repeated
+ *     at each step"): h_b comes from the Philox block with counter
+ *     (wid lo, wid hi, s, 0x80000000 | floor(b/2)) — words (o1:o0) for even b,
+ *     (o3:o2) for odd b — a counter range the attempt counter (< 2^31) never uses.
+ *   - the step then runs the exact rules on the candidates only (P:509-511 steps
+ *     1-4 on the sub-sampled neighbourhood, Fig. 3b): proposal by BOUNDED(x64,
+ *     W_C) and the first candidate whose running weight sum exceeds it; node2vec
+ *     acceptance with the class of x relative to t on the full N(t) (the
+ *     sub-sampling restricts v's candidates, not the graph).
+ * ------------------------------------------------------------------------- */
+#define ORACLE_SUSS_CTR 0x80000000u
+
+/* The k SUSS candidate indices (row-local, strictly increasing) of step s of
+ * walk wid at a node of degree n > k. */
+void oracle_suss(uint64_t seed, uint64_t wid, uint32_t s, uint64_t n, uint32_t k, uint64_t* idx)
+{
+    uint32_t b;
+    for (b = 0; b < k; b++) {
+        uint64_t lo = ((uint64_t)b * n) / k;
+        uint64_t hi = ((uint64_t)(b + 1) * n) / k;
+        uint32_t o[4];
+        uint64_t h;
+        oracle_draw(seed, wid, s, ORACLE_SUSS_CTR | (b / 2), o);
+        h = (b % 2 == 0) ? (((uint64_t)o[1] << 32) | o[0]) : (((uint64_t)o[3] << 32) | o[2]);
+        idx[b] = lo + oracle_bounded(h, hi - lo);
+    }
+}
+
+/* PROPOSE on the candidate set: cand[b] = row-local indices, weights from cw
+ * (NULL: unweighted, each candidate weight 1).  ccum = caller scratch of k u64. */
+static uint32_t oracle_propose_cand(const uint64_t* off, const uint32_t* col, const uint64_t* cw, uint32_t v,
+                                    const uint64_t* cand, uint32_t k, uint64_t* ccum, uint64_t x64)
+{
+    uint64_t lo = off[v];
+    uint64_t acc = 0, r, b;
+    uint32_t j;
+    for (j = 0; j < k; j++) {
+        uint64_t e = lo + cand[j];
+        uint64_t w = 1;
+        if (cw != NULL)
+            w = cw[e] - (cand[j] > 0 ? cw[e - 1] : 0);
+        acc += w;
+        ccum[j] = acc;
+    }
+    r = oracle_bounded(x64, acc);
+    b = oracle_upper_bound(ccum, k, r);
+    return col[lo + cand[b]];
+}
+
+/* WALK with degree threshold k (k = 0: no threshold, the exact WALK).
+ * cand / ccum: caller scratch of k u64 each.  Same conventions and return
+ * value as oracle_walks. */
+int oracle_walks_approx(uint32_t n, const uint64_t* off, const uint32_t* col, const uint64_t* cw,
+                        const uint32_t* starts, uint64_t num_walks, uint64_t base, uint32_t L,
+                        int mode, double p, double q, uint64_t seed, uint32_t k,
+                        uint64_t* cand, uint64_t* ccum, uint32_t* out, uint64_t* steps_out)
+{
+    uint64_t T[3] = {0, 0, 0};
+    uint64_t i;
+    uint64_t steps = 0;
+    if (mode == 1 && oracle_thresholds(p, q, T) != 0)
+        return 1;
+    for (i = 0; i < num_walks; i++) {
+        uint32_t* row = out + i * (uint64_t)L;
+        uint64_t wid = base + i;
+        uint32_t start = starts[i];
+        uint32_t t, v, s, j;
+        for (j = 0; j < L; j++)
+            row[j] = ORACLE_PAD;
+        if (start >= n || L == 0)
+            continue;
+        row[0] = start;
+        t = ORACLE_NONE;
+        v = start;
+        for (s = 1; s < L; s++) {
+            uint64_t deg = off[v + 1] - off[v];
+            int sub = k > 0 && deg > k;
+            uint32_t x;
+            if (deg == 0)
+                break;
+            if (sub)
+                oracle_suss(seed, wid, s, deg, k, cand);
+            if (mode == 0 || t == ORACLE_NONE) {
+                uint32_t o[4];
+                oracle_draw(seed, wid, s, 0, o);
+                x = sub ? oracle_propose_cand(off, col, cw, v, cand, k, ccum, x64_of(o))
+                        : oracle_propose(off, col, cw, v, x64_of(o));
+            } else {
+                uint32_t a = 0;
+                for (;;) {
+                    uint32_t o[4];
+                    uint64_t thr;
+                    oracle_draw(seed, wid, s, a, o);
+                    x = sub ? oracle_propose_cand(off, col, cw, v, cand, k, ccum, x64_of(o))
+                            : oracle_propose(off, col, cw, v, x64_of(o));
+                    if (x == t)
+                        thr = T[0];
+                    else if (oracle_in_row(off, col, t, x))
+                        thr = T[1];
+                    else
+                        thr = T[2];
+                    a++;
+                    if ((uint64_t)o[2] < thr)
+                        break;
+                }
+            }
+            row[s] = x;
+            steps++;
+            t = v;
+            v = x;
+        }
+    }
+    if (steps_out != NULL)
+        *steps_out += steps;
+    return 0;
+}

@@ -67,6 +67,14 @@ def _load():
                 ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64,
                 ctypes.c_uint64, _u32p, _u32p]
             lib.oracle_node2vec_steps.restype = ctypes.c_int
+            lib.oracle_suss.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64,
+                                        ctypes.c_uint32, _u64p]
+            lib.oracle_suss.restype = None
+            lib.oracle_walks_approx.argtypes = [
+                ctypes.c_uint32, _u64p, _u32p, _u64p, _u32p, ctypes.c_uint64, ctypes.c_uint64,
+                ctypes.c_uint32, ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_uint64,
+                ctypes.c_uint32, _u64p, _u64p, _u32p, _u64p]
+            lib.oracle_walks_approx.restype = ctypes.c_int
             _lib = lib
     return _lib
 
@@ -103,6 +111,13 @@ def thresholds(p: float, q: float):
     if _load().oracle_thresholds(p, q, _p64(T)) != 0:
         return None
     return tuple(int(v) for v in T)
+
+
+def suss(seed: int, wid: int, s: int, n: int, k: int) -> np.ndarray:
+    """The k SUSS candidate indices of step s of walk wid at a node of degree n > k."""
+    idx = np.zeros(k, dtype=np.uint64)
+    _load().oracle_suss(seed, wid, s, n, k, _p64(idx))
+    return idx
 
 
 def prefix(n: int, off: np.ndarray, w: np.ndarray | None) -> np.ndarray:
@@ -151,6 +166,24 @@ class Oracle:
             raise ValueError(f"oracle rejected p={p} q={q}")
         if with_attempts:
             return out, int(steps.value), int(att.value)
+        return out, int(steps.value)
+
+    def walks_approx(self, starts, L: int, k: int, *, mode: str = "node2vec", p: float = 1.0,
+                     q: float = 1.0, seed: int = 42, base: int = 0):
+        """Approximated walks with degree threshold k (SUSS, §8(f) f1); (matrix, steps)."""
+        starts = np.ascontiguousarray(starts, dtype=np.uint32)
+        nw = len(starts)
+        out = np.empty((nw, L), dtype=np.uint32)
+        steps = ctypes.c_uint64(0)
+        cand = np.zeros(max(k, 1), dtype=np.uint64)
+        ccum = np.zeros(max(k, 1), dtype=np.uint64)
+        m = 0 if mode in ("first_order", "first-order", 0) else 1
+        rc = _load().oracle_walks_approx(self.n, _p64(self.off), _p32(self.col), _p64(self.cw),
+                                         _p32(starts), nw, base, L, m, float(p), float(q), seed, k,
+                                         _p64(cand), _p64(ccum), out.ctypes.data_as(_u32p),
+                                         ctypes.byref(steps))
+        if rc != 0:
+            raise ValueError(f"oracle rejected p={p} q={q}")
         return out, int(steps.value)
 
     def first_order_steps(self, v: int, s: int, wid0: int, count: int, seed: int = 42):

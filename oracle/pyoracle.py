@@ -97,6 +97,65 @@ class PyGraph:
             if o[2] < thr:
                 return x, a
 
+    # ---- approximated walks (SUSS, §8(f) f1) ----
+    def suss(self, seed, wid, s, n, k):
+        """k sorted unique candidate positions, one uniform draw per bucket
+        [floor(b n / k), floor((b+1) n / k)); bucket b's 64-bit draw is half of the
+        Philox block with counter (wid, s, 2^31 + b // 2)."""
+        out = []
+        for b in range(k):
+            lo, hi = b * n // k, (b + 1) * n // k
+            o = draw(seed, wid, s, 0x80000000 | (b // 2))
+            h = (o[1] << 32 | o[0]) if b % 2 == 0 else (o[3] << 32 | o[2])
+            out.append(lo + bounded(h, hi - lo))
+        return out
+
+    def propose_among(self, v, cand, x64):
+        row = self.rows[v]
+        if self.cw is None:
+            ws = [1] * len(cand)
+        else:
+            c = self.cw[v]
+            ws = [c[j] - (c[j - 1] if j else 0) for j in cand]
+        cum, acc = [], 0
+        for wj in ws:
+            acc += wj
+            cum.append(acc)
+        r = bounded(x64, acc)
+        return row[cand[bisect.bisect_right(cum, r)]]
+
+    def walk_approx(self, start, wid, L, k, mode="node2vec", p=1.0, q=1.0, seed=42):
+        row = [PAD] * L
+        if start >= self.n or L == 0:
+            return row, 0
+        T = thresholds(p, q) if mode == "node2vec" else None
+        row[0] = start
+        t, v, steps = NONE, start, 0
+        for s in range(1, L):
+            n = len(self.rows[v])
+            if n == 0:
+                break
+            cand = self.suss(seed, wid, s, n, k) if 0 < k < n else None
+
+            def prop(x64):
+                return self.propose(v, x64) if cand is None else self.propose_among(v, cand, x64)
+            if mode == "first_order" or t == NONE:
+                o = draw(seed, wid, s, 0)
+                x = prop((o[1] << 32) | o[0])
+            else:
+                a = 0
+                while True:
+                    o = draw(seed, wid, s, a)
+                    x = prop((o[1] << 32) | o[0])
+                    thr = T[0] if x == t else (T[1] if self.member(t, x) else T[2])
+                    a += 1
+                    if o[2] < thr:
+                        break
+            row[s] = x
+            steps += 1
+            t, v = v, x
+        return row, steps
+
     def walk(self, start, wid, L, mode="node2vec", p=1.0, q=1.0, seed=42, mutation=None):
         row = [PAD] * L
         if start >= self.n or L == 0:
