@@ -121,7 +121,7 @@ def _allreduce(x: float, op, world):
     return float(t.item())
 
 
-def _oracle_sample(g_cpu, wk, budget_s: float, first_wid: int = 0, cores: int | None = None):
+def _oracle_sample(g_cpu, wk, budget_s: float, first_wid: int = 0, cores: int | None = None, dT: int = 0):
     """Run the oracle (as it stands) on consecutive walks until ~budget_s of CPU
     work per thread; returns (realised steps, seconds, walks, threads, attempts)."""
     from oracle.oracle import Oracle
@@ -132,7 +132,10 @@ def _oracle_sample(g_cpu, wk, budget_s: float, first_wid: int = 0, cores: int | 
     starts_all = (np.arange(W, dtype=np.int64) % n).astype(np.uint32)
     # calibrate the per-thread batch on 64 walks
     t0 = time.perf_counter()
-    _, s0 = o.walks(starts_all[:64], wk["L"], mode=wk["mode"], p=wk["p"], q=wk["q"], seed=wk["seed"])
+    if dT:
+        _, s0 = o.walks_approx(starts_all[:64], wk["L"], dT, mode=wk["mode"], p=wk["p"], q=wk["q"], seed=wk["seed"])
+    else:
+        _, s0 = o.walks(starts_all[:64], wk["L"], mode=wk["mode"], p=wk["p"], q=wk["q"], seed=wk["seed"])
     dt = max(time.perf_counter() - t0, 1e-4)
     per_thread = max(64, int(64 * budget_s / dt))
     total = min(W - first_wid, per_thread * cores)
@@ -144,8 +147,13 @@ def _oracle_sample(g_cpu, wk, budget_s: float, first_wid: int = 0, cores: int | 
         if len(ids) == 0:
             res[k] = (0, 0)
             return
-        _, st, att = o.walks(starts_all[ids[0]:ids[-1] + 1], wk["L"], mode=wk["mode"], p=wk["p"],
-                             q=wk["q"], seed=wk["seed"], base=int(ids[0]), with_attempts=True)
+        if dT:
+            _, st = o.walks_approx(starts_all[ids[0]:ids[-1] + 1], wk["L"], dT, mode=wk["mode"], p=wk["p"],
+                                   q=wk["q"], seed=wk["seed"], base=int(ids[0]))
+            att = 0
+        else:
+            _, st, att = o.walks(starts_all[ids[0]:ids[-1] + 1], wk["L"], mode=wk["mode"], p=wk["p"],
+                                 q=wk["q"], seed=wk["seed"], base=int(ids[0]), with_attempts=True)
         res[k] = (st, att)
 
     th = [threading.Thread(target=work, args=(k,)) for k in range(cores)]
@@ -177,13 +185,18 @@ def run_reference(args):
     W = g.n * wk["walks_per_node"]
     vals, total_steps, total_secs = [], 0, 0.0
     for i in range(args.warmup + args.steps):
-        steps, secs, walks, cores, _ = _oracle_sample(g, wk, args.ref_budget, first_wid=(i * 997) % max(W - 1, 1))
+        steps, secs, walks, cores, _ = _oracle_sample(g, wk, args.ref_budget, first_wid=(i * 997) % max(W - 1, 1),
+                                                      dT=args.approx)
         if i >= args.warmup:
             vals.append(steps / secs)
             total_steps += steps
             total_secs += secs
     v = total_steps / total_secs
-    line = {"impl": "reference", "metric": "random-walk steps/sec (node2vec 2nd-order)", "value": v,
+    metric = ("random-walk steps/sec (node2vec 2nd-order)" if wk["mode"] == "node2vec" else
+              "random-walk steps/sec (first-order)")
+    if args.approx:
+        metric = metric[:-1] + f", approximated: SUSS d_T={args.approx})"
+    line = {"impl": "reference", "metric": metric, "value": v,
             "unit": "steps/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * total_secs / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32/u64 integer", "data": "synthetic (seeded generator)",
@@ -230,12 +243,19 @@ def run_ours(args):
     stream = torch.cuda.current_stream(dev)
     node2vec = wk["mode"] == "node2vec"
 
-    def one(ctr):
-        if node2vec:
-            grape.walks_node2vec(dg, starts, L, wk["p"], wk["q"], seed=wk["seed"], walk_id_base=base,
-                                 out=out, steps=ctr)
+    dT = args.approx
+
+    def call(st_buf, out_buf, ctr):
+        kw = dict(seed=wk["seed"], walk_id_base=base, out=out_buf, steps=ctr)
+        if dT:
+            grape.walks_approx(dg, st_buf, L, dT, node2vec=node2vec, p=wk["p"], q=wk["q"], **kw)
+        elif node2vec:
+            grape.walks_node2vec(dg, st_buf, L, wk["p"], wk["q"], **kw)
         else:
-            grape.walks_first_order(dg, starts, L, seed=wk["seed"], walk_id_base=base, out=out, steps=ctr)
+            grape.walks_first_order(dg, st_buf, L, **kw)
+
+    def one(ctr):
+        call(starts, out, ctr)
 
     for _ in range(args.warmup):
         one(None)
@@ -269,31 +289,28 @@ def run_ours(args):
         h_starts = starts.cpu().pin_memory()
         h_out = torch.empty((W, L), dtype=torch.int32, pin_memory=True)
         h_steps = torch.zeros(1, dtype=torch.int64)
-        kw = dict(seed=wk["seed"], walk_id_base=base, out=h_out)
-        grape.walks_node2vec(dg, h_starts, L, wk["p"], wk["q"], **kw) if node2vec else \
-            grape.walks_first_order(dg, h_starts, L, **kw)
+        call(h_starts, h_out, None)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize(dev)
         e2e_steps = max(1, min(args.steps, 3))
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            if node2vec:
-                grape.walks_node2vec(dg, h_starts, L, wk["p"], wk["q"], steps=h_steps, **kw)
-            else:
-                grape.walks_first_order(dg, h_starts, L, steps=h_steps, **kw)
+            call(h_starts, h_out, h_steps)
         torch.cuda.synchronize(dev)
         e2e_s = time.perf_counter() - t0
         e2e_s = _allreduce(e2e_s, dist.ReduceOp.MAX, world)
         e2e_tot = _allreduce(float(h_steps.item()), dist.ReduceOp.SUM, world)
         e2e = {"value": e2e_tot / e2e_s, "unit": "steps/s", "h2d_bytes_per_step": int(W * 4),
                "d2h_bytes_per_step": int(W * L * 4 + 8), "steps_timed": e2e_steps,
-               "path": "grape_walks_node2vec with pinned host starts/out (library-staged, chunked H2D/kernel/D2H)"}
+               "path": ("grape_walks_approx" if dT else "grape_walks_node2vec" if node2vec else
+                        "grape_walks_first_order") +
+                       " with pinned host starts/out (library-staged, chunked H2D/kernel/D2H)"}
 
     # ---- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and not args.no_cpu and world == 1:
-        s, secs, walks, cores, att = _oracle_sample(g, wk, args.cpu_budget)
+        s, secs, walks, cores, att = _oracle_sample(g, wk, args.cpu_budget, dT=dT)
         cpu = {"value": s / secs, "unit": "steps/s", "cores": cores, "kind": "oracle",
                "sample": f"first {walks} walks (wid 0..{walks - 1}) of the same workload, "
                          f"{cores} threads, {secs:.1f} s"}
@@ -302,6 +319,7 @@ def run_ours(args):
     roof = None
     if rank == 0:
         _, ev = grape.walks_stats(dg, starts, L, node2vec=node2vec, p=wk["p"], q=wk["q"], seed=wk["seed"],
+                                  degree_threshold=dT,
                                   walk_id_base=base, out=out)
         torch.cuda.synchronize(dev)
         weighted = info["cw_bytes"] > 0
@@ -360,8 +378,10 @@ def run_ours(args):
                                   "ceiling_source": ceil_src}}
     clocks = clk.summary()
     if rank == 0:
-        line = {"metric": "random-walk steps/sec (node2vec 2nd-order)" if node2vec else
-                "random-walk steps/sec (first-order)", "value": value, "unit": "steps/s",
+        metric = "random-walk steps/sec (node2vec 2nd-order)" if node2vec else "random-walk steps/sec (first-order)"
+        if dT:
+            metric = metric[:-1] + f", approximated: SUSS d_T={dT})"
+        line = {"metric": metric, "value": value, "unit": "steps/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32/u64 integer",
                 "data": "synthetic (seeded generator, graphgen/)", "config": _workload_desc(k, g, wk, W),
@@ -392,6 +412,8 @@ def main():
                     help="ncu dram bytes per launch of the walk kernel (from profiles/)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-tables", action="store_true", help="GRAPE_NO_TABLES: the v3 fenced-search walker")
+    ap.add_argument("--approx", type=int, default=0,
+                    help="approximated walks with SUSS degree threshold d_T (grape_walks_approx; 0 = exact)")
     ap.add_argument("--layout", default="", help="force table layout fields, e.g. "
                     "record_bytes=16,guide_bytes=8,guide_factor=1,hash_h=6 (grape_table_options)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle baseline (profiling runs)")

@@ -197,6 +197,30 @@ grape_status grape_walks_node2vec(const grape_graph* g, const uint32_t* starts,
                                   uint32_t* out, uint64_t* steps_out, cudaStream_t stream);
 
 /*
+ * grape_walks_approx — approximated walks (§4.3.3
+ * "Approximated random walks", and Fig. 3): at a node v
+ * with deg(v) > degree_threshold = k the step considers only a Sorted Unique
+ * Sub-Sample of k neighbours — bucket b = [floor(b deg/k), floor((b+1) deg/k))
+ * of v's sorted row contributes the index floor(b deg/k) + BOUNDED(h_b, width),
+ * h_b being half of the Philox block with counter (wid lo, wid hi, s,
+ * 2^31 + floor(b/2)) (words o1:o0 for even b, o3:o2 for odd b) — and then
+ * applies the exact rules above to those candidates (proposal by their weights,
+ * node2vec class of x relative to the full N(t)).  Nodes with deg <= k take the
+ * exact step (bit-identical to grape_walks_*), so k >= the maximum degree, or
+ * k = 0, gives the exact walks.
+ *   node2vec  0: first-order (p, q ignored); 1: node2vec with p, q.
+ * Everything else as grape_walks_node2vec.  Errors: as grape_walks_node2vec;
+ * EINVAL if sub-sampling would apply to a graph without sampling tables
+ * (GRAPE_NO_TABLES); ENOMEM / ECUDA if the per-lane candidate scratch
+ * (weighted graphs: 8 k bytes per resident thread, stream-ordered) cannot be
+ * allocated.
+ */
+grape_status grape_walks_approx(const grape_graph* g, const uint32_t* starts, uint64_t num_walks,
+                                uint64_t walk_id_base, uint32_t walk_length, int node2vec, double p,
+                                double q, uint32_t degree_threshold, uint64_t seed, uint32_t* out,
+                                uint64_t* steps_out, cudaStream_t stream);
+
+/*
  * grape_walks_stats — diagnostics: run the same walks as grape_walks_first_order
  * (node2vec = 0) or grape_walks_node2vec (node2vec = 1) with event counters
  * compiled into the kernel, and return the counts.  `out` receives exactly the
@@ -227,6 +251,12 @@ grape_status grape_walks_stats(const grape_graph* g, const uint32_t* starts, uin
                                uint64_t walk_id_base, uint32_t walk_length, int node2vec,
                                double p, double q, uint64_t seed, uint32_t* out,
                                grape_walk_stats* stats, cudaStream_t stream);
+
+/* grape_walks_stats for grape_walks_approx (degree_threshold as there). */
+grape_status grape_walks_stats_approx(const grape_graph* g, const uint32_t* starts, uint64_t num_walks,
+                                      uint64_t walk_id_base, uint32_t walk_length, int node2vec,
+                                      double p, double q, uint32_t degree_threshold, uint64_t seed,
+                                      uint32_t* out, grape_walk_stats* stats, cudaStream_t stream);
 
 /* Static string for a status code. */
 const char* grape_status_string(grape_status s);

@@ -160,8 +160,40 @@ def walks_node2vec(g: Graph, starts, L: int, p: float, q: float, *, seed: int = 
                   out, steps, stream)
 
 
+def walks_approx(g: Graph, starts, L: int, degree_threshold: int, *, node2vec: bool = True, p: float = 1.0,
+                 q: float = 1.0, seed: int = 42, walk_id_base: int = 0, out=None, steps=None,
+                 stream=None) -> torch.Tensor:
+    """grape_walks_approx: approximated walks with SUSS sub-sampling of rows with more than
+    degree_threshold neighbours (Fig. 3)."""
+    return _walks_approx(g, starts, L, int(node2vec), float(p), float(q), int(degree_threshold), seed,
+                         walk_id_base, out, steps, stream)
+
+
+def _walks_approx(g, starts, L, n2v, p, q, dT, seed, walk_id_base, out, steps, stream):
+    st = _as_tensor(starts, torch.int32)
+    W = st.numel()
+    fn = _lib.grape_walks_approx
+    dev = st.is_cuda
+    with torch.cuda.device(g.device):
+        if out is None:
+            out = (torch.empty((W, L), dtype=torch.int32, device=st.device) if dev else
+                   torch.empty((W, L), dtype=torch.int32, pin_memory=True))
+        if stream is None:
+            stream = torch.cuda.current_stream(g.device).cuda_stream
+        elif isinstance(stream, torch.cuda.Stream):
+            stream = stream.cuda_stream
+        hs = ctypes.c_uint64(0)
+        sp = (None if steps is None else steps.data_ptr()) if dev else ctypes.byref(hs)
+        rc = fn(g.handle, st.data_ptr(), W, walk_id_base, L, n2v, p, q, dT, seed, out.data_ptr(), sp,
+                ctypes.c_void_p(stream))
+    _capi.check(_lib, rc, "grape_walks_approx")
+    if not dev and steps is not None:
+        steps += int(hs.value)
+    return out
+
+
 def walks_stats(g: Graph, starts, L: int, *, node2vec: bool, p: float = 1.0, q: float = 1.0,
-                seed: int = 42, walk_id_base: int = 0, out=None):
+                seed: int = 42, walk_id_base: int = 0, out=None, degree_threshold: int = 0):
     """grape_walks_stats: (walk matrix, dict of event counters) — diagnostics build of the
     same kernel (device buffers only; synchronous)."""
     st = _as_tensor(starts, torch.int32)
@@ -172,10 +204,11 @@ def walks_stats(g: Graph, starts, L: int, *, node2vec: bool, p: float = 1.0, q: 
         if out is None:
             out = torch.empty((W, L), dtype=torch.int32, device=st.device)
         stats = _capi.WalkStats()
-        rc = _lib.grape_walks_stats(g.handle, st.data_ptr(), W, walk_id_base, L, int(node2vec), float(p),
-                                    float(q), seed, out.data_ptr(), ctypes.byref(stats),
-                                    ctypes.c_void_p(torch.cuda.current_stream(g.device).cuda_stream))
-    _capi.check(_lib, rc, "grape_walks_stats")
+        rc = _lib.grape_walks_stats_approx(g.handle, st.data_ptr(), W, walk_id_base, L, int(node2vec),
+                                           float(p), float(q), int(degree_threshold), seed, out.data_ptr(),
+                                           ctypes.byref(stats),
+                                           ctypes.c_void_p(torch.cuda.current_stream(g.device).cuda_stream))
+    _capi.check(_lib, rc, "grape_walks_stats_approx")
     return out, {f: int(getattr(stats, f)) for f in _capi.STATS_FIELDS}
 
 
@@ -184,3 +217,4 @@ grape_graph_from_csr = graph_from_csr
 grape_walks_first_order = walks_first_order
 grape_walks_node2vec = walks_node2vec
 grape_walks_stats = walks_stats
+grape_walks_approx = walks_approx

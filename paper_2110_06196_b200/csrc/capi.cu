@@ -148,7 +148,7 @@ grape_status walks_host(const grape_graph* g, const WalkArgs& a, bool n2v, const
 
 grape_status walks_common(const grape_graph* g, const uint32_t* starts, uint64_t num_walks,
                           uint64_t base, uint32_t L, bool n2v, double p, double q, uint64_t seed,
-                          uint32_t* out, uint64_t* steps_out, cudaStream_t stream)
+                          uint32_t* out, uint64_t* steps_out, cudaStream_t stream, uint32_t dT = 0)
 {
     g_err[0] = 0;
     if (g == nullptr || (num_walks > 0 && (starts == nullptr || out == nullptr))) {
@@ -165,6 +165,12 @@ grape_status walks_common(const grape_graph* g, const uint32_t* starts, uint64_t
     }
     Thresholds T{1ull << 32, 1ull << 32, 1ull << 32};
     if (n2v && !node2vec_thresholds(p, q, &T)) return GRAPE_EINVAL;
+    if (dT >= g->max_degree) dT = 0;   // no row exceeds the threshold: the exact walks
+    if (dT != 0 && !g->tables) {
+        set_error("approximated walks need the sampling tables (graph built with GRAPE_NO_TABLES "
+                  "or outside their index ranges)");
+        return GRAPE_EINVAL;
+    }
     int cur = -1;
     if (cudaGetDevice(&cur) != cudaSuccess) { cudaGetLastError(); cur = -1; }
     if (cur != g->device) {
@@ -185,6 +191,7 @@ grape_status walks_common(const grape_graph* g, const uint32_t* starts, uint64_t
     a.seed = seed;
     a.out = out;
     a.steps_out = nullptr;
+    a.dT = dT;
     if (ms == Mem::Host) return walks_host(g, a, n2v, T, stream, steps_out);
     if (steps_out != nullptr && classify(steps_out) != Mem::Device) {
         set_error("with device buffers, steps_out must be device memory (or NULL)");
@@ -311,10 +318,29 @@ grape_status grape_walks_node2vec(const grape_graph* g, const uint32_t* starts, 
                         steps_out, stream);
 }
 
+grape_status grape_walks_approx(const grape_graph* g, const uint32_t* starts, uint64_t num_walks,
+                                uint64_t walk_id_base, uint32_t walk_length, int node2vec, double p, double q,
+                                uint32_t degree_threshold, uint64_t seed, uint32_t* out, uint64_t* steps_out,
+                                cudaStream_t stream)
+{
+    if (!node2vec) { p = 1.0; q = 1.0; }
+    return walks_common(g, starts, num_walks, walk_id_base, walk_length, node2vec != 0, p, q, seed, out,
+                        steps_out, stream, degree_threshold);
+}
+
 grape_status grape_walks_stats(const grape_graph* g, const uint32_t* starts, uint64_t num_walks,
                                uint64_t walk_id_base, uint32_t walk_length, int node2vec, double p,
                                double q, uint64_t seed, uint32_t* out, grape_walk_stats* stats,
                                cudaStream_t stream)
+{
+    return grape_walks_stats_approx(g, starts, num_walks, walk_id_base, walk_length, node2vec, p, q, 0, seed,
+                                    out, stats, stream);
+}
+
+grape_status grape_walks_stats_approx(const grape_graph* g, const uint32_t* starts, uint64_t num_walks,
+                                      uint64_t walk_id_base, uint32_t walk_length, int node2vec, double p,
+                                      double q, uint32_t degree_threshold, uint64_t seed, uint32_t* out,
+                                      grape_walk_stats* stats, cudaStream_t stream)
 {
     g_err[0] = 0;
     if (g == nullptr || stats == nullptr || (num_walks > 0 && (starts == nullptr || out == nullptr))) {
@@ -331,6 +357,11 @@ grape_status grape_walks_stats(const grape_graph* g, const uint32_t* starts, uin
     }
     Thresholds T{1ull << 32, 1ull << 32, 1ull << 32};
     if (node2vec && !node2vec_thresholds(p, q, &T)) return GRAPE_EINVAL;
+    uint32_t dT = degree_threshold >= g->max_degree ? 0 : degree_threshold;
+    if (dT != 0 && !g->tables) {
+        set_error("approximated walks need the sampling tables");
+        return GRAPE_EINVAL;
+    }
     int cur = -1;
     if (cudaGetDevice(&cur) != cudaSuccess) { cudaGetLastError(); cur = -1; }
     if (cur != g->device) {
@@ -354,6 +385,7 @@ grape_status grape_walks_stats(const grape_graph* g, const uint32_t* starts, uin
     a.seed = seed;
     a.out = out;
     a.stats = d;
+    a.dT = dT;
     e = cudaMemsetAsync(d, 0, sizeof(unsigned long long) * kStatsWords, stream);
     if (e == cudaSuccess) e = launch_walks(g, a, node2vec != 0, T, stream);
     unsigned long long h[kStatsWords] = {0};

@@ -71,6 +71,7 @@ struct WalkArgs {
     uint32_t* out;
     unsigned long long* steps_out;   // device, may be NULL
     unsigned long long* stats;       // device grape_walk_stats (as u64[kStatsWords]) or NULL
+    uint32_t dT;                     // approximated walks: SUSS degree threshold (0: exact walks)
 };
 constexpr int kStatsWords = 13;
 

@@ -76,6 +76,24 @@ __device__ __forceinline__ Draw philox_draw_rk(const RoundKeys& rk, uint64_t wid
     return d;
 }
 
+// All four output words (c0, c1, c2, c3) of the block for counter (wid, step, word3).
+__device__ __forceinline__ uint4 philox_block_rk(const RoundKeys& rk, uint64_t wid, uint32_t step, uint32_t word3)
+{
+    constexpr uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+    uint32_t c0 = (uint32_t)wid, c1 = (uint32_t)(wid >> 32), c2 = step, c3 = word3;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = (uint64_t)M0 * c0, p1 = (uint64_t)M1 * c2;
+        const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ rk.k[2 * r];
+        const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ rk.k[2 * r + 1];
+        c1 = (uint32_t)p1;
+        c3 = (uint32_t)p0;
+        c0 = n0;
+        c2 = n2;
+    }
+    return make_uint4(c0, c1, c2, c3);
+}
+
 // floor(x64 * W / 2^64): the high word of the 128-bit product (§8(c) c8).
 __device__ __forceinline__ uint64_t bounded64(uint64_t x64, uint64_t W)
 {

@@ -32,7 +32,7 @@ namespace grape {
 namespace {
 using namespace walk;
 
-enum : uint32_t { ST_START = 0, ST_NODE, ST_GUIDE, ST_REC, ST_HASH, ST_DRAW, ST_BACK, ST_DONE };
+enum : uint32_t { ST_START = 0, ST_NODE, ST_GUIDE, ST_REC, ST_HASH, ST_CAND, ST_DRAW, ST_BACK, ST_DONE };
 
 constexpr uint32_t kEmptySlot = 0xFFFFFFFFu;
 #ifndef GRAPE_TAB_DRAWS
@@ -50,6 +50,9 @@ struct TabParams {
     uint32_t G;               // guide buckets per arc
     uint32_t h_mul, h_shift;  // floor(v / H) = umulhi(v, h_mul) >> h_shift (edge-hash buckets)
     bool wsym;                // weighted: reverse arcs carry equal weights
+    uint32_t dT;              // approximated walks (SUSS): degree threshold
+    uint32_t* scratch;        // SUSS, weighted: per lane 2 dT words, [2 b + {0: running weight, 1: x}][lane]
+    uint32_t lanes;           // resident lanes of the launch (scratch stride)
     uint32_t n;
     const uint32_t* starts;
     uint64_t num_walks;
@@ -109,7 +112,7 @@ enum : int { C_LOADS = 0, C_NODE, C_XNODE, C_CWPROBE, C_COLPROBE, C_REC, C_ATTEM
              C_GUIDE, C_HASH, C_ALU };
 
 // WEIGHTED: 32-B records + guide; else 16-B records indexed by the draw.
-template <bool WEIGHTED, bool FAT, bool COMPACT, bool NODE2VEC, bool NEED_MEMBER, bool STATS>
+template <bool WEIGHTED, bool FAT, bool COMPACT, bool NODE2VEC, bool NEED_MEMBER, bool STATS, bool SUSS>
 __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(const __grid_constant__ TabParams P)
 {
     uint32_t cnt[kStatsWords];
@@ -141,6 +144,21 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
     bool acc = false;             // the attempt is accepted; the record is read for x's data
     uint32_t x = 0;               // proposal
     uint32_t hrev = 0, hxs = 0, hxd = 0;   // unweighted: x's record, kept across its membership test
+    // SUSS (approximated walks, §8(f) f1): at a node with deg > dT the step runs on dT
+    // candidates, one uniform pick per bucket [floor(b deg/dT), floor((b+1) deg/dT))
+    uint32_t cb = 0;              // weighted: candidates read so far this step (dT: sub-sample in scratch)
+    uint32_t bt = kNone;          // weighted: the candidate that is t, if any
+    uint32_t wc = 0;              // weighted: running / total candidate weight
+    uint32_t clo = 0;             // compact records: cw of the candidate's predecessor
+    bool cph = false;             // compact records: reading the predecessor's sector
+    const uint64_t gl = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    auto suss_index = [&](uint32_t b) {   // row-local index of candidate b of this step
+        const uint32_t lo = (uint32_t)(((uint64_t)b * vdeg) / P.dT);
+        const uint32_t hi = (uint32_t)(((uint64_t)(b + 1) * vdeg) / P.dT);
+        const uint4 o = philox_block_rk(P.rk, P.base + i, s, 0x80000000u | (b >> 1));
+        const uint64_t h = (b & 1) ? ((uint64_t)o.w << 32 | o.z) : ((uint64_t)o.y << 32 | o.x);
+        return lo + bounded32(h, hi - lo);
+    };
 
     for (;;) {
         if (!__any_sync(0xffffffffu, st != ST_DONE)) break;
@@ -149,7 +167,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
         uint32_t sec[8];
         uint32_t j;
         {   // the one load of this iteration: a single address computation for every state
-            const bool rec = st == ST_REC, gd = st == ST_GUIDE, nd = st == ST_NODE;
+            const bool rec = st == ST_REC || (SUSS && st == ST_CAND), gd = st == ST_GUIDE, nd = st == ST_NODE;
             const uint32_t mul = rec ? 1u : gd ? P.G : 0u;
             uint64_t e = (uint64_t)mul * vstart + (rec ? ri : st == ST_HASH ? hb : idx);
             const char* b = rec ? (const char*)P.rec : gd ? (const char*)P.guide
@@ -168,7 +186,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
         if (STATS && load) {
             ++cnt[C_LOADS];
             cnt[C_NODE] += st == ST_NODE;
-            cnt[C_REC] += st == ST_REC;
+            cnt[C_REC] += st == ST_REC || st == ST_CAND;
             cnt[C_START] += st == ST_START;
             cnt[C_GUIDE] += st == ST_GUIDE;
             cnt[C_HASH] += st == ST_HASH;
@@ -265,6 +283,37 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                 x = e1;
                 decide = true;
             }
+        } else if (SUSS && WEIGHTED && st == ST_CAND) {   // candidate cb's record: its node and weight
+            bool done = true;
+            uint32_t wgt = 0;
+            if constexpr (COMPACT) {
+                const bool h = (j & 4) != 0;
+                if (cph) {                    // the predecessor (odd index: upper half): hi = cw[c - 1]
+                    wgt = clo - (h ? sec[5] : sec[1]);
+                    cph = false;
+                    ++ri;
+                } else {
+                    x = h ? sec[4] : sec[0];
+                    const uint32_t hi = h ? sec[5] : sec[1];
+                    const uint32_t rl = h ? sec[6] : sec[2], rh = h ? sec[7] : sec[3];
+                    if (P.wsym && rh > rl) wgt = rh - rl;          // the reverse arc has the same weight
+                    else if (ri == 0) wgt = hi;
+                    else if (h) wgt = hi - sec[1];                 // predecessor in this sector
+                    else { cph = true; clo = hi; --ri; done = false; }   // read the predecessor
+                }
+            } else {
+                x = sec[0];
+                wgt = sec[1] - sec[7];        // hi - lo
+            }
+            if (done) {
+                wc += wgt;
+                P.scratch[(uint64_t)(2 * cb) * P.lanes + gl] = wc;
+                P.scratch[(uint64_t)(2 * cb + 1) * P.lanes + gl] = x;
+                if (x == tid) bt = cb;
+                ++cb;
+                if (cb < P.dT) ri = suss_index(cb);
+                else draw = true;
+            }
         } else if (st == ST_HASH) {   // one bucket (8 slots) of t's set
             bool found = false, empty = false;
 #pragma unroll
@@ -300,6 +349,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
             vdeg = h ? sec[6] : sec[2];
             vW = h ? sec[7] : sec[3];
             a = 0;
+            cb = 0;
             if (vdeg == 0) fin = true;
             else draw = true;
         } else if (st == ST_START) {
@@ -376,6 +426,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
             }
             ++s;
             a = 0;
+            cb = 0;
             if (need_node) {
                 fin = s == L;
                 if (!fin) {
@@ -403,18 +454,47 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
         for (int k = 0; k < GRAPE_TAB_DRAWS; ++k) {
             __syncwarp();
             if (!__any_sync(0xffffffffu, draw)) break;
+            const bool sub = SUSS && vdeg > P.dT;   // this step runs on a SUSS sub-sample
+            if (SUSS && WEIGHTED && draw && sub && cb < P.dT) {   // first: read the dT candidates
+                draw = false;
+                wc = 0;
+                bt = kNone;
+                cph = false;
+                ri = suss_index(0);
+                st = ST_CAND;
+            }
             if (draw) {
                 if (STATS) ++cnt[C_ATTEMPT];
                 const Draw dr = philox_draw_rk(P.rk, P.base + i, s, a);
                 u = dr.u;
-                r = bounded32(dr.x64, vW);   // index (unweighted: vW = deg) or weight point
+                bool known = tlo <= thi;
+                uint32_t bs = 0;                 // SUSS: the proposed candidate
+                if (SUSS && sub) {
+                    if constexpr (WEIGHTED) {    // first candidate whose running weight exceeds r
+                        r = bounded32(dr.x64, wc);
+                        uint32_t lo = 0, hi = P.dT;
+                        while (lo < hi) {
+                            const uint32_t mid = (lo + hi) >> 1;
+                            if (P.scratch[(uint64_t)(2 * mid) * P.lanes + gl] <= r) lo = mid + 1;
+                            else hi = mid;
+                        }
+                        bs = lo;
+                        r = bs;                  // "x == t" <=> the candidate is t's
+                        known = true;
+                    } else {                     // uniform candidate; its row index vs t's
+                        bs = bounded32(dr.x64, P.dT);
+                        r = suss_index(bs);
+                    }
+                } else {
+                    r = bounded32(dr.x64, vW);   // index (unweighted: vW = deg) or weight point
+                }
                 bool need_x = true, ret = false;
                 if (NODE2VEC && tid != kNone) {
                     const bool cp = u <= P.tp_m1, c1 = u <= P.t1_m1, cq = u <= P.tq_m1;
                     if (cp == c1 && c1 == cq) {
                         need_x = cp;
-                    } else if (c1 == cq && tlo <= thi) {   // only "x == t" matters, and it is known
-                        const bool is_t = r - tlo < thi - tlo;
+                    } else if (c1 == cq && known) {   // only "x == t" matters, and it is known
+                        const bool is_t = (SUSS && WEIGHTED && sub) ? bs == bt : r - tlo < thi - tlo;
                         const bool ok = is_t ? cp : c1;
                         need_x = ok && !is_t;
                         ret = ok && is_t;
@@ -438,6 +518,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                         q = thi; thi = shi; shi = q;
                         ++s;
                         a = 0;
+                        cb = 0;
                         draw = true;
                     } else {        // emitted next iteration
                         x = tid;
@@ -447,6 +528,28 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                     ++a;            // rejected without reading the graph
                     st = ST_DRAW;
                     draw = true;
+                } else if (SUSS && WEIGHTED && sub) {   // x is in scratch: decide, then read its record
+                    x = P.scratch[(uint64_t)(2 * bs + 1) * P.lanes + gl];
+                    ri = suss_index(bs);
+                    bool ok = true, hash = false;
+                    if (NODE2VEC && tid != kNone) {
+                        const bool cp = u <= P.tp_m1, c1 = u <= P.t1_m1, cq = u <= P.tq_m1;
+                        if (x == tid) ok = cp;
+                        else if (!NEED_MEMBER || c1 == cq) ok = c1;
+                        else hash = true;
+                    }
+                    if (hash) {
+                        if (STATS) ++cnt[C_MEMB];
+                        st = ST_HASH;
+                        hb = divH(tstart) + tid + (uint32_t)(((uint64_t)fmix32(x) * (divH(tdeg) + 1)) >> 32);
+                    } else if (ok) {
+                        acc = true;
+                        st = ST_REC;
+                    } else {
+                        ++a;
+                        st = ST_DRAW;
+                        draw = true;
+                    }
                 } else if constexpr (WEIGHTED) {
                     if (vdeg == 1) {
                         ri = 0;
@@ -476,7 +579,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
     }
 }
 
-template <bool WEIGHTED, bool FAT, bool COMPACT, bool NODE2VEC, bool NEED_MEMBER, bool STATS>
+template <bool WEIGHTED, bool FAT, bool COMPACT, bool NODE2VEC, bool NEED_MEMBER, bool STATS, bool SUSS>
 cudaError_t launch_k(const grape_graph* g, const WalkArgs& a, const Thresholds& T, cudaStream_t stream)
 {
     TabParams P{};
@@ -500,26 +603,39 @@ cudaError_t launch_k(const grape_graph* g, const WalkArgs& a, const Thresholds& 
     P.tp_m1 = (uint32_t)(T.Tp - 1);
     P.t1_m1 = (uint32_t)(T.T1 - 1);
     P.tq_m1 = (uint32_t)(T.Tq - 1);
+    P.dT = a.dT;
     static int resident = 0;
     if (resident == 0) {
         int dev = 0, sms = 0, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, walk_tab_kernel<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, STATS>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, walk_tab_kernel<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, STATS, SUSS>,
                                                       kBlock, 0);
         resident = sms * (per_sm > 0 ? per_sm : 1);
     }
     uint64_t blocks = (a.num_walks + kBlock - 1) / kBlock;
     if (blocks > (uint64_t)resident) blocks = resident;
-    walk_tab_kernel<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, STATS><<<(unsigned)blocks, kBlock, 0, stream>>>(P);
-    return cudaGetLastError();
+    P.lanes = (uint32_t)(blocks * kBlock);
+    if (SUSS && WEIGHTED) {   // per-lane candidate scratch, stream-ordered
+        cudaError_t e = cudaMallocAsync((void**)&P.scratch, (uint64_t)2 * a.dT * P.lanes * 4, stream);
+        if (e != cudaSuccess) return e;
+    }
+    walk_tab_kernel<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, STATS, SUSS><<<(unsigned)blocks, kBlock, 0, stream>>>(P);
+    cudaError_t e = cudaGetLastError();
+    if (SUSS && WEIGHTED) cudaFreeAsync(P.scratch, stream);
+    return e;
 }
 
 template <bool WEIGHTED, bool FAT, bool COMPACT, bool NODE2VEC, bool NEED_MEMBER>
 cudaError_t launch_s(const grape_graph* g, const WalkArgs& a, const Thresholds& T, cudaStream_t stream)
 {
-    if (a.stats != nullptr) return launch_k<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, true>(g, a, T, stream);
-    return launch_k<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, false>(g, a, T, stream);
+    // approximated walks only when some row exceeds the threshold (else they are the exact walks)
+    if (a.dT != 0 && a.dT < g->max_degree) {
+        if (a.stats != nullptr) return launch_k<WEIGHTED, FAT, COMPACT, NODE2VEC, true, true, true>(g, a, T, stream);
+        return launch_k<WEIGHTED, FAT, COMPACT, NODE2VEC, true, false, true>(g, a, T, stream);
+    }
+    if (a.stats != nullptr) return launch_k<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, true, false>(g, a, T, stream);
+    return launch_k<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, false, false>(g, a, T, stream);
 }
 
 template <bool WEIGHTED, bool FAT, bool COMPACT>
