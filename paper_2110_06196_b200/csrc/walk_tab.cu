@@ -38,6 +38,9 @@ constexpr uint32_t kEmptySlot = 0xFFFFFFFFu;
 #ifndef GRAPE_TAB_DRAWS
 #define GRAPE_TAB_DRAWS 2
 #endif
+#ifndef GRAPE_TAB_STATIC_PCT
+#define GRAPE_TAB_STATIC_PCT 50
+#endif
 #ifndef GRAPE_TAB_MIN_BLOCKS
 #define GRAPE_TAB_MIN_BLOCKS 4
 #endif
@@ -53,6 +56,8 @@ struct TabParams {
     uint32_t dT;              // approximated walks (SUSS): degree threshold
     uint32_t* scratch;        // SUSS, weighted: per lane 2 dT words, [2 b + {0: running weight, 1: x}][lane]
     uint32_t lanes;           // resident lanes of the launch (scratch stride)
+    uint64_t nstatic;         // walks [0, nstatic) go round-robin to the lanes; the rest via *next
+    unsigned long long* next; // shared walk counter (starts at nstatic)
     uint32_t n;
     const uint32_t* starts;
     uint64_t num_walks;
@@ -441,7 +446,17 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
         if (fin) {
             for (uint32_t q = s; q < L; ++q) w.put(q, kPad);
             w.finish(L);
+            // next walk: round-robin over the statically assigned prefix [0, P.nstatic),
+            // then from the shared counter (balances the tail across lanes)
             i += stride;
+            if (i >= P.nstatic) {
+                const unsigned am = __activemask();
+                const int leader = __ffs(am) - 1;
+                const unsigned rank = __popc(am & ((1u << (threadIdx.x & 31)) - 1));
+                unsigned long long b0 = 0;
+                if ((int)(threadIdx.x & 31) == leader) b0 = atomicAdd(P.next, (unsigned long long)__popc(am));
+                i = P.nstatic + __shfl_sync(am, b0, leader) + rank;
+            }
             st = i < P.num_walks ? ST_START : ST_DONE;
             draw = false;
         }
@@ -616,13 +631,26 @@ cudaError_t launch_k(const grape_graph* g, const WalkArgs& a, const Thresholds& 
     uint64_t blocks = (a.num_walks + kBlock - 1) / kBlock;
     if (blocks > (uint64_t)resident) blocks = resident;
     P.lanes = (uint32_t)(blocks * kBlock);
-    if (SUSS && WEIGHTED) {   // per-lane candidate scratch, stream-ordered
-        cudaError_t e = cudaMallocAsync((void**)&P.scratch, (uint64_t)2 * a.dT * P.lanes * 4, stream);
+    // static share: GRAPE_TAB_STATIC_PCT percent of the walks, in whole rounds of the grid
+    // (launches of under 4 rounds are all static: no counter to allocate)
+    const uint64_t rounds = a.num_walks / P.lanes;
+    uint64_t srounds = rounds * GRAPE_TAB_STATIC_PCT / 100;
+    if (srounds < 1) srounds = 1;
+    P.nstatic = rounds < 4 ? ~0ull : srounds * P.lanes;   // >= lanes: every lane's first walk is static
+    cudaError_t e = cudaSuccess;
+    if (rounds >= 4) {
+        e = cudaMallocAsync((void**)&P.next, 8, stream);
         if (e != cudaSuccess) return e;
+        e = cudaMemsetAsync(P.next, 0, 8, stream);
     }
-    walk_tab_kernel<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, STATS, SUSS><<<(unsigned)blocks, kBlock, 0, stream>>>(P);
-    cudaError_t e = cudaGetLastError();
-    if (SUSS && WEIGHTED) cudaFreeAsync(P.scratch, stream);
+    if (e == cudaSuccess && SUSS && WEIGHTED)   // per-lane candidate scratch, stream-ordered
+        e = cudaMallocAsync((void**)&P.scratch, (uint64_t)2 * a.dT * P.lanes * 4, stream);
+    if (e == cudaSuccess) {
+        walk_tab_kernel<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, STATS, SUSS><<<(unsigned)blocks, kBlock, 0, stream>>>(P);
+        e = cudaGetLastError();
+    }
+    if (SUSS && WEIGHTED && P.scratch) cudaFreeAsync(P.scratch, stream);
+    if (P.next) cudaFreeAsync(P.next, stream);
     return e;
 }
 
