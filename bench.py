@@ -389,8 +389,9 @@ def run_ours(args):
                 "nominal_steps_per_gpu_step": W * (L - 1), "wall_s_timed": t_wall,
                 "clocks": clocks, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "graph_device_bytes": info["device_bytes"],
-                "graph_layout": {k_: info.get(k_) for k_ in ("tables", "guide_bytes", "guide_factor",
-                                                              "weights_symmetric", "table_bytes")}}
+                "graph_layout": {k_: info.get(k_) for k_ in ("tables", "record_bytes", "guide_bytes", "guide_factor",
+                                                              "hash_h", "notri", "weights_symmetric",
+                                                              "table_bytes")}}
         print(json.dumps(line), flush=True)
     dg.free()
     if world > 1:

@@ -108,6 +108,7 @@ typedef struct {
     uint32_t guide_bytes;     /* weighted tables: 32 (entries of unsplit buckets hold the record) or 8 */
     uint32_t record_bytes;    /* tables: bytes per arc record */
     uint32_t hash_h;          /* tables: arcs per edge-hash bucket (4 or 6) */
+    uint32_t notri;           /* tables: records carry the no-common-neighbour flags */
 } grape_graph_info;
 
 /*

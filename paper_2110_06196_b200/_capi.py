@@ -45,6 +45,7 @@ class GraphInfo(ctypes.Structure):
         ("guide_bytes", ctypes.c_uint32),
         ("record_bytes", ctypes.c_uint32),
         ("hash_h", ctypes.c_uint32),
+        ("notri", ctypes.c_uint32),
     ]
 
 

@@ -299,6 +299,7 @@ grape_status grape_graph_get_info(const grape_graph* g, grape_graph_info* info)
     info->guide_bytes = g->guide_bytes;
     info->record_bytes = g->tables ? g->rec_bytes : 0;
     info->hash_h = g->hash_h;
+    info->notri = g->notri ? 1u : 0u;
     return GRAPE_OK;
 }
 

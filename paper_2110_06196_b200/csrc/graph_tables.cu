@@ -30,7 +30,7 @@
 //          bucketised linear probing from bucket floor(fmix32(x) nb / 2^32);
 //          empty = 0xFFFFFFFF (never a node id).  Load factor <= 1/2, so a
 //          lookup reads one sector unless its home bucket is full.
-// Index ranges: 2m < 2^32 - 64 (u32 arc and slot indices), max degree < 2^29 (guide
+// Index ranges: 2m < 2^32 - 64 (u32 arc and slot indices), max degree < 2^28 (flag bits, guide
 // bits 30-31, G deg < 2^32), row sums < 2^32 (u32 prefix).  When the tables are
 // built, col / cw / fences are released (graph.cu): nothing reads them after.  Outside them the tables are not built and
 // the v3 walker (fenced searches) runs.
@@ -78,10 +78,14 @@ __device__ inline uint64_t upper_bound_u32(const uint32_t* __restrict__ cw, uint
 // One warp per row, lanes over the row's arcs.  Each record also carries the
 // node record of its head x (start, degree, W_x), so a walk that takes the arc
 // needs no separate node load.
+// Flags of arc e = (v -> x) (rev = its reverse arc): NOTRI_SELF = notri[e] (used on
+// arriving at x through e), NOTRI_REV = notri[rev] (used on a register-decided return
+// x -> v).  Full records keep them in bits 29 / 28 of the degree word, compact records
+// in bits 31 / 30 of x (only when n < 2^30; else never set).
 template <bool WEIGHTED, bool COMPACT>
 __global__ void build_records(const uint64_t* __restrict__ off, const uint32_t* __restrict__ col,
                               const uint32_t* __restrict__ cw, uint32_t n, void* __restrict__ rec,
-                              unsigned* __restrict__ asym)
+                              unsigned* __restrict__ asym, const uint8_t* __restrict__ notri)
 {
     const unsigned lane = threadIdx.x & 31;
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -94,6 +98,10 @@ __global__ void build_records(const uint64_t* __restrict__ off, const uint32_t* 
             const uint64_t xa = off[x], xb = off[x + 1];
             const uint64_t j = lower_bound_u32(col, xa, xb, (uint32_t)v);
             const bool found = j < xb && col[j] == (uint32_t)v;
+            uint32_t fl = 0;   // flag bits (0: self, 1: reverse)
+            if (notri != nullptr) fl = (notri[e] ? 1u : 0u) | (found && notri[j] ? 2u : 0u);
+            const uint32_t xf = COMPACT ? (x | (fl & 1) << 31 | (fl >> 1) << 30) : x;   // compact: bits 31 (self), 30 (rev)
+            const uint32_t df = COMPACT ? 0u : ((fl & 1) << 29 | (fl >> 1) << 28);   // full: bits 29, 28 of deg
             if (WEIGHTED) {
                 const uint32_t own_hi = cw[e];
                 const uint32_t own_lo = e > lo ? cw[e - 1] : 0u;
@@ -104,19 +112,19 @@ __global__ void build_records(const uint64_t* __restrict__ off, const uint32_t* 
                     bad |= (rhi - rlo) != own_hi - own_lo;
                 }
                 if (COMPACT) {
-                    reinterpret_cast<uint4*>(rec)[e] = make_uint4(x, own_hi, rlo, rhi);
+                    reinterpret_cast<uint4*>(rec)[e] = make_uint4(xf, own_hi, rlo, rhi);
                 } else {
                     const uint32_t xW = xb > xa ? cw[xb - 1] : 0u;
                     uint4* r = reinterpret_cast<uint4*>(rec) + 2 * e;
                     r[0] = make_uint4(x, own_hi, rlo, rhi);
-                    r[1] = make_uint4((uint32_t)xa, (uint32_t)(xb - xa), xW, own_lo);
+                    r[1] = make_uint4((uint32_t)xa, (uint32_t)(xb - xa) | df, xW, own_lo);
                 }
             } else {
                 const uint32_t rev = found ? (uint32_t)(j - xa) : kNone;
                 if (COMPACT)
-                    reinterpret_cast<uint2*>(rec)[e] = make_uint2(x, rev);
+                    reinterpret_cast<uint2*>(rec)[e] = make_uint2(xf, rev);
                 else
-                    reinterpret_cast<uint4*>(rec)[e] = make_uint4(x, rev, (uint32_t)xa, (uint32_t)(xb - xa));
+                    reinterpret_cast<uint4*>(rec)[e] = make_uint4(x, rev, (uint32_t)xa, (uint32_t)(xb - xa) | df);
             }
         }
     }
@@ -222,6 +230,58 @@ __global__ void build_ehash(const uint64_t* __restrict__ off, const uint32_t* __
     }
 }
 
+// notri[e] for arc e = (t -> v): 1 iff no x != t in N(v) lies in N(t), i.e. at v
+// coming from t every proposal other than t itself is in class q (P:453-470:
+// X_beta = N(v) \ N(t) is all of N(v) \ {t}).  One warp per row t; each lane
+// scans the shorter of N(t), N(v) and probes the other's edge-hash set, stopping
+// at the first common neighbour.
+__device__ inline bool hash_has(const uint32_t* __restrict__ ehash, uint64_t base, uint64_t nb, uint32_t x)
+{
+    uint64_t b = ((uint64_t)fmix32(x) * nb) >> 32;
+    for (uint64_t tries = 0; tries < nb; ++tries) {
+        const uint32_t* slot = ehash + 8 * (base + b);
+        bool empty = false;
+        for (int q = 0; q < 8; ++q) {
+            const uint32_t y = slot[q];
+            if (y == x) return true;
+            empty |= y == kEmpty;
+        }
+        if (empty) return false;
+        b = b + 1 == nb ? 0 : b + 1;
+    }
+    return false;
+}
+
+__global__ void build_notri(const uint64_t* __restrict__ off, const uint32_t* __restrict__ col, uint32_t n,
+                            uint32_t H, const uint32_t* __restrict__ ehash, uint8_t* __restrict__ notri)
+{
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t t = warp; t < n; t += nwarps) {
+        const uint64_t ta = off[t], tb = off[t + 1];
+        for (uint64_t e = ta + lane; e < tb; e += 32) {
+            const uint32_t v = col[e];
+            const uint64_t va = off[v], vb = off[v + 1];
+            bool common = false;
+            if (vb - va <= tb - ta) {   // x in N(v), x != t: in N(t)?
+                const uint64_t base = ta / H + t, nb = (tb - ta) / H + 1;
+                for (uint64_t f = va; f < vb && !common; ++f) {
+                    const uint32_t x = col[f];
+                    common = x != (uint32_t)t && hash_has(ehash, base, nb, x);
+                }
+            } else {                    // x in N(t), x != t: in N(v)?
+                const uint64_t base = va / H + v, nb = (vb - va) / H + 1;
+                for (uint64_t f = ta; f < tb && !common; ++f) {
+                    const uint32_t x = col[f];
+                    common = x != (uint32_t)t && hash_has(ehash, base, nb, x);
+                }
+            }
+            notri[e] = common ? 0 : 1;
+        }
+    }
+}
+
 int rows_grid(uint64_t n)
 {
     uint64_t blocks = (n + 7) / 8;
@@ -246,6 +306,7 @@ void destroy_tables(grape_graph* g)
     g->guide_bytes = 0;
     g->hash_h = 0;
     g->compact = false;
+    g->notri = false;
     g->tables = false;
     g->table_bytes = 0;
 }
@@ -260,7 +321,7 @@ grape_status build_tables(grape_graph* g, const grape_table_options& o)
 {
     const uint64_t m = g->m, n = g->n;
     const bool weighted = g->cw_bytes != 0;
-    if (2 * m >= (1ull << 32) - 64 || (m >> 2) + n + 2 >= (1ull << 32) || g->max_degree >= (1u << 29) ||
+    if (2 * m >= (1ull << 32) - 64 || (m >> 2) + n + 2 >= (1ull << 32) || g->max_degree >= (1u << 28) ||
         g->cw_bytes == 8)
         return GRAPE_OK;
     cudaError_t e = cudaSuccess;
@@ -344,11 +405,23 @@ grape_status build_tables(grape_graph* g, const grape_table_options& o)
     cudaMemset(g->ehash, 0xFF, hash_b);
     if (weighted) cudaMemset(g->guide, 0, guide_b);
     const int grid = rows_grid(g->n);
+    build_ehash<<<grid, kThreads>>>(g->off, g->col, g->n, g->hash_h, g->ehash);
+    // no-common-neighbour flags (a temporary byte per arc); compact records need n < 2^30
+    uint8_t* d_notri = nullptr;
+    const bool flags_ok = !(g->compact && n >= (1u << 30));
+    if (flags_ok && cudaMalloc((void**)&d_notri, m ? m : 1) == cudaSuccess) {
+        build_notri<<<grid, kThreads>>>(g->off, g->col, g->n, g->hash_h, g->ehash, d_notri);
+    } else {
+        cudaGetLastError();
+        d_notri = nullptr;
+    }
     if (weighted) {
         if (g->compact)
-            build_records<true, true><<<grid, kThreads>>>(g->off, g->col, (const uint32_t*)g->cw, g->n, g->rec, d_asym);
+            build_records<true, true><<<grid, kThreads>>>(g->off, g->col, (const uint32_t*)g->cw, g->n, g->rec, d_asym,
+                                                          d_notri);
         else
-            build_records<true, false><<<grid, kThreads>>>(g->off, g->col, (const uint32_t*)g->cw, g->n, g->rec, d_asym);
+            build_records<true, false><<<grid, kThreads>>>(g->off, g->col, (const uint32_t*)g->cw, g->n, g->rec, d_asym,
+                                                           d_notri);
         if (gbytes == 32)
             build_guide_fat<<<grid, kThreads>>>(g->off, (const uint32_t*)g->cw, g->n, G, (const uint4*)g->rec,
                                                 (uint4*)g->guide);
@@ -356,11 +429,15 @@ grape_status build_tables(grape_graph* g, const grape_table_options& o)
             build_guide<<<grid, kThreads>>>(g->off, g->col, (const uint32_t*)g->cw, g->n, G, (uint2*)g->guide);
     } else {
         if (g->compact)
-            build_records<false, true><<<grid, kThreads>>>(g->off, g->col, nullptr, g->n, g->rec, d_asym);
+            build_records<false, true><<<grid, kThreads>>>(g->off, g->col, nullptr, g->n, g->rec, d_asym, d_notri);
         else
-            build_records<false, false><<<grid, kThreads>>>(g->off, g->col, nullptr, g->n, g->rec, d_asym);
+            build_records<false, false><<<grid, kThreads>>>(g->off, g->col, nullptr, g->n, g->rec, d_asym, d_notri);
     }
-    build_ehash<<<grid, kThreads>>>(g->off, g->col, g->n, g->hash_h, g->ehash);
+    g->notri = d_notri != nullptr;
+    if (d_notri) {
+        cudaDeviceSynchronize();
+        cudaFree(d_notri);
+    }
     if ((e = cudaGetLastError()) != cudaSuccess) return fail(e, "table kernels");
     unsigned asym = 0;
     if ((e = cudaMemcpy(&asym, d_asym, 4, cudaMemcpyDeviceToHost)) != cudaSuccess) return fail(e, "table build");

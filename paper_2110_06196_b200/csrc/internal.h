@@ -44,6 +44,7 @@ struct grape_graph {
     uint32_t guide_bytes;    // 32 (fat: unsplit buckets hold a record copy) or 8 (slim)
     uint32_t hash_h;         // edge-hash buckets: floor(deg / H) + 1 per row (H = 4 or 6)
     bool compact;            // records without the head's node record (16 B weighted / 8 B)
+    bool notri;              // records carry the no-common-neighbour flags (graph_tables.cu)
     uint32_t* ehash;      // per-row linear-probing sets of N(v): 2*deg(v) slots at 2*off[v]
     uint64_t table_bytes;
     uint32_t max_degree;

@@ -53,6 +53,8 @@ struct TabParams {
     uint32_t G;               // guide buckets per arc
     uint32_t h_mul, h_shift;  // floor(v / H) = umulhi(v, h_mul) >> h_shift (edge-hash buckets)
     bool wsym;                // weighted: reverse arcs carry equal weights
+    bool notri;               // records carry the no-common-neighbour flags
+    uint32_t xmask;           // compact records: x without its flag bits
     uint32_t dT;              // approximated walks (SUSS): degree threshold
     uint32_t* scratch;        // SUSS, weighted: per lane 2 dT words, [2 b + {0: running weight, 1: x}][lane]
     uint32_t lanes;           // resident lanes of the launch (scratch stride)
@@ -136,6 +138,10 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
     uint32_t idx = 0;   // what the next load reads: NODE node id, GUIDE bucket (REC: ri, HASH: hb)
     uint32_t hb = 0;    // edge-hash bucket (absolute index)
     bool gsrc = false;  // fat guide: the proposal's record is the guide entry idx
+    // no common neighbour (graph_tables.cu build_notri): nt for the current (t, v) —
+    // every proposal x != t is then in class q — and ntr for (v, t), used after a return
+    bool nt = false, ntr = false;
+    uint32_t hfl = 0;   // unweighted: x's record flags, kept across its membership test
     unsigned long long steps = 0;
 
     uint32_t s = 0, a = 0;
@@ -202,6 +208,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
         // the record of the taken arc (valid when emit): head x, its node record,
         // the new T = [nlo, nhi) and S = [nslo, nshi)
         uint32_t xs = 0, xd = 0, xw = 0, nlo = 0, nhi = 0, nslo = 0, nshi = 0;
+        uint32_t xfl = 0;   // the record's flags: bit 1 = no common neighbour of (v, x), bit 0 = of (x, v)
         bool have_rec = false;   // the sector in hand is x's record
         if (st == ST_REC) {
             have_rec = true;
@@ -213,7 +220,9 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                     found = false;
                     ++ri;
                 }
-                x = h ? sec[4] : sec[0];
+                const uint32_t xr = h ? sec[4] : sec[0];
+                x = xr & P.xmask;
+                xfl = P.notri ? xr >> 30 : 0u;
                 nlo = h ? sec[6] : sec[2];
                 nhi = h ? sec[7] : sec[3];
                 nshi = hi;
@@ -226,10 +235,14 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                 }
                 x = sec[0];
                 nlo = sec[2]; nhi = sec[3];
-                xs = sec[4]; xd = sec[5]; xw = sec[6];
+                xs = sec[4]; xd = sec[5] & 0x0FFFFFFFu; xw = sec[6];
+                xfl = (sec[5] >> 28) & 3u;
                 nslo = sec[7]; nshi = sec[1];
             } else if constexpr (COMPACT) {   // 8-B {x, rev} at word j (even)
-                x = pick8(sec, j);
+                const uint32_t xr = pick8(sec, j);
+                x = xr & P.xmask;
+                xfl = P.notri ? xr >> 30 : 0u;
+                hfl = xfl;
                 const uint32_t rev = pick8(sec, j | 1);
                 hrev = rev;
                 nlo = rev;
@@ -242,8 +255,10 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                 const uint32_t rev = h ? sec[5] : sec[1];
                 xs = h ? sec[6] : sec[2];
                 xd = h ? sec[7] : sec[3];
+                xfl = (xd >> 28) & 3u;
+                xd &= 0x0FFFFFFFu;
                 xw = xd;
-                hrev = rev; hxs = xs; hxd = xd;
+                hrev = rev; hxs = xs; hxd = xd; hfl = xfl;
                 nlo = rev;
                 nhi = rev == kNone ? rev : rev + 1;   // [rev, rev+1), or the empty [NONE, NONE)
                 nslo = ri;
@@ -279,7 +294,8 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                 gsrc = true;
                 x = sec[0];
                 nlo = sec[2]; nhi = sec[3];
-                xs = sec[4]; xd = sec[5]; xw = sec[6];
+                xs = sec[4]; xd = sec[5] & 0x0FFFFFFFu; xw = sec[6];
+                xfl = (sec[5] >> 28) & 3u;
                 nslo = sec[7]; nshi = sec[1];
                 if (acc) emit = true;
                 else decide = true;
@@ -298,7 +314,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                     cph = false;
                     ++ri;
                 } else {
-                    x = h ? sec[4] : sec[0];
+                    x = (h ? sec[4] : sec[0]) & P.xmask;
                     const uint32_t hi = h ? sec[5] : sec[1];
                     const uint32_t rl = h ? sec[6] : sec[2], rh = h ? sec[7] : sec[3];
                     if (P.wsym && rh > rl) wgt = rh - rl;          // the reverse arc has the same weight
@@ -335,6 +351,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                     } else {          // the record was kept in registers
                         emit = true;
                         xs = hxs; xd = hxd; xw = hxd;   // (compact: unused, x's node record is read)
+                        xfl = hfl;
                         nlo = hrev;
                         nhi = hrev == kNone ? hrev : hrev + 1;
                         nslo = ri;
@@ -348,7 +365,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                 const uint32_t base = divH(tstart) + tid;
                 hb = hb + 1 == base + divH(tdeg) + 1 ? base : hb + 1;
             }
-        } else if (st == ST_NODE) {   // start node
+        } else if (st == ST_NODE) {   // node record: a start node, or (compact records) a taken arc's head
             const bool h = (j & 4) != 0;
             vstart = h ? sec[4] : sec[0];
             vdeg = h ? sec[6] : sec[2];
@@ -362,6 +379,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
             w.begin(P.out + i * L);
             s = 0;
             tid = kNone;
+            nt = ntr = false;
             if (start < P.n) {
                 w.put(0, start);
                 vid = start;
@@ -379,7 +397,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
         if (decide) {   // x is known: its class, if it matters
             bool ok = true, hash = false;
             if (NODE2VEC && tid != kNone) {
-                const bool cp = u <= P.tp_m1, c1 = u <= P.t1_m1, cq = u <= P.tq_m1;
+                const bool cp = u <= P.tp_m1, cq = u <= P.tq_m1, c1 = nt ? cq : u <= P.t1_m1;
                 if (x == tid) ok = cp;
                 else if (!NEED_MEMBER || c1 == cq) ok = c1;
                 else hash = true;
@@ -413,6 +431,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                 if constexpr (COMPACT) need_node = true;   // x's node record: next iteration
                 else { vstart = xs; vdeg = xd; vW = xw; }
                 tlo = nlo; thi = nhi; slo = nslo; shi = nshi;
+                nt = (xfl >> 1) != 0; ntr = (xfl & 1) != 0;
             } else if (emit) {   // compact record of a return: t's node record is in registers
                 uint32_t q;
                 q = vstart; vstart = tstart; tstart = q;
@@ -420,7 +439,9 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                 q = vW; vW = tW; tW = q;
                 q = vid; vid = tid; tid = q;
                 tlo = nlo; thi = nhi; slo = nslo; shi = nshi;
+                nt = (xfl >> 1) != 0; ntr = (xfl & 1) != 0;
             } else {   // x = t: v and t swap, and so do T and S
+                const bool b_ = nt; nt = ntr; ntr = b_;
                 uint32_t q;
                 q = vstart; vstart = tstart; tstart = q;
                 q = vdeg; vdeg = tdeg; tdeg = q;
@@ -505,7 +526,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                 }
                 bool need_x = true, ret = false;
                 if (NODE2VEC && tid != kNone) {
-                    const bool cp = u <= P.tp_m1, c1 = u <= P.t1_m1, cq = u <= P.tq_m1;
+                    const bool cp = u <= P.tp_m1, cq = u <= P.tq_m1, c1 = nt ? cq : u <= P.t1_m1;
                     if (cp == c1 && c1 == cq) {
                         need_x = cp;
                     } else if (c1 == cq && known) {   // only "x == t" matters, and it is known
@@ -531,6 +552,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                         q = vid; vid = tid; tid = q;
                         q = tlo; tlo = slo; slo = q;
                         q = thi; thi = shi; shi = q;
+                        const bool b_ = nt; nt = ntr; ntr = b_;
                         ++s;
                         a = 0;
                         cb = 0;
@@ -548,7 +570,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                     ri = suss_index(bs);
                     bool ok = true, hash = false;
                     if (NODE2VEC && tid != kNone) {
-                        const bool cp = u <= P.tp_m1, c1 = u <= P.t1_m1, cq = u <= P.tq_m1;
+                        const bool cp = u <= P.tp_m1, cq = u <= P.tq_m1, c1 = nt ? cq : u <= P.t1_m1;
                         if (x == tid) ok = cp;
                         else if (!NEED_MEMBER || c1 == cq) ok = c1;
                         else hash = true;
@@ -606,6 +628,8 @@ cudaError_t launch_k(const grape_graph* g, const WalkArgs& a, const Thresholds& 
     if (g->hash_h == 6) { P.h_mul = 0xAAAAAAABu; P.h_shift = 2; }   // floor(v/6) = umulhi(v, ceil(2^34/6)) >> 2
     else { P.h_mul = 0x40000000u; P.h_shift = 0; }                  // floor(v/4)
     P.wsym = g->wsym;
+    P.notri = g->notri;
+    P.xmask = (g->notri && g->compact) ? 0x3FFFFFFFu : 0xFFFFFFFFu;
     P.n = g->n;
     P.starts = a.starts;
     P.num_walks = a.num_walks;
