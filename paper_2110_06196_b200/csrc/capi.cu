@@ -76,32 +76,61 @@ struct DeviceGuard {
     ~DeviceGuard() { if (prev >= 0) cudaSetDevice(prev); }
 };
 
+#ifndef GRAPE_HOST_CHUNK_MB
+#define GRAPE_HOST_CHUNK_MB 256
+#endif
+#ifndef GRAPE_HOST_NBUF
+#define GRAPE_HOST_NBUF 2
+#endif
+
 // Host buffers: stage chunks through device memory.  Chunk k runs on the
 // caller's stream (H2D starts -> kernel), its D2H runs on an internal copy
-// stream, so the copy of chunk k overlaps the kernel of chunk k+1.
+// stream, so the copy of chunk k overlaps the kernels of chunks k+1 ..; with
+// NBUF staging buffers the kernels run ahead of the (PCIe-bound) copies.
 grape_status walks_host(const grape_graph* g, const WalkArgs& a, bool n2v, const Thresholds& T,
                         cudaStream_t stream, uint64_t* steps_host)
 {
+    constexpr int NB = GRAPE_HOST_NBUF;
     const uint64_t L = a.L;
-    // ~256 MB of output per chunk, at least 1 walk.
-    uint64_t chunk = (256ull << 20) / (4 * L);
+    uint64_t chunk = ((uint64_t)GRAPE_HOST_CHUNK_MB << 20) / (4 * L);   // walks per chunk, >= 1
     if (chunk < 1) chunk = 1;
     if (chunk > a.num_walks) chunk = a.num_walks;
-    uint32_t* d_starts[2] = {nullptr, nullptr};
-    uint32_t* d_out[2] = {nullptr, nullptr};
+    uint32_t* d_starts[NB] = {};
+    uint32_t* d_out[NB] = {};
     unsigned long long* d_steps = nullptr;
     cudaStream_t cs = nullptr;
-    cudaEvent_t ev_kernel[2] = {nullptr, nullptr}, ev_copied[2] = {nullptr, nullptr};
+    cudaEvent_t ev_kernel[NB] = {}, ev_copied[NB] = {};
     grape_status st = GRAPE_OK;
     cudaError_t e = cudaSuccess;
-    const int nbuf = a.num_walks > chunk ? 2 : 1;
+    const uint64_t nchunks = (a.num_walks + chunk - 1) / chunk;
+    const int nbuf = nchunks < (uint64_t)NB ? (int)nchunks : NB;
+    // one device allocation for all staging buffers: the graph's cached one when free
+    const uint64_t per = ((chunk * 4 + 255) & ~255ull) + ((chunk * L * 4 + 255) & ~255ull);
+    const uint64_t need = per * nbuf + 256;
+    grape_graph* gm = const_cast<grape_graph*>(g);
+    std::unique_lock<std::mutex> lk(gm->stage_mu, std::try_to_lock);
+    char* base = nullptr;
+    bool own = false;
+    if (lk.owns_lock()) {
+        if (gm->stage_bytes < need) {
+            cudaFree(gm->stage_buf);
+            gm->stage_buf = nullptr;
+            gm->stage_bytes = 0;
+            e = cudaMalloc(&gm->stage_buf, need);
+            if (e == cudaSuccess) gm->stage_bytes = need;
+        }
+        base = (char*)gm->stage_buf;
+    } else {
+        e = cudaMalloc((void**)&base, need);
+        own = e == cudaSuccess;
+    }
     for (int b = 0; b < nbuf && e == cudaSuccess; ++b) {
-        e = cudaMalloc(&d_starts[b], chunk * 4);
-        if (e == cudaSuccess) e = cudaMalloc(&d_out[b], chunk * L * 4);
-        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_kernel[b], cudaEventDisableTiming);
+        d_starts[b] = (uint32_t*)(base + b * per);
+        d_out[b] = (uint32_t*)(base + b * per + ((chunk * 4 + 255) & ~255ull));
+        e = cudaEventCreateWithFlags(&ev_kernel[b], cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_copied[b], cudaEventDisableTiming);
     }
-    if (e == cudaSuccess) e = cudaMalloc(&d_steps, 8);
+    if (e == cudaSuccess) d_steps = (unsigned long long*)(base + per * nbuf);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaMemsetAsync(d_steps, 0, 8, stream);
     if (e != cudaSuccess) {
@@ -136,13 +165,12 @@ grape_status walks_host(const grape_graph* g, const WalkArgs& a, bool n2v, const
         else if (steps_host) *steps_host += steps;
     }
     if (cs) { cudaStreamSynchronize(cs); cudaStreamDestroy(cs); }
-    for (int b = 0; b < 2; ++b) {
-        cudaFree(d_starts[b]);
-        cudaFree(d_out[b]);
+    cudaStreamSynchronize(stream);
+    for (int b = 0; b < NB; ++b) {
         if (ev_kernel[b]) cudaEventDestroy(ev_kernel[b]);
         if (ev_copied[b]) cudaEventDestroy(ev_copied[b]);
     }
-    cudaFree(d_steps);
+    if (own) cudaFree(base);
     return st;
 }
 

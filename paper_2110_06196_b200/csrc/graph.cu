@@ -194,6 +194,7 @@ void destroy_graph(grape_graph* g)
     cudaFree(g->cw);
     cudaFree(g->nodes);
     destroy_tables(g);
+    cudaFree(g->stage_buf);
     for (int l = 0; l < kFenceLevels; ++l) {
         cudaFree(g->col_fence[l]);
         cudaFree(g->cw_fence[l]);
@@ -207,8 +208,7 @@ grape_status build_graph(uint32_t n, uint64_t m, const uint64_t* off_in, const u
 {
     DeviceGuard guard(device);
     cudaError_t e = cudaGetLastError();  // clear stale errors
-    grape_graph* g = new grape_graph();
-    std::memset(g, 0, sizeof(*g));
+    grape_graph* g = new grape_graph();   // value-initialised (pointers null, counts 0)
     g->device = device;
     g->n = n;
     g->m = m;

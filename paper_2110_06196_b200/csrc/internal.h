@@ -2,6 +2,7 @@
 // Not part of the ABI (the ABI is include/grape_walk.h).
 #pragma once
 #include <cstdint>
+#include <mutex>
 #include <cuda_runtime.h>
 #include "grape_walk.h"
 
@@ -47,6 +48,11 @@ struct grape_graph {
     bool notri;              // records carry the no-common-neighbour flags (graph_tables.cu)
     uint32_t* ehash;      // per-row linear-probing sets of N(v): 2*deg(v) slots at 2*off[v]
     uint64_t table_bytes;
+    // host-buffer staging (capi.cu walks_host): device buffers kept between calls;
+    // a call that finds the mutex taken (a concurrent host-buffer call) allocates its own
+    std::mutex stage_mu;
+    void* stage_buf = nullptr;
+    uint64_t stage_bytes = 0;
     uint32_t max_degree;
     uint64_t max_row_weight;
     uint64_t device_bytes;
