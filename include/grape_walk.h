@@ -246,6 +246,9 @@ typedef struct {
     uint64_t guide_loads;       /* guide-table entries read (weighted proposals) */
     uint64_t hash_probes;       /* edge-hash sectors read by membership tests */
     uint64_t alu_decisions;     /* attempts decided without reading the graph */
+    uint64_t iterations;        /* lane-iterations of the state machine (one load at most each) */
+    uint64_t draw_iterations;   /* ... of them spent drawing only (no load) */
+    uint64_t back_iterations;   /* ... of them emitting a register-decided return (no load) */
 } grape_walk_stats;
 
 grape_status grape_walks_stats(const grape_graph* g, const uint32_t* starts, uint64_t num_walks,

@@ -61,7 +61,7 @@ class TableOptions(ctypes.Structure):
 
 STATS_FIELDS = ("sector_loads", "node_loads", "xnode_loads", "cw_probes", "col_probes", "col_loads",
                 "attempts", "membership_tests", "start_loads", "steps", "guide_loads", "hash_probes",
-                "alu_decisions")
+                "alu_decisions", "iterations", "draw_iterations", "back_iterations")
 
 
 class WalkStats(ctypes.Structure):

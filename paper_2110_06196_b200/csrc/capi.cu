@@ -435,6 +435,9 @@ grape_status grape_walks_stats_approx(const grape_graph* g, const uint32_t* star
     stats->guide_loads = h[10];
     stats->hash_probes = h[11];
     stats->alu_decisions = h[12];
+    stats->iterations = h[13];
+    stats->draw_iterations = h[14];
+    stats->back_iterations = h[15];
     return GRAPE_OK;
 }
 

@@ -80,7 +80,7 @@ struct WalkArgs {
     unsigned long long* stats;       // device grape_walk_stats (as u64[kStatsWords]) or NULL
     uint32_t dT;                     // approximated walks: SUSS degree threshold (0: exact walks)
 };
-constexpr int kStatsWords = 13;
+constexpr int kStatsWords = 16;
 
 // walk.cu: launch one walk kernel (device buffers) on `stream`.
 // node2vec == false -> first order.  Returns cudaGetLastError() of the launch.

@@ -38,6 +38,12 @@ constexpr uint32_t kEmptySlot = 0xFFFFFFFFu;
 #ifndef GRAPE_TAB_DRAWS
 #define GRAPE_TAB_DRAWS 2
 #endif
+#ifndef GRAPE_TAB_DRAWS_EXTRA
+#define GRAPE_TAB_DRAWS_EXTRA 0
+#endif
+#ifndef GRAPE_TAB_DRAWS_QUORUM
+#define GRAPE_TAB_DRAWS_QUORUM 16
+#endif
 #ifndef GRAPE_TAB_STATIC_PCT
 #define GRAPE_TAB_STATIC_PCT 50
 #endif
@@ -116,7 +122,7 @@ __device__ __forceinline__ void ld8(const uint32_t* p, uint32_t (&v)[8])
 }
 
 enum : int { C_LOADS = 0, C_NODE, C_XNODE, C_CWPROBE, C_COLPROBE, C_REC, C_ATTEMPT, C_MEMB, C_START, C_STEPS,
-             C_GUIDE, C_HASH, C_ALU };
+             C_GUIDE, C_HASH, C_ALU, C_ITER, C_ITER_DRAW, C_ITER_BACK };
 
 // WEIGHTED: 32-B records + guide; else 16-B records indexed by the draw.
 template <bool WEIGHTED, bool FAT, bool COMPACT, bool NODE2VEC, bool NEED_MEMBER, bool STATS, bool SUSS>
@@ -193,6 +199,11 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
             const char* addr = b + (e << sh);
             if (load) ld8(sector_of(addr), sec);
             j = word_of(addr);
+        }
+        if (STATS && st != ST_DONE) {
+            ++cnt[C_ITER];
+            cnt[C_ITER_DRAW] += st == ST_DRAW;
+            cnt[C_ITER_BACK] += st == ST_BACK;
         }
         if (STATS && load) {
             ++cnt[C_LOADS];
@@ -487,9 +498,13 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
         // in the same iteration, up to GRAPE_TAB_DRAWS draws; a register-decided
         // return x = t is emitted on the spot when another draw follows it.
 #pragma unroll 1
-        for (int k = 0; k < GRAPE_TAB_DRAWS; ++k) {
+        for (int k = 0; k < GRAPE_TAB_DRAWS + GRAPE_TAB_DRAWS_EXTRA; ++k) {
             __syncwarp();
-            if (!__any_sync(0xffffffffu, draw)) break;
+            if (k < GRAPE_TAB_DRAWS) {
+                if (!__any_sync(0xffffffffu, draw)) break;
+            } else if (__popc(__ballot_sync(0xffffffffu, draw)) < GRAPE_TAB_DRAWS_QUORUM) {
+                break;   // extra rounds only while most of the warp is still drawing
+            }
             const bool sub = SUSS && vdeg > P.dT;   // this step runs on a SUSS sub-sample
             if (SUSS && WEIGHTED && draw && sub && cb < P.dT) {   // first: read the dT candidates
                 draw = false;
@@ -542,7 +557,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                 gsrc = false;
                 draw = false;
                 if (ret) {          // return to t, no read
-                    if (k + 1 < GRAPE_TAB_DRAWS && s + 1 < L) {   // emit now; t's row is not empty
+                    if (k + 1 < GRAPE_TAB_DRAWS + GRAPE_TAB_DRAWS_EXTRA && s + 1 < L) {   // emit now; t's row is not empty
                         w.put(s, tid);
                         ++steps;
                         uint32_t q;
