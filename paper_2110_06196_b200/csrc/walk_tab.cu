@@ -93,8 +93,8 @@ __device__ __forceinline__ uint32_t fmix32(uint32_t h)
 // carries across a multiple of 2^32.
 __device__ __forceinline__ uint32_t bounded32(uint64_t x64, uint32_t w)
 {
-    const uint64_t lo = ((uint64_t)(uint32_t)x64 * w) >> 32;
-    return (uint32_t)(((uint64_t)(uint32_t)(x64 >> 32) * w + lo) >> 32);
+    const uint32_t lo = __umulhi((uint32_t)x64, w);                             // IMAD.HI
+    return (uint32_t)(((uint64_t)(uint32_t)(x64 >> 32) * w + lo) >> 32);      // IMAD.WIDE + carry word
 }
 
 __device__ __forceinline__ uint32_t pick8(const uint32_t (&w)[8], uint32_t j)
@@ -216,11 +216,11 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
 
         // ---- interpret the sector
         bool emit = false, back = st == ST_BACK, fin = false, draw = st == ST_DRAW, decide = false;
-        // the record of the taken arc (valid when emit): head x, its node record,
-        // the new T = [nlo, nhi) and S = [nslo, nshi)
-        uint32_t xs = 0, xd = 0, xw = 0, nlo = 0, nhi = 0, nslo = 0, nshi = 0;
-        uint32_t xfl = 0;   // the record's flags: bit 1 = no common neighbour of (v, x), bit 0 = of (x, v)
+        // when emit: the taken arc's record is in sec (at word j for 8/16-B records) —
+        // read by the emit block itself, so no per-branch copies — or, after an
+        // unweighted membership test, in the kept registers (kept)
         bool have_rec = false;   // the sector in hand is x's record
+        bool kept = false;
         if (st == ST_REC) {
             have_rec = true;
             bool found = true;
@@ -231,49 +231,24 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                     found = false;
                     ++ri;
                 }
-                const uint32_t xr = h ? sec[4] : sec[0];
-                x = xr & P.xmask;
-                xfl = P.notri ? xr >> 30 : 0u;
-                nlo = h ? sec[6] : sec[2];
-                nhi = h ? sec[7] : sec[3];
-                nshi = hi;
-                nslo = P.wsym ? hi - (nhi - nlo) : 1u;   // [1, 0): unknown (asymmetric weights)
-                if (!P.wsym) nshi = 0;
+                x = (h ? sec[4] : sec[0]) & P.xmask;
             } else if constexpr (WEIGHTED) {
                 if (scan && r >= sec[1]) {   // past this record's interval: the next one
                     found = false;
                     ++ri;
                 }
                 x = sec[0];
-                nlo = sec[2]; nhi = sec[3];
-                xs = sec[4]; xd = sec[5] & 0x0FFFFFFFu; xw = sec[6];
-                xfl = (sec[5] >> 28) & 3u;
-                nslo = sec[7]; nshi = sec[1];
             } else if constexpr (COMPACT) {   // 8-B {x, rev} at word j (even)
                 const uint32_t xr = pick8(sec, j);
                 x = xr & P.xmask;
-                xfl = P.notri ? xr >> 30 : 0u;
-                hfl = xfl;
-                const uint32_t rev = pick8(sec, j | 1);
-                hrev = rev;
-                nlo = rev;
-                nhi = rev == kNone ? rev : rev + 1;
-                nslo = ri;
-                nshi = ri + 1;
+                hfl = P.notri ? xr >> 30 : 0u;
+                hrev = pick8(sec, j | 1);
             } else {
                 const bool h = (j & 4) != 0;
                 x = h ? sec[4] : sec[0];
-                const uint32_t rev = h ? sec[5] : sec[1];
-                xs = h ? sec[6] : sec[2];
-                xd = h ? sec[7] : sec[3];
-                xfl = (xd >> 28) & 3u;
-                xd &= 0x0FFFFFFFu;
-                xw = xd;
-                hrev = rev; hxs = xs; hxd = xd; hfl = xfl;
-                nlo = rev;
-                nhi = rev == kNone ? rev : rev + 1;   // [rev, rev+1), or the empty [NONE, NONE)
-                nslo = ri;
-                nshi = ri + 1;
+                hrev = h ? sec[5] : sec[1];
+                hxs = h ? sec[6] : sec[2];
+                hxd = h ? sec[7] : sec[3];
             }
             if (found) {
                 if (acc) emit = true;
@@ -304,10 +279,6 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                 have_rec = true;
                 gsrc = true;
                 x = sec[0];
-                nlo = sec[2]; nhi = sec[3];
-                xs = sec[4]; xd = sec[5] & 0x0FFFFFFFu; xw = sec[6];
-                xfl = (sec[5] >> 28) & 3u;
-                nslo = sec[7]; nshi = sec[1];
                 if (acc) emit = true;
                 else decide = true;
             } else {          // the bucket proposes i_lo = e1 whatever the draw
@@ -361,12 +332,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                         st = gsrc ? ST_GUIDE : ST_REC;
                     } else {          // the record was kept in registers
                         emit = true;
-                        xs = hxs; xd = hxd; xw = hxd;   // (compact: unused, x's node record is read)
-                        xfl = hfl;
-                        nlo = hrev;
-                        nhi = hrev == kNone ? hrev : hrev + 1;
-                        nslo = ri;
-                        nshi = ri + 1;
+                        kept = true;
                     }
                 } else {
                     draw = true;
@@ -436,21 +402,52 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
             w.put(s, x);
             ++steps;
             bool need_node = false;
-            if (emit && !(COMPACT && x == tid)) {
-                tid = vid; tstart = vstart; tdeg = vdeg; tW = vW;
-                vid = x;
-                if constexpr (COMPACT) need_node = true;   // x's node record: next iteration
-                else { vstart = xs; vdeg = xd; vW = xw; }
-                tlo = nlo; thi = nhi; slo = nslo; shi = nshi;
-                nt = (xfl >> 1) != 0; ntr = (xfl & 1) != 0;
-            } else if (emit) {   // compact record of a return: t's node record is in registers
-                uint32_t q;
-                q = vstart; vstart = tstart; tstart = q;
-                q = vdeg; vdeg = tdeg; tdeg = q;
-                q = vW; vW = tW; tW = q;
-                q = vid; vid = tid; tid = q;
-                tlo = nlo; thi = nhi; slo = nslo; shi = nshi;
-                nt = (xfl >> 1) != 0; ntr = (xfl & 1) != 0;
+            if (emit) {   // the record of the taken arc: T, S, flags and (full records) x's node record
+                uint32_t fnlo, fnhi, fnslo, fnshi, fxs = 0, fxd = 0, fxw = 0, ffl;
+                if constexpr (WEIGHTED && !COMPACT) {   // 32-B record at word 0 (also a fat guide entry)
+                    fnlo = sec[2]; fnhi = sec[3]; fnslo = sec[7]; fnshi = sec[1];
+                    fxs = sec[4]; fxd = sec[5] & 0x0FFFFFFFu; fxw = sec[6];
+                    ffl = (sec[5] >> 28) & 3u;
+                } else if constexpr (WEIGHTED) {        // 16-B {x, hi, rlo, rhi} at word j
+                    const bool h = (j & 4) != 0;
+                    const uint32_t hi = h ? sec[5] : sec[1];
+                    ffl = P.notri ? (h ? sec[4] : sec[0]) >> 30 : 0u;
+                    fnlo = h ? sec[6] : sec[2];
+                    fnhi = h ? sec[7] : sec[3];
+                    fnshi = P.wsym ? hi : 0u;
+                    fnslo = P.wsym ? hi - (fnhi - fnlo) : 1u;   // [1, 0): unknown (asymmetric weights)
+                } else {                                 // unweighted: index intervals
+                    uint32_t rev;
+                    if constexpr (COMPACT) {
+                        rev = hrev;
+                        ffl = hfl;
+                    } else {
+                        rev = hrev;
+                        fxs = hxs;
+                        ffl = (hxd >> 28) & 3u;
+                        fxd = hxd & 0x0FFFFFFFu;
+                        fxw = fxd;
+                    }
+                    (void)kept;
+                    fnlo = rev;
+                    fnhi = rev == kNone ? rev : rev + 1;   // [rev, rev+1), or the empty [NONE, NONE)
+                    fnslo = ri;
+                    fnshi = ri + 1;
+                }
+                if (!(COMPACT && x == tid)) {
+                    tid = vid; tstart = vstart; tdeg = vdeg; tW = vW;
+                    vid = x;
+                    if constexpr (COMPACT) need_node = true;   // x's node record: next iteration
+                    else { vstart = fxs; vdeg = fxd; vW = fxw; }
+                } else {   // compact record of a return: t's node record is in registers
+                    uint32_t q;
+                    q = vstart; vstart = tstart; tstart = q;
+                    q = vdeg; vdeg = tdeg; tdeg = q;
+                    q = vW; vW = tW; tW = q;
+                    q = vid; vid = tid; tid = q;
+                }
+                tlo = fnlo; thi = fnhi; slo = fnslo; shi = fnshi;
+                nt = (ffl >> 1) != 0; ntr = (ffl & 1) != 0;
             } else {   // x = t: v and t swap, and so do T and S
                 const bool b_ = nt; nt = ntr; ntr = b_;
                 uint32_t q;
