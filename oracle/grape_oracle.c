@@ -452,3 +452,117 @@ int oracle_walks_approx(uint32_t n, const uint64_t* off, const uint32_t* col, co
         *steps_out += steps;
     return 0;
 }
+
+/* ---------------------------------------------------------------------------
+ * The paper's own node2vec sampler, step by step — SURVEY.md §8(f) row f2;
+ * PAPER.md §4.3.2 "Efficient sampling for Node2Vec random walks":
+ *   "1) computation of the un-normalized transition probabilities to each
+ *    neighbour of v according to the provided in-out and return biases;
+ *    2) computation of the un-normalized cumulative distribution, which is
+ *    equivalent to a cumulative sum; 3) uniform sampling of a random value
+ *    between 0 and the maximum value in the un-normalized cumulative
+ *    distribution; 4) identification of the corresponding index".
+ * Readings (f2-*):
+ *   - the biases alpha = 1/p, 1, 1/q (Eq.1) enter as the integer
+ *     thresholds T_p, T_1, T_q of §8(c) c9 (proportional to them; exact for
+ *     every BASELINE config): pi_x = w_vx * T_class(x), a u64;
+ *   - the running sum is exact (u128: deg < 2^28 terms below 2^64);
+ *   - step 3 draws ONE x64 per step, DRAW(seed, wid, s, 0) words o1:o0, and
+ *     maps it by BOUNDED on the total (128-bit): r = floor(x64 * S / 2^64);
+ *   - step 4 takes the smallest i with cum_i > r;
+ *   - the first step of a walk (no t) is the first-order step (§8(c) c2), and
+ *     so is every step when p = q = 1 (then pi = w * T with one T, which
+ *     selects exactly the first-order index — see the proof in DESIGN.md §7c).
+ * ------------------------------------------------------------------------- */
+typedef unsigned __int128 oracle_u128;
+
+/* floor(x64 * S / 2^64) for S < 2^128 with the result < 2^128 (S < 2^92 here). */
+static oracle_u128 oracle_bounded128(uint64_t x64, oracle_u128 S)
+{
+    uint64_t s_lo = (uint64_t)S, s_hi = (uint64_t)(S >> 64);
+    oracle_u128 lo = ((oracle_u128)x64 * s_lo) >> 64;
+    return (oracle_u128)x64 * s_hi + lo;
+}
+
+/* One CDF node2vec step from v coming from t (t != NONE). */
+uint32_t oracle_cdf_step(const uint64_t* off, const uint32_t* col, const uint64_t* cw, const uint64_t T[3],
+                         uint64_t seed, uint64_t wid, uint32_t s, uint32_t t, uint32_t v)
+{
+    uint64_t lo = off[v], d = off[v + 1] - lo, i;
+    oracle_u128 total = 0, cum = 0, r;
+    uint32_t o[4];
+    for (i = 0; i < d; i++) {                    /* step 1-2 (first pass: the total) */
+        uint32_t x = col[lo + i];
+        uint64_t w = cw == NULL ? 1 : cw[lo + i] - (i > 0 ? cw[lo + i - 1] : 0);
+        uint64_t Tc = x == t ? T[0] : (oracle_in_row(off, col, t, x) ? T[1] : T[2]);
+        total += (oracle_u128)w * Tc;
+    }
+    oracle_draw(seed, wid, s, 0, o);             /* step 3 */
+    r = oracle_bounded128(x64_of(o), total);
+    for (i = 0; i < d; i++) {                    /* step 4 (second pass: the running sum) */
+        uint32_t x = col[lo + i];
+        uint64_t w = cw == NULL ? 1 : cw[lo + i] - (i > 0 ? cw[lo + i - 1] : 0);
+        uint64_t Tc = x == t ? T[0] : (oracle_in_row(off, col, t, x) ? T[1] : T[2]);
+        cum += (oracle_u128)w * Tc;
+        if (cum > r)
+            return x;
+    }
+    return ORACLE_NONE;   /* unreachable: cum reaches total > r */
+}
+
+/* WALK with the CDF sampler (node2vec only; conventions as oracle_walks). */
+int oracle_walks_cdf(uint32_t n, const uint64_t* off, const uint32_t* col, const uint64_t* cw,
+                     const uint32_t* starts, uint64_t num_walks, uint64_t base, uint32_t L,
+                     double p, double q, uint64_t seed, uint32_t* out, uint64_t* steps_out)
+{
+    uint64_t T[3];
+    uint64_t i, steps = 0;
+    if (oracle_thresholds(p, q, T) != 0)
+        return 1;
+    for (i = 0; i < num_walks; i++) {
+        uint32_t* row = out + i * (uint64_t)L;
+        uint64_t wid = base + i;
+        uint32_t start = starts[i];
+        uint32_t t, v, s, j;
+        for (j = 0; j < L; j++)
+            row[j] = ORACLE_PAD;
+        if (start >= n || L == 0)
+            continue;
+        row[0] = start;
+        t = ORACLE_NONE;
+        v = start;
+        for (s = 1; s < L; s++) {
+            uint32_t x;
+            if (off[v + 1] == off[v])
+                break;
+            if (t == ORACLE_NONE) {
+                uint32_t o[4];
+                oracle_draw(seed, wid, s, 0, o);
+                x = oracle_propose(off, col, cw, v, x64_of(o));
+            } else {
+                x = oracle_cdf_step(off, col, cw, T, seed, wid, s, t, v);
+            }
+            row[s] = x;
+            steps++;
+            t = v;
+            v = x;
+        }
+    }
+    if (steps_out != NULL)
+        *steps_out += steps;
+    return 0;
+}
+
+/* Batched single CDF steps for the statistical pins (tests only). */
+int oracle_cdf_steps(const uint64_t* off, const uint32_t* col, const uint64_t* cw, double p, double q,
+                     uint64_t seed, uint32_t t, uint32_t v, uint32_t s, uint64_t wid0, uint64_t count,
+                     uint32_t* x_out)
+{
+    uint64_t T[3];
+    uint64_t k;
+    if (oracle_thresholds(p, q, T) != 0)
+        return 1;
+    for (k = 0; k < count; k++)
+        x_out[k] = oracle_cdf_step(off, col, cw, T, seed, wid0 + k, s, t, v);
+    return 0;
+}

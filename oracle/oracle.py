@@ -75,6 +75,14 @@ def _load():
                 ctypes.c_uint32, ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_uint64,
                 ctypes.c_uint32, _u64p, _u64p, _u32p, _u64p]
             lib.oracle_walks_approx.restype = ctypes.c_int
+            lib.oracle_walks_cdf.argtypes = [
+                ctypes.c_uint32, _u64p, _u32p, _u64p, _u32p, ctypes.c_uint64, ctypes.c_uint64,
+                ctypes.c_uint32, ctypes.c_double, ctypes.c_double, ctypes.c_uint64, _u32p, _u64p]
+            lib.oracle_walks_cdf.restype = ctypes.c_int
+            lib.oracle_cdf_steps.argtypes = [
+                _u64p, _u32p, _u64p, ctypes.c_double, ctypes.c_double, ctypes.c_uint64,
+                ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, _u32p]
+            lib.oracle_cdf_steps.restype = ctypes.c_int
             _lib = lib
     return _lib
 
@@ -185,6 +193,27 @@ class Oracle:
         if rc != 0:
             raise ValueError(f"oracle rejected p={p} q={q}")
         return out, int(steps.value)
+
+    def walks_cdf(self, starts, L: int, *, p: float = 1.0, q: float = 1.0, seed: int = 42, base: int = 0):
+        """Node2vec walks with the paper's CDF sampler (§8(f) f2); (matrix, steps)."""
+        starts = np.ascontiguousarray(starts, dtype=np.uint32)
+        nw = len(starts)
+        out = np.empty((nw, L), dtype=np.uint32)
+        steps = ctypes.c_uint64(0)
+        rc = _load().oracle_walks_cdf(self.n, _p64(self.off), _p32(self.col), _p64(self.cw), _p32(starts), nw,
+                                      base, L, float(p), float(q), seed, out.ctypes.data_as(_u32p),
+                                      ctypes.byref(steps))
+        if rc != 0:
+            raise ValueError(f"oracle rejected p={p} q={q}")
+        return out, int(steps.value)
+
+    def cdf_steps(self, t: int, v: int, s: int, wid0: int, count: int, p: float, q: float, seed: int = 42):
+        x = np.empty(count, dtype=np.uint32)
+        rc = _load().oracle_cdf_steps(_p64(self.off), _p32(self.col), _p64(self.cw), float(p), float(q), seed,
+                                      t, v, s, wid0, count, _p32(x))
+        if rc != 0:
+            raise ValueError(f"oracle rejected p={p} q={q}")
+        return x
 
     def first_order_steps(self, v: int, s: int, wid0: int, count: int, seed: int = 42):
         x = np.empty(count, dtype=np.uint32)

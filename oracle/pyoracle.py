@@ -156,6 +156,44 @@ class PyGraph:
             t, v = v, x
         return row, steps
 
+    # ---- the paper's CDF sampler (§8(f) f2; P:507-511 steps 1-4) ----
+    def cdf_step(self, T, seed, wid, s, t, v):
+        row = self.rows[v]
+        if self.cw is None:
+            ws = [1] * len(row)
+        else:
+            c = self.cw[v]
+            ws = [c[i] - (c[i - 1] if i else 0) for i in range(len(c))]
+        pis = [wx * (T[0] if x == t else (T[1] if self.member(t, x) else T[2])) for x, wx in zip(row, ws)]
+        o = draw(seed, wid, s, 0)
+        r = ((o[1] << 32 | o[0]) * sum(pis)) >> 64       # exact big-integer product
+        acc = 0
+        for x, pi in zip(row, pis):
+            acc += pi
+            if acc > r:
+                return x
+        raise AssertionError("unreachable")
+
+    def walk_cdf(self, start, wid, L, p=1.0, q=1.0, seed=42):
+        row = [PAD] * L
+        if start >= self.n or L == 0:
+            return row, 0
+        T = thresholds(p, q)
+        row[0] = start
+        t, v, steps = NONE, start, 0
+        for s in range(1, L):
+            if not self.rows[v]:
+                break
+            if t == NONE:
+                o = draw(seed, wid, s, 0)
+                x = self.propose(v, (o[1] << 32) | o[0])
+            else:
+                x = self.cdf_step(T, seed, wid, s, t, v)
+            row[s] = x
+            steps += 1
+            t, v = v, x
+        return row, steps
+
     def walk(self, start, wid, L, mode="node2vec", p=1.0, q=1.0, seed=42, mutation=None):
         row = [PAD] * L
         if start >= self.n or L == 0:
