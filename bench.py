@@ -249,6 +249,8 @@ def run_ours(args):
         kw = dict(seed=wk["seed"], walk_id_base=base, out=out_buf, steps=ctr)
         if dT:
             grape.walks_approx(dg, st_buf, L, dT, node2vec=node2vec, p=wk["p"], q=wk["q"], **kw)
+        elif args.sampler == "cdf":
+            grape.walks_node2vec_cdf(dg, st_buf, L, wk["p"], wk["q"], **kw)
         elif node2vec:
             grape.walks_node2vec(dg, st_buf, L, wk["p"], wk["q"], **kw)
         else:
@@ -317,7 +319,7 @@ def run_ours(args):
     # ---- roofline of the walk kernel: event counts from the counting
     # build of the same kernel (grape_walks_stats, untimed), times the measured time.
     roof = None
-    if rank == 0:
+    if rank == 0 and args.sampler != "cdf":   # (no counting build of the CDF sampler)
         _, ev = grape.walks_stats(dg, starts, L, node2vec=node2vec, p=wk["p"], q=wk["q"], seed=wk["seed"],
                                   degree_threshold=dT,
                                   walk_id_base=base, out=out)
@@ -381,6 +383,8 @@ def run_ours(args):
         metric = "random-walk steps/sec (node2vec 2nd-order)" if node2vec else "random-walk steps/sec (first-order)"
         if dT:
             metric = metric[:-1] + f", approximated: SUSS d_T={dT})"
+        if args.sampler == "cdf":
+            metric = metric[:-1] + ", paper CDF sampler)"
         line = {"metric": metric, "value": value, "unit": "steps/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32/u64 integer",
@@ -413,6 +417,9 @@ def main():
                     help="ncu dram bytes per launch of the walk kernel (from profiles/)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-tables", action="store_true", help="GRAPE_NO_TABLES: the v3 fenced-search walker")
+    ap.add_argument("--sampler", default="rejection", choices=["rejection", "cdf"],
+                    help="node2vec sampler: the default rejection rules, or the paper's CDF sampler "
+                         "(grape_walks_node2vec_cdf, P:507-511)")
     ap.add_argument("--approx", type=int, default=0,
                     help="approximated walks with SUSS degree threshold d_T (grape_walks_approx; 0 = exact)")
     ap.add_argument("--layout", default="", help="force table layout fields, e.g. "

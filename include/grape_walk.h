@@ -222,6 +222,24 @@ grape_status grape_walks_approx(const grape_graph* g, const uint32_t* starts, ui
                                 uint64_t* steps_out, cudaStream_t stream);
 
 /*
+ * grape_walks_node2vec_cdf — node2vec walks with the paper's own sampler
+ * (§4.3.2, P:507-511 steps 1-4): at each step
+ * after the first, the un-normalised probabilities pi_x = w_vx * T_class(x)
+ * of every neighbour of v (classes and integer thresholds as above), their
+ * exact running sum S_i (128-bit), ONE draw x64 = DRAW(seed, wid, s, 0) mapped
+ * to r = floor(x64 * S / 2^64), and the neighbour at the smallest i with
+ * S_i > r.  The first step is the first-order step; with p = q = 1 every walk
+ * equals grape_walks_first_order's.  Same law as grape_walks_node2vec (Eq.1),
+ * different draws, so different walks; O(deg v) work per step.
+ * Arguments, ownership and errors as grape_walks_node2vec; EINVAL if the graph
+ * has no sampling tables (GRAPE_NO_TABLES).
+ */
+grape_status grape_walks_node2vec_cdf(const grape_graph* g, const uint32_t* starts, uint64_t num_walks,
+                                      uint64_t walk_id_base, uint32_t walk_length, double p, double q,
+                                      uint64_t seed, uint32_t* out, uint64_t* steps_out,
+                                      cudaStream_t stream);
+
+/*
  * grape_walks_stats — diagnostics: run the same walks as grape_walks_first_order
  * (node2vec = 0) or grape_walks_node2vec (node2vec = 1) with event counters
  * compiled into the kernel, and return the counts.  `out` receives exactly the

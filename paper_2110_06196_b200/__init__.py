@@ -160,6 +160,13 @@ def walks_node2vec(g: Graph, starts, L: int, p: float, q: float, *, seed: int = 
                   out, steps, stream)
 
 
+def walks_node2vec_cdf(g: Graph, starts, L: int, p: float, q: float, *, seed: int = 42,
+                       walk_id_base: int = 0, out=None, steps=None, stream=None) -> torch.Tensor:
+    """grape_walks_node2vec_cdf: node2vec with the paper's inverse-CDF sampler."""
+    return _walks("grape_walks_node2vec_cdf", g, starts, L, (float(p), float(q)), seed, walk_id_base,
+                  out, steps, stream)
+
+
 def walks_approx(g: Graph, starts, L: int, degree_threshold: int, *, node2vec: bool = True, p: float = 1.0,
                  q: float = 1.0, seed: int = 42, walk_id_base: int = 0, out=None, steps=None,
                  stream=None) -> torch.Tensor:
@@ -218,3 +225,4 @@ grape_walks_first_order = walks_first_order
 grape_walks_node2vec = walks_node2vec
 grape_walks_stats = walks_stats
 grape_walks_approx = walks_approx
+grape_walks_node2vec_cdf = walks_node2vec_cdf

@@ -176,7 +176,8 @@ grape_status walks_host(const grape_graph* g, const WalkArgs& a, bool n2v, const
 
 grape_status walks_common(const grape_graph* g, const uint32_t* starts, uint64_t num_walks,
                           uint64_t base, uint32_t L, bool n2v, double p, double q, uint64_t seed,
-                          uint32_t* out, uint64_t* steps_out, cudaStream_t stream, uint32_t dT = 0)
+                          uint32_t* out, uint64_t* steps_out, cudaStream_t stream, uint32_t dT = 0,
+                          uint32_t sampler = 0)
 {
     g_err[0] = 0;
     if (g == nullptr || (num_walks > 0 && (starts == nullptr || out == nullptr))) {
@@ -194,6 +195,11 @@ grape_status walks_common(const grape_graph* g, const uint32_t* starts, uint64_t
     Thresholds T{1ull << 32, 1ull << 32, 1ull << 32};
     if (n2v && !node2vec_thresholds(p, q, &T)) return GRAPE_EINVAL;
     if (dT >= g->max_degree) dT = 0;   // no row exceeds the threshold: the exact walks
+    if (sampler == 1 && !g->tables) {
+        set_error("the CDF sampler needs the sampling tables (graph built with GRAPE_NO_TABLES "
+                  "or outside their index ranges)");
+        return GRAPE_EINVAL;
+    }
     if (dT != 0 && !g->tables) {
         set_error("approximated walks need the sampling tables (graph built with GRAPE_NO_TABLES "
                   "or outside their index ranges)");
@@ -220,6 +226,7 @@ grape_status walks_common(const grape_graph* g, const uint32_t* starts, uint64_t
     a.out = out;
     a.steps_out = nullptr;
     a.dT = dT;
+    a.sampler = sampler;
     if (ms == Mem::Host) return walks_host(g, a, n2v, T, stream, steps_out);
     if (steps_out != nullptr && classify(steps_out) != Mem::Device) {
         set_error("with device buffers, steps_out must be device memory (or NULL)");
@@ -355,6 +362,14 @@ grape_status grape_walks_approx(const grape_graph* g, const uint32_t* starts, ui
     if (!node2vec) { p = 1.0; q = 1.0; }
     return walks_common(g, starts, num_walks, walk_id_base, walk_length, node2vec != 0, p, q, seed, out,
                         steps_out, stream, degree_threshold);
+}
+
+grape_status grape_walks_node2vec_cdf(const grape_graph* g, const uint32_t* starts, uint64_t num_walks,
+                                      uint64_t walk_id_base, uint32_t walk_length, double p, double q,
+                                      uint64_t seed, uint32_t* out, uint64_t* steps_out, cudaStream_t stream)
+{
+    return walks_common(g, starts, num_walks, walk_id_base, walk_length, true, p, q, seed, out, steps_out,
+                        stream, 0, 1);
 }
 
 grape_status grape_walks_stats(const grape_graph* g, const uint32_t* starts, uint64_t num_walks,

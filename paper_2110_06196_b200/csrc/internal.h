@@ -79,6 +79,7 @@ struct WalkArgs {
     unsigned long long* steps_out;   // device, may be NULL
     unsigned long long* stats;       // device grape_walk_stats (as u64[kStatsWords]) or NULL
     uint32_t dT;                     // approximated walks: SUSS degree threshold (0: exact walks)
+    uint32_t sampler;                // 0: rejection (the default rules), 1: the paper's CDF sampler (walk_cdf.cu)
 };
 constexpr int kStatsWords = 16;
 
@@ -86,6 +87,7 @@ constexpr int kStatsWords = 16;
 // node2vec == false -> first order.  Returns cudaGetLastError() of the launch.
 cudaError_t launch_walks(const grape_graph* g, const WalkArgs& a, bool node2vec,
                          const Thresholds& T, cudaStream_t stream);
+cudaError_t launch_walks_cdf(const grape_graph* g, const WalkArgs& a, const Thresholds& T, cudaStream_t stream);
 cudaError_t launch_walks_tab(const grape_graph* g, const WalkArgs& a, bool node2vec,
                              const Thresholds& T, cudaStream_t stream);
 cudaError_t launch_walks_sm(const grape_graph* g, const WalkArgs& a, bool node2vec,

@@ -241,6 +241,7 @@ cudaError_t launch_walks_structured(const grape_graph* g, const WalkArgs& a, boo
 cudaError_t launch_walks(const grape_graph* g, const WalkArgs& a, bool node2vec, const Thresholds& T,
                          cudaStream_t stream)
 {
+    if (a.sampler == 1) return launch_walks_cdf(g, a, T, stream);
     if (g->tables) return launch_walks_tab(g, a, node2vec, T, stream);
     if (GRAPE_WALKER == 2) return launch_walks_structured(g, a, node2vec, T, stream);
     return launch_walks_sm(g, a, node2vec, T, stream);
