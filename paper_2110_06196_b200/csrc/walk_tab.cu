@@ -1,31 +1,40 @@
-// walk_tab.cu — the v4 walker: convergent state machine over the sampling
-// tables of graph_tables.cu ("v4").  Same rules, same results as
-// every other walker (include/grape_walk.h); the oracle decides.
+// walk_tab.cu — the table walker (v4/v5/v6): a convergent state machine over
+// the sampling tables of graph_tables.cu.  Same rules, same
+// results as every other walker (include/grape_walk.h); the oracle decides.
 //
 // Each lane owns one walk.  Every iteration of the outer loop issues at most
-// ONE aligned 32-byte sector load per lane (LDG.E.ENL2.256), whatever the lane
-// is doing:
-//   ST_START  starts[i]                          -> row[0]
-//   ST_NODE   node record of v {start, deg, W_v}
-//   ST_GUIDE  guide entry of the draw's bucket    -> first candidate index
-//   ST_REC    arc record(s) {x, hi, rlo, rhi}     -> proposal x, and the reverse arc's
-//                                                   interval for the next step
-//   ST_HASH   one bucket of t's edge-hash set     -> "x in N(t)"
-// then an ALU-only phase (the inner loop) that may run several draws, emits and
-// walk ends without touching memory:
+// ONE aligned 32-byte sector load per lane (LDG.E.ENL2.256), its address
+// computed in one place for every state:
+//   ST_START  starts[i]                           -> row[0]
+//   ST_NODE   node record {start, deg, W}          -> a start node (or, compact
+//                                                    records, a taken arc's head)
+//   ST_GUIDE  guide entry of the draw's bucket     -> the proposal and its record (fat,
+//                                                    unsplit), or the split boundary
+//   ST_REC    arc record {x, hi, rlo, rhi, x's node record, lo}
+//                                                  -> proposal x, the reverse arc's interval
+//                                                    and the pair's no-common-neighbour flags
+//   ST_HASH   one bucket of t's edge-hash set      -> "x in N(t)"
+//   ST_CAND   (SUSS, weighted) a candidate's record into the lane's scratch
+// No load: ST_DRAW (keep drawing), ST_BACK (emit a register-decided return).
+// After the load: the decision where x is needed, the walk's advance (emit,
+// reading the taken arc's record from the sector in hand), and up to
+// GRAPE_TAB_DRAWS draws:
 //   * The three acceptance classes (thresholds §8(c) c9) split the
 //     u range into bands.  When u accepts all classes or rejects all, x does
 //     not matter (§8(c) c12: early accept / early reject).  When the decision
-//     hinges only on "x == t", it is settled by comparing r with the interval
-//     [tlo, thi) that the proposal index of t occupies in v's row — known from
-//     the arc record that brought the walk to v — so the attempt costs a
-//     Philox draw and nothing else; an accepted return x = t needs no load
-//     either (t's node record is kept in registers, v and t swap).
+//     hinges only on "x == t" — always so when the pair (t, v) has no common
+//     neighbour, since then every x != t is class q — it is settled by
+//     comparing r with the interval [tlo, thi) that the proposal index of t
+//     occupies in v's row, known from the arc record that brought the walk to
+//     v: the attempt costs a Philox draw and nothing else; an accepted return
+//     x = t needs no load either (t's node record is in registers, v and t swap).
 //   * Only when the class of x matters beyond "x == t" is x read and, if
 //     x != t, looked up in t's edge-hash set.
-// Counter layout, bounded draws, thresholds and PAD handling are the ABI's;
-// every decision above is decision-identical to the oracle's loop (the GPU
-// parity tests compare whole walk matrices bit for bit).
+// Walks are assigned round-robin for the first half of the launch, then from a
+// warp-aggregated shared counter (balances the tail).  Counter layout, bounded
+// draws, thresholds and PAD handling are the ABI's; every decision above is
+// decision-identical to the oracle's loop (the GPU parity tests compare whole
+// walk matrices bit for bit).
 #include "walk_common.cuh"
 
 namespace grape {
@@ -37,12 +46,6 @@ enum : uint32_t { ST_START = 0, ST_NODE, ST_GUIDE, ST_REC, ST_HASH, ST_CAND, ST_
 constexpr uint32_t kEmptySlot = 0xFFFFFFFFu;
 #ifndef GRAPE_TAB_DRAWS
 #define GRAPE_TAB_DRAWS 2
-#endif
-#ifndef GRAPE_TAB_DRAWS_EXTRA
-#define GRAPE_TAB_DRAWS_EXTRA 0
-#endif
-#ifndef GRAPE_TAB_DRAWS_QUORUM
-#define GRAPE_TAB_DRAWS_QUORUM 16
 #endif
 #ifndef GRAPE_TAB_STATIC_PCT
 #define GRAPE_TAB_STATIC_PCT 50
@@ -495,13 +498,9 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
         // in the same iteration, up to GRAPE_TAB_DRAWS draws; a register-decided
         // return x = t is emitted on the spot when another draw follows it.
 #pragma unroll 1
-        for (int k = 0; k < GRAPE_TAB_DRAWS + GRAPE_TAB_DRAWS_EXTRA; ++k) {
+        for (int k = 0; k < GRAPE_TAB_DRAWS; ++k) {
             __syncwarp();
-            if (k < GRAPE_TAB_DRAWS) {
-                if (!__any_sync(0xffffffffu, draw)) break;
-            } else if (__popc(__ballot_sync(0xffffffffu, draw)) < GRAPE_TAB_DRAWS_QUORUM) {
-                break;   // extra rounds only while most of the warp is still drawing
-            }
+            if (!__any_sync(0xffffffffu, draw)) break;
             const bool sub = SUSS && vdeg > P.dT;   // this step runs on a SUSS sub-sample
             if (SUSS && WEIGHTED && draw && sub && cb < P.dT) {   // first: read the dT candidates
                 draw = false;
@@ -554,7 +553,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                 gsrc = false;
                 draw = false;
                 if (ret) {          // return to t, no read
-                    if (k + 1 < GRAPE_TAB_DRAWS + GRAPE_TAB_DRAWS_EXTRA && s + 1 < L) {   // emit now; t's row is not empty
+                    if (k + 1 < GRAPE_TAB_DRAWS && s + 1 < L) {   // emit now; t's row is not empty
                         w.put(s, tid);
                         ++steps;
                         uint32_t q;
