@@ -47,6 +47,15 @@ constexpr uint32_t kEmptySlot = 0xFFFFFFFFu;
 #ifndef GRAPE_TAB_DRAWS
 #define GRAPE_TAB_DRAWS 2
 #endif
+#ifndef GRAPE_TAB_SYNC_TOP
+#define GRAPE_TAB_SYNC_TOP 0     // explicit reconvergence points (measured: the emit one matters)
+#endif
+#ifndef GRAPE_TAB_SYNC_EMIT
+#define GRAPE_TAB_SYNC_EMIT 1
+#endif
+#ifndef GRAPE_TAB_SYNC_DRAW
+#define GRAPE_TAB_SYNC_DRAW 1
+#endif
 #ifndef GRAPE_TAB_STATIC_PCT
 #define GRAPE_TAB_STATIC_PCT 50
 #endif
@@ -183,7 +192,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
     for (;;) {
         if (!__any_sync(0xffffffffu, st != ST_DONE)) break;
         const bool load = st < ST_DRAW;
-        __syncwarp();
+        if (GRAPE_TAB_SYNC_TOP) __syncwarp();
         uint32_t sec[8];
         uint32_t j;
         {   // the one load of this iteration: a single address computation for every state
@@ -400,7 +409,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
 
         // ---- the walk advances: from a record (emit) or by a register-decided
         // return to t (back, decided by the previous iteration's draw)
-        __syncwarp();
+        if (GRAPE_TAB_SYNC_EMIT) __syncwarp();
         if (emit || back) {
             w.put(s, x);
             ++steps;
@@ -499,7 +508,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
         // return x = t is emitted on the spot when another draw follows it.
 #pragma unroll 1
         for (int k = 0; k < GRAPE_TAB_DRAWS; ++k) {
-            __syncwarp();
+            if (GRAPE_TAB_SYNC_DRAW) __syncwarp();
             if (!__any_sync(0xffffffffu, draw)) break;
             const bool sub = SUSS && vdeg > P.dT;   // this step runs on a SUSS sub-sample
             if (SUSS && WEIGHTED && draw && sub && cb < P.dT) {   // first: read the dT candidates
