@@ -57,18 +57,21 @@ typedef enum {
 /* Flags for grape_graph_from_csr. */
 enum {
     /* Caller asserts arc (u,v) exists iff arc (v,u) exists (undirected graph).
-     * Lets the node2vec membership test "x in N(t)" be evaluated as
-     * "t in N(x)" on the shorter of the two rows — the same predicate
-     * (§8(c) c12).  Checked on the device unless GRAPE_SKIP_VALIDATION. */
+     * Checked on the device unless GRAPE_SKIP_VALIDATION.  Without sampling
+     * tables it lets the v3 walker evaluate "x in N(t)" as "t in N(x)" on the
+     * shorter row — the same predicate (§8(c) c12); with tables the edge-hash
+     * sets answer it either way. */
     GRAPE_SYMMETRIC = 1u << 0,
     /* Skip the O(m) device validation of the CSR (trusted input). */
     GRAPE_SKIP_VALIDATION = 1u << 1,
     /* Do not build the sampling tables (per-arc records with the
-     * reverse arc's interval and the head's node record, per-row guide tables,
-     * per-row edge hash sets: 16 + 8 B per arc unweighted, 32 + 8G + 8 B per
-     * arc weighted, G = 4, 2 or 1 chosen from free device memory; the CSR
-     * arrays are released once the tables exist).  Without them walks run on
-     * the fenced-search walker (v3).  Results are identical either way. */
+     * reverse arc's interval, the head's node record and no-common-neighbour
+     * flags; per-row guide tables; per-row edge-hash sets — between ~16 and
+     * ~550 bytes per arc depending on the layout grape_table_options selects;
+     * the CSR arrays are released once the tables exist).  Without them walks
+     * run on the fenced-search walker (v3), and grape_walks_approx (when a row
+     * exceeds its threshold) and grape_walks_node2vec_cdf are unavailable.
+     * Results are identical either way. */
     GRAPE_NO_TABLES = 1u << 2
 };
 
@@ -127,9 +130,13 @@ typedef struct {
  *   out          receives the handle.
  * The three arrays may be host (pageable or pinned) or device pointers; they
  * are copied, and the call is synchronous: the caller may free them on return.
- * The handle stores off (u64[n+1]), col (u32[m]) and the row-local inclusive
- * prefix sums of the weights — u32[m] when every row sum fits in 32 bits,
- * else u64[m] (same selected index either way).
+ * The handle stores off (u64[n+1]), the node records and, by default, the
+ * sampling tables (built from col and the row-local inclusive
+ * prefix sums of the weights, then those are released); graphs built with
+ * GRAPE_NO_TABLES, or outside the tables' index ranges (2m >= 2^32, a degree
+ * >= 2^28, a row sum >= 2^32), keep col (u32[m]), the prefix sums (u32[m] when
+ * every row sum fits in 32 bits, else u64[m]) and their fence levels instead.
+ * grape_graph_from_csr = grape_graph_from_csr_opts with automatic layout.
  * Errors: GRAPE_EINVAL for null pointers, n >= 2^32-1, or a CSR that fails
  * validation (message names the first check that failed); GRAPE_ENOMEM;
  * GRAPE_ECUDA.  On error *out is set to NULL and nothing is leaked.
