@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 import torch
 
-from graphgen import CSR
+from graphgen import CSR, tiny_graph
 from oracle.oracle import Oracle
 
 pytestmark = pytest.mark.gpu
@@ -181,3 +181,36 @@ def test_single_arc_rows_and_long_walks(grape):
     _check_all(grape, _undirected(n, pairs, lambda r, k: r.integers(1, 5, k)), L=300)
     path = [(i, i + 1) for i in range(9)]
     _check_all(grape, _undirected(10, path), L=300)
+
+
+def test_random_graphs_random_layouts(grape):
+    """60 seeded random cases: graph shape, weights, direction, hub, layout, (p, q),
+    walk length, walk-id base and seed all drawn at random; every walk == oracle."""
+    rng = np.random.default_rng(2026)
+    for case in range(60):
+        n = int(rng.integers(2, 160))
+        dens = float(rng.uniform(0.0, 0.5))
+        directed = bool(rng.integers(0, 2))
+        weighted = bool(rng.integers(0, 2))
+        g = tiny_graph(5000 + case, n, dens, directed=directed, weighted=weighted, self_loops=directed,
+                       max_w=int(rng.choice([3, 100, 60000])))
+        lay = (LAYOUTS_W if weighted else LAYOUTS_U)[int(rng.integers(0, len(LAYOUTS_W if weighted else LAYOUTS_U)))]
+        p = float(rng.choice([0.25, 0.5, 1.0, 2.0, 4.0, 0.3, 7.0]))
+        q = float(rng.choice([0.25, 0.5, 1.0, 2.0, 4.0, 0.3, 7.0]))
+        L = int(rng.integers(1, 70))
+        seed = int(rng.integers(0, 2 ** 63))
+        base = int(rng.integers(0, 2 ** 40))
+        starts = rng.integers(0, n + 2, int(rng.integers(1, 3 * n + 2))).astype(np.uint32)
+        try:
+            d = grape.graph_from_csr(g.off, g.col, g.w, device=0, symmetric=g.symmetric, layout=lay)
+        except grape.GrapeError as e:   # a forced layout can be invalid for an edge-less graph
+            assert g.m == 0, e
+            continue
+        exp, esteps = Oracle(*g.numpy()).walks(starts, L, mode="node2vec", p=p, q=q, seed=seed, base=base)
+        steps = torch.zeros(1, dtype=torch.int64, device="cuda")
+        out = grape.walks_node2vec(d, torch.as_tensor(starts.view(np.int32)).cuda(), L, p, q, seed=seed,
+                                   walk_id_base=base, steps=steps)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), exp), (case, n, dens, directed, weighted, lay, p, q)
+        assert int(steps.item()) == esteps
+        d.free()
