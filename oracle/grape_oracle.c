@@ -566,3 +566,129 @@ int oracle_cdf_steps(const uint64_t* off, const uint32_t* col, const uint64_t* c
         x_out[k] = oracle_cdf_step(off, col, cw, T, seed, wid0 + k, s, t, v);
     return 0;
 }
+
+/* ---------------------------------------------------------------------------
+ * Outlier-folded rejection ("outlier-folded
+ * proposals").  Same law as the default rule — Eq.1
+ * — with fewer attempts when the return class dominates (p < min(1, q)):
+ *   E = max(T_1, T_q)            envelope of the non-return classes
+ *   X = T_p - E if T_p > E else 0  the return's excess over the envelope
+ *   w_t = w_vt (0 if no arc v -> t),  N = w_t * X,  M = W_v * E + N  (< 2^64:
+ *         M <= W_v * T_p since w_t <= W_v)
+ *   A_c = ceil(min(T_c, E) * 2^32 / E)  acceptance thresholds scaled to E
+ * attempt a: o = DRAW(seed, wid, s, a);
+ *   if N > 0 and o3 * M < N * 2^32 (exact 96-bit compare): x = t, accepted
+ *     (the return's excess mass, probability N / M up to 2^-32);
+ *   else x = PROPOSE(v, o1:o0) and accept iff o2 < A_class(x).
+ * P(x) is proportional to w_vx * min(T_c, E) + [x == t] * N = w_vx * T_c(x),
+ * i.e. Eq.1.  When T_p <= E (then E = 2^32 and N = 0, A = T) this is the
+ * default rule draw for draw; the first step stays first-order (c2).
+ * ------------------------------------------------------------------------- */
+static void oracle_fold_consts(const uint64_t T[3], uint64_t* E, uint64_t* X, uint64_t A[3])
+{
+    int c;
+    *E = T[1] > T[2] ? T[1] : T[2];
+    *X = T[0] > *E ? T[0] - *E : 0;
+    for (c = 0; c < 3; c++) {
+        uint64_t tc = T[c] < *E ? T[c] : *E;
+        oracle_u128 num = ((oracle_u128)tc << 32) + *E - 1;
+        A[c] = (uint64_t)(num / *E);
+    }
+}
+
+uint32_t oracle_folded_step(const uint64_t* off, const uint32_t* col, const uint64_t* cw, const uint64_t T[3],
+                            uint64_t seed, uint64_t wid, uint32_t s, uint32_t t, uint32_t v, uint32_t* attempts)
+{
+    uint64_t E, X, A[3];
+    uint64_t lo = off[v], d = off[v + 1] - lo, W, wt = 0, N, M, i;
+    uint32_t a = 0;
+    oracle_fold_consts(T, &E, &X, A);
+    W = cw != NULL ? cw[lo + d - 1] : d;
+    for (i = 0; i < d; i++)   /* w_vt: the weight of the arc v -> t, if any */
+        if (col[lo + i] == t)
+            wt = cw != NULL ? cw[lo + i] - (i > 0 ? cw[lo + i - 1] : 0) : 1;
+    N = wt * X;
+    M = W * E + N;
+    for (;;) {
+        uint32_t o[4];
+        uint32_t x;
+        uint64_t thr;
+        oracle_draw(seed, wid, s, a, o);
+        a++;
+        if (N > 0 && (oracle_u128)o[3] * M < ((oracle_u128)N << 32)) {
+            *attempts = a;
+            return t;
+        }
+        x = oracle_propose(off, col, cw, v, x64_of(o));
+        if (x == t)
+            thr = A[0];
+        else if (oracle_in_row(off, col, t, x))
+            thr = A[1];
+        else
+            thr = A[2];
+        if ((uint64_t)o[2] < thr) {
+            *attempts = a;
+            return x;
+        }
+    }
+}
+
+int oracle_walks_folded(uint32_t n, const uint64_t* off, const uint32_t* col, const uint64_t* cw,
+                        const uint32_t* starts, uint64_t num_walks, uint64_t base, uint32_t L,
+                        double p, double q, uint64_t seed, uint32_t* out, uint64_t* steps_out,
+                        uint64_t* attempts_out)
+{
+    uint64_t T[3];
+    uint64_t i, steps = 0, attempts = 0;
+    if (oracle_thresholds(p, q, T) != 0)
+        return 1;
+    for (i = 0; i < num_walks; i++) {
+        uint32_t* row = out + i * (uint64_t)L;
+        uint64_t wid = base + i;
+        uint32_t start = starts[i];
+        uint32_t t, v, s, j;
+        for (j = 0; j < L; j++)
+            row[j] = ORACLE_PAD;
+        if (start >= n || L == 0)
+            continue;
+        row[0] = start;
+        t = ORACLE_NONE;
+        v = start;
+        for (s = 1; s < L; s++) {
+            uint32_t x;
+            if (off[v + 1] == off[v])
+                break;
+            if (t == ORACLE_NONE) {
+                uint32_t o[4];
+                oracle_draw(seed, wid, s, 0, o);
+                x = oracle_propose(off, col, cw, v, x64_of(o));
+            } else {
+                uint32_t a = 0;
+                x = oracle_folded_step(off, col, cw, T, seed, wid, s, t, v, &a);
+                attempts += a;
+            }
+            row[s] = x;
+            steps++;
+            t = v;
+            v = x;
+        }
+    }
+    if (steps_out != NULL)
+        *steps_out += steps;
+    if (attempts_out != NULL)
+        *attempts_out += attempts;
+    return 0;
+}
+
+int oracle_folded_steps(const uint64_t* off, const uint32_t* col, const uint64_t* cw, double p, double q,
+                        uint64_t seed, uint32_t t, uint32_t v, uint32_t s, uint64_t wid0, uint64_t count,
+                        uint32_t* x_out, uint32_t* att_out)
+{
+    uint64_t T[3];
+    uint64_t k;
+    if (oracle_thresholds(p, q, T) != 0)
+        return 1;
+    for (k = 0; k < count; k++)
+        x_out[k] = oracle_folded_step(off, col, cw, T, seed, wid0 + k, s, t, v, &att_out[k]);
+    return 0;
+}

@@ -83,6 +83,14 @@ def _load():
                 _u64p, _u32p, _u64p, ctypes.c_double, ctypes.c_double, ctypes.c_uint64,
                 ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, _u32p]
             lib.oracle_cdf_steps.restype = ctypes.c_int
+            lib.oracle_walks_folded.argtypes = [
+                ctypes.c_uint32, _u64p, _u32p, _u64p, _u32p, ctypes.c_uint64, ctypes.c_uint64,
+                ctypes.c_uint32, ctypes.c_double, ctypes.c_double, ctypes.c_uint64, _u32p, _u64p, _u64p]
+            lib.oracle_walks_folded.restype = ctypes.c_int
+            lib.oracle_folded_steps.argtypes = [
+                _u64p, _u32p, _u64p, ctypes.c_double, ctypes.c_double, ctypes.c_uint64,
+                ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, _u32p, _u32p]
+            lib.oracle_folded_steps.restype = ctypes.c_int
             _lib = lib
     return _lib
 
@@ -206,6 +214,32 @@ class Oracle:
         if rc != 0:
             raise ValueError(f"oracle rejected p={p} q={q}")
         return out, int(steps.value)
+
+    def walks_folded(self, starts, L: int, *, p: float = 1.0, q: float = 1.0, seed: int = 42, base: int = 0,
+                     with_attempts: bool = False):
+        """Node2vec walks with the outlier-folded rejection rule (§8(f) f2)."""
+        starts = np.ascontiguousarray(starts, dtype=np.uint32)
+        nw = len(starts)
+        out = np.empty((nw, L), dtype=np.uint32)
+        steps = ctypes.c_uint64(0)
+        att = ctypes.c_uint64(0)
+        rc = _load().oracle_walks_folded(self.n, _p64(self.off), _p32(self.col), _p64(self.cw), _p32(starts), nw,
+                                         base, L, float(p), float(q), seed, out.ctypes.data_as(_u32p),
+                                         ctypes.byref(steps), ctypes.byref(att))
+        if rc != 0:
+            raise ValueError(f"oracle rejected p={p} q={q}")
+        if with_attempts:
+            return out, int(steps.value), int(att.value)
+        return out, int(steps.value)
+
+    def folded_steps(self, t: int, v: int, s: int, wid0: int, count: int, p: float, q: float, seed: int = 42):
+        x = np.empty(count, dtype=np.uint32)
+        a = np.empty(count, dtype=np.uint32)
+        rc = _load().oracle_folded_steps(_p64(self.off), _p32(self.col), _p64(self.cw), float(p), float(q), seed,
+                                         t, v, s, wid0, count, _p32(x), _p32(a))
+        if rc != 0:
+            raise ValueError(f"oracle rejected p={p} q={q}")
+        return x, a
 
     def cdf_steps(self, t: int, v: int, s: int, wid0: int, count: int, p: float, q: float, seed: int = 42):
         x = np.empty(count, dtype=np.uint32)

@@ -156,6 +156,54 @@ class PyGraph:
             t, v = v, x
         return row, steps
 
+    # ---- outlier-folded rejection (§8(f) f2) ----
+    def folded_step(self, T, seed, wid, s, t, v):
+        E = max(T[1], T[2])
+        X = T[0] - E if T[0] > E else 0
+        A = [-(-(min(tc, E) << 32) // E) for tc in T]          # ceil(min(T_c, E) 2^32 / E)
+        row = self.rows[v]
+        if self.cw is None:
+            W, wt = len(row), (1 if t in row else 0)
+        else:
+            c = self.cw[v]
+            W = c[-1]
+            wt = 0
+            for i, x in enumerate(row):
+                if x == t:
+                    wt = c[i] - (c[i - 1] if i else 0)
+        N = wt * X
+        M = W * E + N
+        a = 0
+        while True:
+            o = draw(seed, wid, s, a)
+            a += 1
+            if N > 0 and o[3] * M < (N << 32):
+                return t, a
+            x = self.propose(v, (o[1] << 32) | o[0])
+            thr = A[0] if x == t else (A[1] if self.member(t, x) else A[2])
+            if o[2] < thr:
+                return x, a
+
+    def walk_folded(self, start, wid, L, p=1.0, q=1.0, seed=42):
+        row = [PAD] * L
+        if start >= self.n or L == 0:
+            return row, 0
+        T = thresholds(p, q)
+        row[0] = start
+        t, v, steps = NONE, start, 0
+        for s in range(1, L):
+            if not self.rows[v]:
+                break
+            if t == NONE:
+                o = draw(seed, wid, s, 0)
+                x = self.propose(v, (o[1] << 32) | o[0])
+            else:
+                x, _ = self.folded_step(T, seed, wid, s, t, v)
+            row[s] = x
+            steps += 1
+            t, v = v, x
+        return row, steps
+
     # ---- the paper's CDF sampler (§8(f) f2; P:507-511 steps 1-4) ----
     def cdf_step(self, T, seed, wid, s, t, v):
         row = self.rows[v]
