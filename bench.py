@@ -251,6 +251,8 @@ def run_ours(args):
             grape.walks_approx(dg, st_buf, L, dT, node2vec=node2vec, p=wk["p"], q=wk["q"], **kw)
         elif args.sampler == "cdf":
             grape.walks_node2vec_cdf(dg, st_buf, L, wk["p"], wk["q"], **kw)
+        elif args.sampler == "folded" and node2vec:
+            grape.walks_node2vec_folded(dg, st_buf, L, wk["p"], wk["q"], **kw)
         elif node2vec:
             grape.walks_node2vec(dg, st_buf, L, wk["p"], wk["q"], **kw)
         else:
@@ -321,7 +323,7 @@ def run_ours(args):
     roof = None
     if rank == 0 and args.sampler != "cdf":   # (no counting build of the CDF sampler)
         _, ev = grape.walks_stats(dg, starts, L, node2vec=node2vec, p=wk["p"], q=wk["q"], seed=wk["seed"],
-                                  degree_threshold=dT,
+                                  degree_threshold=dT, sampler=args.sampler if node2vec else "rejection",
                                   walk_id_base=base, out=out)
         torch.cuda.synchronize(dev)
         weighted = info["cw_bytes"] > 0
@@ -385,6 +387,8 @@ def run_ours(args):
             metric = metric[:-1] + f", approximated: SUSS d_T={dT})"
         if args.sampler == "cdf":
             metric = metric[:-1] + ", paper CDF sampler)"
+        if args.sampler == "folded" and node2vec:
+            metric = metric[:-1] + ", outlier-folded rejection)"
         line = {"metric": metric, "value": value, "unit": "steps/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32/u64 integer",
@@ -417,7 +421,7 @@ def main():
                     help="ncu dram bytes per launch of the walk kernel (from profiles/)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-tables", action="store_true", help="GRAPE_NO_TABLES: the v3 fenced-search walker")
-    ap.add_argument("--sampler", default="rejection", choices=["rejection", "cdf"],
+    ap.add_argument("--sampler", default="rejection", choices=["rejection", "cdf", "folded"],
                     help="node2vec sampler: the default rejection rules, or the paper's CDF sampler "
                          "(grape_walks_node2vec_cdf, P:507-511)")
     ap.add_argument("--approx", type=int, default=0,

@@ -247,6 +247,25 @@ grape_status grape_walks_node2vec_cdf(const grape_graph* g, const uint32_t* star
                                       cudaStream_t stream);
 
 /*
+ * grape_walks_node2vec_folded — node2vec walks with outlier-folded rejection
+ * ("outlier-folded proposals"): the same
+ * law as grape_walks_node2vec (Eq.1), fewer attempts when the
+ * return class dominates (p < min(1, q)).  At v coming from t, with
+ * E = max(T_1, T_q), X = T_p - E (> 0), w_t = w_vt (0 if no arc v -> t),
+ * N = w_t X and M = W_v E + N: attempt a draws o = DRAW(seed, wid, s, a); if
+ * o3 * M < N * 2^32 the walk returns to t; else x = the proposal of o1:o0 and
+ * it is accepted iff o2 < A_class(x), A_c = ceil(min(T_c, E) * 2^32 / E).
+ * When p >= min(1, q) (T_p <= E) every walk equals grape_walks_node2vec's.
+ * Arguments, ownership and errors as grape_walks_node2vec; EINVAL on graphs
+ * without sampling tables, and on weighted graphs with asymmetric weights
+ * stored in 16-B records (the return arc's weight is not kept there).
+ */
+grape_status grape_walks_node2vec_folded(const grape_graph* g, const uint32_t* starts, uint64_t num_walks,
+                                         uint64_t walk_id_base, uint32_t walk_length, double p, double q,
+                                         uint64_t seed, uint32_t* out, uint64_t* steps_out,
+                                         cudaStream_t stream);
+
+/*
  * grape_walks_stats — diagnostics: run the same walks as grape_walks_first_order
  * (node2vec = 0) or grape_walks_node2vec (node2vec = 1) with event counters
  * compiled into the kernel, and return the counts.  `out` receives exactly the
@@ -281,11 +300,15 @@ grape_status grape_walks_stats(const grape_graph* g, const uint32_t* starts, uin
                                double p, double q, uint64_t seed, uint32_t* out,
                                grape_walk_stats* stats, cudaStream_t stream);
 
-/* grape_walks_stats for grape_walks_approx (degree_threshold as there). */
-grape_status grape_walks_stats_approx(const grape_graph* g, const uint32_t* starts, uint64_t num_walks,
-                                      uint64_t walk_id_base, uint32_t walk_length, int node2vec,
-                                      double p, double q, uint32_t degree_threshold, uint64_t seed,
-                                      uint32_t* out, grape_walk_stats* stats, cudaStream_t stream);
+/* grape_walks_stats for the other modes: degree_threshold as grape_walks_approx
+ * (0: exact), sampler 0 = the default rejection rules, 2 = outlier-folded
+ * (grape_walks_node2vec_folded).  EINVAL for the CDF sampler (no counting build)
+ * and for combinations the walk calls reject. */
+grape_status grape_walks_stats_ex(const grape_graph* g, const uint32_t* starts, uint64_t num_walks,
+                                  uint64_t walk_id_base, uint32_t walk_length, int node2vec,
+                                  double p, double q, uint32_t degree_threshold, int sampler,
+                                  uint64_t seed, uint32_t* out, grape_walk_stats* stats,
+                                  cudaStream_t stream);
 
 /* Static string for a status code. */
 const char* grape_status_string(grape_status s);

@@ -167,6 +167,14 @@ def walks_node2vec_cdf(g: Graph, starts, L: int, p: float, q: float, *, seed: in
                   out, steps, stream)
 
 
+def walks_node2vec_folded(g: Graph, starts, L: int, p: float, q: float, *, seed: int = 42,
+                          walk_id_base: int = 0, out=None, steps=None, stream=None) -> torch.Tensor:
+    """grape_walks_node2vec_folded: node2vec with outlier-folded rejection (same law, fewer
+    attempts when p < min(1, q))."""
+    return _walks("grape_walks_node2vec_folded", g, starts, L, (float(p), float(q)), seed, walk_id_base,
+                  out, steps, stream)
+
+
 def walks_approx(g: Graph, starts, L: int, degree_threshold: int, *, node2vec: bool = True, p: float = 1.0,
                  q: float = 1.0, seed: int = 42, walk_id_base: int = 0, out=None, steps=None,
                  stream=None) -> torch.Tensor:
@@ -200,7 +208,8 @@ def _walks_approx(g, starts, L, n2v, p, q, dT, seed, walk_id_base, out, steps, s
 
 
 def walks_stats(g: Graph, starts, L: int, *, node2vec: bool, p: float = 1.0, q: float = 1.0,
-                seed: int = 42, walk_id_base: int = 0, out=None, degree_threshold: int = 0):
+                seed: int = 42, walk_id_base: int = 0, out=None, degree_threshold: int = 0,
+                sampler: str = "rejection"):
     """grape_walks_stats: (walk matrix, dict of event counters) — diagnostics build of the
     same kernel (device buffers only; synchronous)."""
     st = _as_tensor(starts, torch.int32)
@@ -211,11 +220,12 @@ def walks_stats(g: Graph, starts, L: int, *, node2vec: bool, p: float = 1.0, q: 
         if out is None:
             out = torch.empty((W, L), dtype=torch.int32, device=st.device)
         stats = _capi.WalkStats()
-        rc = _lib.grape_walks_stats_approx(g.handle, st.data_ptr(), W, walk_id_base, L, int(node2vec),
-                                           float(p), float(q), int(degree_threshold), seed, out.data_ptr(),
-                                           ctypes.byref(stats),
-                                           ctypes.c_void_p(torch.cuda.current_stream(g.device).cuda_stream))
-    _capi.check(_lib, rc, "grape_walks_stats_approx")
+        smp = {"rejection": 0, "cdf": 1, "folded": 2}[sampler]
+        rc = _lib.grape_walks_stats_ex(g.handle, st.data_ptr(), W, walk_id_base, L, int(node2vec),
+                                       float(p), float(q), int(degree_threshold), smp, seed, out.data_ptr(),
+                                       ctypes.byref(stats),
+                                       ctypes.c_void_p(torch.cuda.current_stream(g.device).cuda_stream))
+    _capi.check(_lib, rc, "grape_walks_stats_ex")
     return out, {f: int(getattr(stats, f)) for f in _capi.STATS_FIELDS}
 
 
@@ -226,3 +236,4 @@ grape_walks_node2vec = walks_node2vec
 grape_walks_stats = walks_stats
 grape_walks_approx = walks_approx
 grape_walks_node2vec_cdf = walks_node2vec_cdf
+grape_walks_node2vec_folded = walks_node2vec_folded

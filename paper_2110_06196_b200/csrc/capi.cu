@@ -195,9 +195,14 @@ grape_status walks_common(const grape_graph* g, const uint32_t* starts, uint64_t
     Thresholds T{1ull << 32, 1ull << 32, 1ull << 32};
     if (n2v && !node2vec_thresholds(p, q, &T)) return GRAPE_EINVAL;
     if (dT >= g->max_degree) dT = 0;   // no row exceeds the threshold: the exact walks
-    if (sampler == 1 && !g->tables) {
-        set_error("the CDF sampler needs the sampling tables (graph built with GRAPE_NO_TABLES "
-                  "or outside their index ranges)");
+    if ((sampler == 1 || sampler == 2) && !g->tables) {
+        set_error("the %s sampler needs the sampling tables (graph built with GRAPE_NO_TABLES "
+                  "or outside their index ranges)", sampler == 1 ? "CDF" : "outlier-folded");
+        return GRAPE_EINVAL;
+    }
+    if (sampler == 2 && g->cw_bytes != 0 && g->compact && !g->wsym) {
+        set_error("the outlier-folded sampler needs each return arc's weight: rebuild this graph "
+                  "(asymmetric weights) with grape_table_options.record_bytes = 32");
         return GRAPE_EINVAL;
     }
     if (dT != 0 && !g->tables) {
@@ -372,19 +377,27 @@ grape_status grape_walks_node2vec_cdf(const grape_graph* g, const uint32_t* star
                         stream, 0, 1);
 }
 
+grape_status grape_walks_node2vec_folded(const grape_graph* g, const uint32_t* starts, uint64_t num_walks,
+                                         uint64_t walk_id_base, uint32_t walk_length, double p, double q,
+                                         uint64_t seed, uint32_t* out, uint64_t* steps_out, cudaStream_t stream)
+{
+    return walks_common(g, starts, num_walks, walk_id_base, walk_length, true, p, q, seed, out, steps_out,
+                        stream, 0, 2);
+}
+
 grape_status grape_walks_stats(const grape_graph* g, const uint32_t* starts, uint64_t num_walks,
                                uint64_t walk_id_base, uint32_t walk_length, int node2vec, double p,
                                double q, uint64_t seed, uint32_t* out, grape_walk_stats* stats,
                                cudaStream_t stream)
 {
-    return grape_walks_stats_approx(g, starts, num_walks, walk_id_base, walk_length, node2vec, p, q, 0, seed,
-                                    out, stats, stream);
+    return grape_walks_stats_ex(g, starts, num_walks, walk_id_base, walk_length, node2vec, p, q, 0, 0, seed,
+                                out, stats, stream);
 }
 
-grape_status grape_walks_stats_approx(const grape_graph* g, const uint32_t* starts, uint64_t num_walks,
-                                      uint64_t walk_id_base, uint32_t walk_length, int node2vec, double p,
-                                      double q, uint32_t degree_threshold, uint64_t seed, uint32_t* out,
-                                      grape_walk_stats* stats, cudaStream_t stream)
+grape_status grape_walks_stats_ex(const grape_graph* g, const uint32_t* starts, uint64_t num_walks,
+                                  uint64_t walk_id_base, uint32_t walk_length, int node2vec, double p,
+                                  double q, uint32_t degree_threshold, int sampler, uint64_t seed, uint32_t* out,
+                                  grape_walk_stats* stats, cudaStream_t stream)
 {
     g_err[0] = 0;
     if (g == nullptr || stats == nullptr || (num_walks > 0 && (starts == nullptr || out == nullptr))) {
@@ -404,6 +417,12 @@ grape_status grape_walks_stats_approx(const grape_graph* g, const uint32_t* star
     uint32_t dT = degree_threshold >= g->max_degree ? 0 : degree_threshold;
     if (dT != 0 && !g->tables) {
         set_error("approximated walks need the sampling tables");
+        return GRAPE_EINVAL;
+    }
+    if (sampler != 0 && (sampler != 2 || !g->tables || dT != 0 || !node2vec ||
+                         (g->cw_bytes != 0 && g->compact && !g->wsym))) {
+        set_error("grape_walks_stats_ex: sampler %d is not available with these arguments / this graph "
+                  "(counting builds exist for the default and the outlier-folded samplers)", sampler);
         return GRAPE_EINVAL;
     }
     int cur = -1;
@@ -430,6 +449,7 @@ grape_status grape_walks_stats_approx(const grape_graph* g, const uint32_t* star
     a.out = out;
     a.stats = d;
     a.dT = dT;
+    a.sampler = (uint32_t)sampler;
     e = cudaMemsetAsync(d, 0, sizeof(unsigned long long) * kStatsWords, stream);
     if (e == cudaSuccess) e = launch_walks(g, a, node2vec != 0, T, stream);
     unsigned long long h[kStatsWords] = {0};

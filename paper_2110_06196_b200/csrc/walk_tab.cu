@@ -76,6 +76,7 @@ struct TabParams {
     uint32_t dT;              // approximated walks (SUSS): degree threshold
     uint32_t* scratch;        // SUSS, weighted: per lane 2 dT words, [2 b + {0: running weight, 1: x}][lane]
     uint32_t lanes;           // resident lanes of the launch (scratch stride)
+    uint32_t fold_e, fold_x;  // outlier-folded rule: E = max(T_1, T_q), X = T_p - E (thresholds hold A_c)
     uint64_t nstatic;         // walks [0, nstatic) go round-robin to the lanes; the rest via *next
     unsigned long long* next; // shared walk counter (starts at nstatic)
     uint32_t n;
@@ -137,9 +138,11 @@ enum : int { C_LOADS = 0, C_NODE, C_XNODE, C_CWPROBE, C_COLPROBE, C_REC, C_ATTEM
              C_GUIDE, C_HASH, C_ALU, C_ITER, C_ITER_DRAW, C_ITER_BACK };
 
 // WEIGHTED: 32-B records + guide; else 16-B records indexed by the draw.
-template <bool WEIGHTED, bool FAT, bool COMPACT, bool NODE2VEC, bool NEED_MEMBER, bool STATS, bool SUSS>
+template <bool WEIGHTED, bool FAT, bool COMPACT, bool NODE2VEC, bool NEED_MEMBER, bool STATS, int MODE>
 __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(const __grid_constant__ TabParams P)
 {
+    constexpr bool SUSS = MODE == 1;   // approximated walks (grape_walks_approx)
+    constexpr bool FOLD = MODE == 2;   // outlier-folded rejection (grape_walks_node2vec_folded)
     uint32_t cnt[kStatsWords];
     if (STATS) {
 #pragma unroll
@@ -521,7 +524,16 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
             }
             if (draw) {
                 if (STATS) ++cnt[C_ATTEMPT];
-                const Draw dr = philox_draw_rk(P.rk, P.base + i, s, a);
+                Draw dr;
+                uint32_t o3 = 0;
+                if constexpr (FOLD) {   // all four words: o3 decides the return's excess mass
+                    const uint4 o = philox_block_rk(P.rk, P.base + i, s, a);
+                    dr.x64 = (uint64_t)o.y << 32 | o.x;
+                    dr.u = o.z;
+                    o3 = o.w;
+                } else {
+                    dr = philox_draw_rk(P.rk, P.base + i, s, a);
+                }
                 u = dr.u;
                 bool known = tlo <= thi;
                 uint32_t bs = 0;                 // SUSS: the proposed candidate
@@ -545,7 +557,18 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                     r = bounded32(dr.x64, vW);   // index (unweighted: vW = deg) or weight point
                 }
                 bool need_x = true, ret = false;
-                if (NODE2VEC && tid != kNone) {
+                bool outlier = false;
+                if (FOLD && tid != kNone) {   // o3 * M < N * 2^32, N = w_vt X, M = W_v E + N
+                    const uint64_t N = known ? (uint64_t)(thi - tlo) * P.fold_x : 0;   // w_vt = width of t's interval
+                    const uint64_t M = (uint64_t)vW * P.fold_e + N;
+                    const uint64_t p1 = (uint64_t)o3 * (M >> 32) + (((uint64_t)o3 * (uint32_t)M) >> 32);
+                    outlier = p1 < N;
+                }
+                if (outlier) {
+                    need_x = false;
+                    ret = true;
+                    if (STATS) ++cnt[C_ALU];
+                } else if (NODE2VEC && tid != kNone) {
                     const bool cp = u <= P.tp_m1, cq = u <= P.tq_m1, c1 = nt ? cq : u <= P.t1_m1;
                     if (cp == c1 && c1 == cq) {
                         need_x = cp;
@@ -636,7 +659,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
     }
 }
 
-template <bool WEIGHTED, bool FAT, bool COMPACT, bool NODE2VEC, bool NEED_MEMBER, bool STATS, bool SUSS>
+template <bool WEIGHTED, bool FAT, bool COMPACT, bool NODE2VEC, bool NEED_MEMBER, bool STATS, int MODE>
 cudaError_t launch_k(const grape_graph* g, const WalkArgs& a, const Thresholds& T, cudaStream_t stream)
 {
     TabParams P{};
@@ -662,13 +685,25 @@ cudaError_t launch_k(const grape_graph* g, const WalkArgs& a, const Thresholds& 
     P.tp_m1 = (uint32_t)(T.Tp - 1);
     P.t1_m1 = (uint32_t)(T.T1 - 1);
     P.tq_m1 = (uint32_t)(T.Tq - 1);
+    if (MODE == 2) {   // A_c = ceil(min(T_c, E) 2^32 / E); accept iff u < A_c
+        const uint64_t E = T.T1 > T.Tq ? T.T1 : T.Tq;
+        auto A = [&](uint64_t tc) {
+            const uint64_t m = tc < E ? tc : E;
+            return (uint64_t)((((unsigned __int128)m << 32) + E - 1) / E);
+        };
+        P.tp_m1 = (uint32_t)(A(T.Tp) - 1);
+        P.t1_m1 = (uint32_t)(A(T.T1) - 1);
+        P.tq_m1 = (uint32_t)(A(T.Tq) - 1);
+        P.fold_e = (uint32_t)E;   // < 2^32: T_p > E
+        P.fold_x = (uint32_t)(T.Tp - E);
+    }
     P.dT = a.dT;
     static int resident = 0;
     if (resident == 0) {
         int dev = 0, sms = 0, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, walk_tab_kernel<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, STATS, SUSS>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, walk_tab_kernel<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, STATS, MODE>,
                                                       kBlock, 0);
         resident = sms * (per_sm > 0 ? per_sm : 1);
     }
@@ -687,10 +722,11 @@ cudaError_t launch_k(const grape_graph* g, const WalkArgs& a, const Thresholds& 
         if (e != cudaSuccess) return e;
         e = cudaMemsetAsync(P.next, 0, 8, stream);
     }
+    constexpr bool SUSS = MODE == 1;
     if (e == cudaSuccess && SUSS && WEIGHTED)   // per-lane candidate scratch, stream-ordered
         e = cudaMallocAsync((void**)&P.scratch, (uint64_t)2 * a.dT * P.lanes * 4, stream);
     if (e == cudaSuccess) {
-        walk_tab_kernel<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, STATS, SUSS><<<(unsigned)blocks, kBlock, 0, stream>>>(P);
+        walk_tab_kernel<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, STATS, MODE><<<(unsigned)blocks, kBlock, 0, stream>>>(P);
         e = cudaGetLastError();
     }
     if (SUSS && WEIGHTED && P.scratch) cudaFreeAsync(P.scratch, stream);
@@ -703,11 +739,16 @@ cudaError_t launch_s(const grape_graph* g, const WalkArgs& a, const Thresholds& 
 {
     // approximated walks only when some row exceeds the threshold (else they are the exact walks)
     if (a.dT != 0 && a.dT < g->max_degree) {
-        if (a.stats != nullptr) return launch_k<WEIGHTED, FAT, COMPACT, NODE2VEC, true, true, true>(g, a, T, stream);
-        return launch_k<WEIGHTED, FAT, COMPACT, NODE2VEC, true, false, true>(g, a, T, stream);
+        if (a.stats != nullptr) return launch_k<WEIGHTED, FAT, COMPACT, NODE2VEC, true, true, 1>(g, a, T, stream);
+        return launch_k<WEIGHTED, FAT, COMPACT, NODE2VEC, true, false, 1>(g, a, T, stream);
     }
-    if (a.stats != nullptr) return launch_k<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, true, false>(g, a, T, stream);
-    return launch_k<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, false, false>(g, a, T, stream);
+    // outlier folding only when the return class dominates (else it is the default rule)
+    if (NODE2VEC && a.sampler == 2 && T.Tp > (T.T1 > T.Tq ? T.T1 : T.Tq)) {
+        if (a.stats != nullptr) return launch_k<WEIGHTED, FAT, COMPACT, NODE2VEC, true, true, 2>(g, a, T, stream);
+        return launch_k<WEIGHTED, FAT, COMPACT, NODE2VEC, true, false, 2>(g, a, T, stream);
+    }
+    if (a.stats != nullptr) return launch_k<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, true, 0>(g, a, T, stream);
+    return launch_k<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, false, 0>(g, a, T, stream);
 }
 
 template <bool WEIGHTED, bool FAT, bool COMPACT>
