@@ -300,7 +300,9 @@ def run_ours(args):
         e2e_steps = max(1, min(args.steps, 3))
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
+            t1 = time.perf_counter()
             call(h_starts, h_out, h_steps)
+            print(f"e2e call {1e3 * (time.perf_counter() - t1):.1f} ms", file=sys.stderr, flush=True)
         torch.cuda.synchronize(dev)
         e2e_s = time.perf_counter() - t0
         e2e_s = _allreduce(e2e_s, dist.ReduceOp.MAX, world)
