@@ -1,6 +1,6 @@
-// walk_common.cuh — device building blocks shared by the walk kernels (walk.cu,
-// walk_sm.cu): kernel parameters, cache-policy loads, sector scans, node
-// records and the staged row writer.  Internal to libgrape_walk.
+// walk_common.cuh — device building blocks shared by the walk kernels
+// (walk_sm.cu, walk_tab.cu, walk_cdf.cu): the v3 kernel parameters, the staged
+// row writer, the step counter.  Internal to libgrape_walk.
 #pragma once
 #include <cstdint>
 #include <type_traits>
@@ -50,149 +50,6 @@ struct Params {
     uint32_t tp_m1, t1_m1, lo_m1, hi_m1;
     bool member_accepts;   // for u in [T_lo, T_hi): accepted iff (x in N(t)) == (T_1 > T_q)
 };
-
-__device__ __forceinline__ uint4 ldg_v4(const void* p)
-{
-    return __ldg(reinterpret_cast<const uint4*>(p));
-}
-
-// ---- L2 residency: the hot set (node records + fence levels,
-// tens of MB) is loaded with an evict_last policy so that the random stream of
-// cold leaf sectors (col / cw rows, hundreds of MB) cannot flush it; leaf loads
-// take GRAPE_LEAF_HINT (0: default, 1: evict_first, 2: evict_first and no L1
-// allocation).  Policies live in uniform registers (memory descriptors).
-#ifndef GRAPE_HOT_HINT
-#define GRAPE_HOT_HINT 1
-#endif
-#ifndef GRAPE_LEAF_HINT
-#define GRAPE_LEAF_HINT 1
-#endif
-enum Temp { kHot = 0, kLeaf = 1 };
-
-__device__ __forceinline__ uint64_t policy_evict_last()
-{
-    uint64_t pol;
-    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-__device__ __forceinline__ uint64_t policy_evict_first()
-{
-    uint64_t pol;
-    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-
-template <int TEMP>
-__device__ __forceinline__ uint32_t ld_u32(const uint32_t* p)
-{
-    uint32_t r;
-    if (TEMP == kHot && GRAPE_HOT_HINT == 1) {
-        asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(policy_evict_last()));
-    } else if (TEMP == kLeaf && GRAPE_LEAF_HINT == 1) {
-        asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(policy_evict_first()));
-    } else if (TEMP == kLeaf && GRAPE_LEAF_HINT == 2) {
-        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(policy_evict_first()));
-    } else {
-        r = __ldg(p);
-    }
-    return r;
-}
-
-template <int TEMP>
-__device__ __forceinline__ uint64_t ld_u64(const uint64_t* p)
-{
-    uint64_t r;
-    if (TEMP == kHot && GRAPE_HOT_HINT == 1) {
-        asm("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(policy_evict_last()));
-    } else if (TEMP == kLeaf && GRAPE_LEAF_HINT >= 1) {
-        asm("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(policy_evict_first()));
-    } else {
-        r = __ldg(p);
-    }
-    return r;
-}
-
-template <typename T, int TEMP>
-__device__ __forceinline__ T ld_elem(const T* p)
-{
-    if constexpr (sizeof(T) == 4) return ld_u32<TEMP>(p);
-    else return ld_u64<TEMP>(p);
-}
-
-// One aligned 32-byte sector in one 256-bit load (LDG.E.ENL2.256 on sm_100a).
-template <int TEMP>
-__device__ __forceinline__ void ld_sector(const void* p, uint32_t (&v)[8])
-{
-#define GRAPE_LD8(QUAL, POL)                                                                              \
-    asm("ld.global.nc" QUAL ".v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"                               \
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]) \
-        : "l"(p), "l"(POL))
-    if (TEMP == kHot && GRAPE_HOT_HINT == 1) {
-        GRAPE_LD8(".L2::cache_hint", policy_evict_last());
-    } else if (TEMP == kLeaf && GRAPE_LEAF_HINT == 1) {
-        GRAPE_LD8(".L2::cache_hint", policy_evict_first());
-    } else if (TEMP == kLeaf && GRAPE_LEAF_HINT == 2) {
-        GRAPE_LD8(".L1::no_allocate.L2::cache_hint", policy_evict_first());
-    } else {
-        asm("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
-            : "l"(p));
-    }
-#undef GRAPE_LD8
-}
-
-// Number of entries j of the aligned 32-byte block `blk` of `arr` with index in
-// [a, b) and value < key; eq: whether one of them equals key.
-template <typename T, typename IDX, int TEMP>
-__device__ __forceinline__ uint32_t block_count_lt(const T* arr, IDX blk, IDX a, IDX b, T key, bool& eq)
-{
-    constexpr int B = 32 / sizeof(T);
-    const T* p = arr + (uint64_t)blk * B;
-    uint32_t w[8];
-    ld_sector<TEMP>(p, w);
-    T v[B];
-    if constexpr (sizeof(T) == 4) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = w[j];
-    } else {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) v[j] = ((uint64_t)w[2 * j + 1] << 32) | w[2 * j];
-    }
-    const int ja = (int)(a - blk * B), jb = (int)(b - blk * B);   // 0 <= ja < jb <= B
-    uint32_t cnt = 0;
-    bool e = false;
-#pragma unroll
-    for (int j = 0; j < B; ++j) {
-        const bool in = j >= ja && j < jb;
-        cnt += (in && v[j] < key) ? 1u : 0u;
-        e |= in && v[j] == key;
-    }
-    eq = e;
-    return cnt;
-}
-
-template <typename IDX>
-struct Node {
-    IDX start;
-    uint32_t deg, w32;
-};
-
-template <typename IDX>
-__device__ __forceinline__ Node<IDX> load_node(const NodeRec* nodes, uint32_t v)
-{
-    uint4 q;
-    if (GRAPE_HOT_HINT == 1)
-        asm("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-            : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w) : "l"(nodes + v), "l"(policy_evict_last()));
-    else
-        q = ldg_v4(nodes + v);
-    Node<IDX> r;
-    if constexpr (sizeof(IDX) == 8) r.start = ((uint64_t)q.y << 32) | q.x;
-    else r.start = q.x;
-    r.deg = q.z;
-    r.w32 = q.w;
-    return r;
-}
 
 __device__ __forceinline__ void st_cs_v4(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d)
 {
