@@ -47,6 +47,10 @@ constexpr uint32_t kEmptySlot = 0xFFFFFFFFu;
 #ifndef GRAPE_TAB_DRAWS
 #define GRAPE_TAB_DRAWS 2
 #endif
+#ifndef GRAPE_TAB_DRAW_UNROLL
+#define GRAPE_TAB_DRAW_UNROLL 1
+#endif
+constexpr int kDrawUnroll = GRAPE_TAB_DRAW_UNROLL;
 #ifndef GRAPE_TAB_SYNC_TOP
 #define GRAPE_TAB_SYNC_TOP 0     // explicit reconvergence points (measured: the emit one matters)
 #endif
@@ -509,7 +513,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
         // (§8(c) c12).  A lane whose attempt is decided from registers draws again
         // in the same iteration, up to GRAPE_TAB_DRAWS draws; a register-decided
         // return x = t is emitted on the spot when another draw follows it.
-#pragma unroll 1
+#pragma unroll kDrawUnroll
         for (int k = 0; k < GRAPE_TAB_DRAWS; ++k) {
             if (GRAPE_TAB_SYNC_DRAW) __syncwarp();
             if (!__any_sync(0xffffffffu, draw)) break;
