@@ -104,7 +104,7 @@ typedef struct {
     uint64_t max_row_weight;  /* max_v W_v (deg for unweighted) */
     uint64_t device_bytes;    /* device memory owned by the handle */
     int device;
-    uint32_t tables;          /* 1 if the sampling tables were built (v4 walker) */
+    uint32_t tables;          /* 1 if the sampling tables were built (table walker) */
     uint32_t weights_symmetric; /* 1 if every arc with a reverse arc has its weight */
     uint64_t table_bytes;     /* part of device_bytes held by the tables */
     uint32_t guide_factor;    /* weighted tables: guide buckets per arc (16 ... 1) */
@@ -281,12 +281,12 @@ typedef struct {
     uint64_t xnode_loads;       /* node-record loads of a proposal x (symmetric membership) */
     uint64_t cw_probes;         /* sector probes of weight-prefix searches (proposals) */
     uint64_t col_probes;        /* sector probes of membership searches */
-    uint64_t col_loads;         /* proposal loads: col[i] (v3) or arc records (v4, incl. guide-split scans) */
+    uint64_t col_loads;         /* proposal loads: col[i] (v3) or arc records (tables; incl. guide-split scans) */
     uint64_t attempts;          /* proposals drawn (Philox draws) */
     uint64_t membership_tests;  /* "x in N(t)" searches performed */
     uint64_t start_loads;       /* walks started */
     uint64_t steps;             /* realised transitions */
-    /* v4 (tables) walker; zero on the v3 walker: */
+    /* table walker only (zero on the v3 walker): */
     uint64_t guide_loads;       /* guide-table entries read (weighted proposals) */
     uint64_t hash_probes;       /* edge-hash sectors read by membership tests */
     uint64_t alu_decisions;     /* attempts decided without reading the graph */
