@@ -11,10 +11,12 @@
 // One warp per walk (walks from a shared counter), lanes over v's row in
 // chunks of 32 arcs: the arc records give x, its weight (difference of
 // consecutive prefix values, the predecessor's by shuffle) and the
-// no-common-neighbour flag of (t, v); "x in N(t)" is an edge-hash probe.  Two
-// passes over the row (total, then the running sum to the index) — O(deg v)
-// reads per step, the cost the paper's sampler has by construction.  It is the
-// paper-faithful mode, not the fast one.
+// no-common-neighbour flag of (t, v); "x in N(t)" is an edge-hash probe.  Pass 1
+// reduces the row's total and keeps each chunk's sum in a per-warp scratch; pass
+// 2 finds the chunk holding r from those sums and rescans only that chunk —
+// O(deg v) reads per step, the
+// cost the paper's sampler has by construction.  It is the paper-faithful mode,
+// not the fast one.
 #include "walk_common.cuh"
 
 namespace grape {
@@ -40,6 +42,8 @@ struct CdfParams {
     uint32_t h_mul, h_shift;       // floor(v / H)
     uint32_t xmask;                // compact records: x without flag bits
     bool notri;
+    uint4* chunk_scratch;          // per resident warp: chunks_max x {sum lo, sum mid, sum hi, carry}
+    uint64_t chunks_max;           // ceil(max degree / 32)
 };
 
 __device__ __forceinline__ uint32_t fmix32(uint32_t h)
@@ -141,6 +145,9 @@ template <bool WEIGHTED, bool COMPACT>
 __global__ void __launch_bounds__(256) walk_cdf_kernel(const __grid_constant__ CdfParams P)
 {
     const int lane = threadIdx.x & 31;
+    // per-warp chunk sums of the current row: {sum lo, sum hi, carry} x nchunks_max in global scratch
+    const uint64_t gwarp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    uint4* cs = P.chunk_scratch + gwarp * P.chunks_max;
     const uint32_t L = P.L;
     unsigned long long steps = 0;
     for (;;) {
@@ -194,7 +201,8 @@ __global__ void __launch_bounds__(256) walk_cdf_kernel(const __grid_constant__ C
                     }
                     return w * Tc;
                 };
-                // pass 1: the total
+                // pass 1: the total, and each 32-arc chunk's sum (and prefix carry) kept
+                // in the warp's scratch
                 U128 tot{0, 0};
                 uint32_t carry = 0;
                 for (uint32_t c0 = 0; c0 < vdeg; c0 += 32) {
@@ -202,6 +210,7 @@ __global__ void __launch_bounds__(256) walk_cdf_kernel(const __grid_constant__ C
                     uint32_t x = 0;
                     bool xnt = false;
                     uint64_t pi = 0;
+                    const uint32_t carry_in = carry;
                     if (WEIGHTED || k < vdeg) {
                         // weighted: every lane takes part in the shuffles (out-of-row lanes read a
                         // valid record of the padded array and are masked below)
@@ -217,15 +226,51 @@ __global__ void __launch_bounds__(256) walk_cdf_kernel(const __grid_constant__ C
                         b.hi = __shfl_xor_sync(0xffffffffu, a.hi, o);
                         a = add128(a, b);
                     }
+                    if (lane == 0)   // a chunk's sum < 2^69
+                        cs[c0 >> 5] = make_uint4((uint32_t)a.lo, (uint32_t)(a.lo >> 32), (uint32_t)a.hi, carry_in);
                     tot = add128(tot, a);
                 }
                 const U128 r = bounded128(dr.x64, tot);
-                // pass 2: the running sum to the first index beyond r
+                __syncwarp();
+                // pass 2: the first chunk whose running sum exceeds r (from the kept chunk
+                // sums), then the running sum inside it
                 U128 run{0, 0};
-                carry = 0;
+                uint32_t cfirst = 0;
+                {
+                    const uint32_t nch = (vdeg + 31) >> 5;
+                    for (uint32_t b0 = 0; b0 < nch; b0 += 32) {
+                        const uint32_t c = b0 + lane;
+                        const uint4 e = c < nch ? cs[c] : make_uint4(0, 0, 0, 0);
+                        U128 a{(uint64_t)e.y << 32 | e.x, (uint64_t)e.z};
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const U128 b = shfl_up128(a, o);
+                            if (lane >= o) a = add128(a, b);
+                        }
+                        const U128 cum = add128(run, a);
+                        const unsigned hit = __ballot_sync(0xffffffffu, c < nch && gt128(cum, r));
+                        if (hit) {
+                            const int src = __ffs(hit) - 1;
+                            cfirst = b0 + src;
+                            const U128 before = shfl128(a, src);   // inclusive sum up to chunk cfirst
+                            const U128 mine{(uint64_t)e.y << 32 | e.x, (uint64_t)e.z};
+                            const U128 own = shfl128(mine, src);
+                            // run = (run + before) - own: the sum of the chunks before cfirst
+                            U128 t2 = add128(run, before);
+                            U128 negown;
+                            negown.lo = ~own.lo + 1;
+                            negown.hi = ~own.hi + (own.lo == 0 ? 1 : 0);
+                            run = add128(t2, negown);
+                            break;
+                        }
+                        run = add128(run, shfl128(a, 31));
+                    }
+                    carry = cs[cfirst].w;
+                }
+                __syncwarp();
                 uint32_t xsel = 0;
                 bool ntsel = false;
-                for (uint32_t c0 = 0; c0 < vdeg; c0 += 32) {
+                for (uint32_t c0 = cfirst * 32; c0 < vdeg; c0 += 32) {
                     const uint32_t k = c0 + lane;
                     uint32_t x = 0;
                     bool xnt = false;
@@ -297,13 +342,17 @@ cudaError_t launch(const grape_graph* g, const WalkArgs& a, const Thresholds& T,
     }
     uint64_t blocks = (a.num_walks * 32 + 255) / 256;
     if (blocks > (uint64_t)resident) blocks = resident;
+    P.chunks_max = ((uint64_t)g->max_degree + 31) / 32 + 1;
     cudaError_t e = cudaMallocAsync((void**)&P.next, 8, stream);
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(P.next, 0, 8, stream);
+    if (e == cudaSuccess)
+        e = cudaMallocAsync((void**)&P.chunk_scratch, blocks * 8 * P.chunks_max * sizeof(uint4), stream);
     if (e == cudaSuccess) {
         walk_cdf_kernel<WEIGHTED, COMPACT><<<(unsigned)blocks, 256, 0, stream>>>(P);
         e = cudaGetLastError();
     }
+    if (P.chunk_scratch) cudaFreeAsync(P.chunk_scratch, stream);
     cudaFreeAsync(P.next, stream);
     return e;
 }
