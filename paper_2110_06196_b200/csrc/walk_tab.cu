@@ -60,6 +60,9 @@ constexpr int kDrawUnroll = GRAPE_TAB_DRAW_UNROLL;
 #ifndef GRAPE_TAB_SYNC_DRAW
 #define GRAPE_TAB_SYNC_DRAW 1
 #endif
+#ifndef GRAPE_TAB_DYN_MIN_ROUNDS
+#define GRAPE_TAB_DYN_MIN_ROUNDS 2
+#endif
 #ifndef GRAPE_TAB_STATIC_PCT
 #define GRAPE_TAB_STATIC_PCT 50
 #endif
@@ -715,13 +718,14 @@ cudaError_t launch_k(const grape_graph* g, const WalkArgs& a, const Thresholds& 
     if (blocks > (uint64_t)resident) blocks = resident;
     P.lanes = (uint32_t)(blocks * kBlock);
     // static share: GRAPE_TAB_STATIC_PCT percent of the walks, in whole rounds of the grid
-    // (launches of under 4 rounds are all static: no counter to allocate)
+    // (launches of under GRAPE_TAB_DYN_MIN_ROUNDS rounds are all static: no counter to allocate)
     const uint64_t rounds = a.num_walks / P.lanes;
     uint64_t srounds = rounds * GRAPE_TAB_STATIC_PCT / 100;
     if (srounds < 1) srounds = 1;
-    P.nstatic = rounds < 4 ? ~0ull : srounds * P.lanes;   // >= lanes: every lane's first walk is static
+    const bool dyn = rounds >= GRAPE_TAB_DYN_MIN_ROUNDS;
+    P.nstatic = dyn ? srounds * P.lanes : ~0ull;   // >= lanes: every lane's first walk is static
     cudaError_t e = cudaSuccess;
-    if (rounds >= 4) {
+    if (dyn) {
         e = cudaMallocAsync((void**)&P.next, 8, stream);
         if (e != cudaSuccess) return e;
         e = cudaMemsetAsync(P.next, 0, 8, stream);
