@@ -377,6 +377,10 @@ def run_ours(args):
                 "algorithmic_bytes_per_launch": alg_bytes,
                 "bytes_per_step": alg_bytes / max(ev["steps"], 1),
                 "events_per_launch": ev,
+                # achieved HBM bandwidth (BASELINE metric): the ncu-measured DRAM bytes of one launch
+                # of this kernel (profiles/traffic_cfgK.json) over the launch time measured here
+                "dram_gbs": (traffic / t_launch / 1e9) if traffic else None,
+                "dram_frac": (traffic / t_launch / 1e9 / peak) if traffic else None,
                 "random_access": {"compulsory_sectors_per_step": rand_sectors / max(ev["steps"], 1),
                                   "achieved_per_s": rand_sectors / t_launch,
                                   "ceiling_per_s": ceil,
