@@ -1,6 +1,6 @@
 #!/usr/bin/env python
 """Write profiles/traffic_cfgK.json (DRAM bytes per launch of the walk kernel) from
-an `ncu --set full` report of one timed launch:  tools/traffic.py REP K [kernel-tag]"""
+an ncu report of one timed launch:  tools/traffic.py REP K [mode]"""
 import csv, io, json, subprocess, sys
 rep, k = sys.argv[1], int(sys.argv[2])
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
@@ -16,7 +16,8 @@ scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 rd *= scale.get(unit_row[col["dram__bytes_read.sum"]], 1)
 wr *= scale.get(unit_row[col["dram__bytes_write.sum"]], 1)
 kern = vals[col["Kernel Name"]]
+mode = sys.argv[3] if len(sys.argv) > 3 else "node2vec"
 out = {"dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr, "kernel": kern,
-       "source": rep.split("/")[-1]}
+       "source": rep.split("/")[-1], "mode": mode}
 json.dump(out, open(f"profiles/traffic_cfg{k}.json", "w"), indent=1)
 print(json.dumps(out))
