@@ -349,7 +349,8 @@ def run_ours(args):
         if traffic is None and os.path.exists(tfile):
             tj = json.load(open(tfile))
             # only a capture of the same kernel and walk mode counts
-            if kname in tj.get("kernel", "") and tj.get("mode", wk["mode"]) == wk["mode"]:
+            if (kname in tj.get("kernel", "") and tj.get("mode", wk["mode"]) == wk["mode"]
+                    and tj.get("sampler", "rejection") == args.sampler and tj.get("dT", 0) == dT):
                 traffic = tj["dram_bytes_per_launch"]
         # random-sector ceiling at this graph's randomly read footprint (measured,
         # profiles/gather_footprint.json; linear interpolation in footprint)
