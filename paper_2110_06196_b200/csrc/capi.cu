@@ -3,6 +3,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include "internal.h"
 
@@ -77,7 +78,10 @@ struct DeviceGuard {
 };
 
 #ifndef GRAPE_HOST_CHUNK_MB
-#define GRAPE_HOST_CHUNK_MB 256
+#define GRAPE_HOST_CHUNK_MB 256        // smallest default chunk of the walk matrix
+#endif
+#ifndef GRAPE_HOST_CHUNK_MAX_MB
+#define GRAPE_HOST_CHUNK_MAX_MB 1024
 #endif
 #ifndef GRAPE_HOST_NBUF
 #define GRAPE_HOST_NBUF 2
@@ -87,14 +91,22 @@ struct DeviceGuard {
 // caller's stream (H2D starts -> kernel), its D2H runs on an internal copy
 // stream, so the copy of chunk k overlaps the kernels of chunks k+1 ..; with
 // NBUF staging buffers the kernels run ahead of the (PCIe-bound) copies.
+// Chunk size: ~1/32 of the walk matrix within [256 MB, 1 GB] (measured, DESIGN.md
+// §9: small chunks cost per-launch tails on slow-per-walk workloads, large ones
+// leave the first kernel and the last copy unoverlapped); halved while the
+// staging allocation fails; GRAPE_HOST_CHUNK_MB in the environment overrides it.
 grape_status walks_host(const grape_graph* g, const WalkArgs& a, bool n2v, const Thresholds& T,
                         cudaStream_t stream, uint64_t* steps_host)
 {
     constexpr int NB = GRAPE_HOST_NBUF;
     const uint64_t L = a.L;
-    uint64_t chunk = ((uint64_t)GRAPE_HOST_CHUNK_MB << 20) / (4 * L);   // walks per chunk, >= 1
-    if (chunk < 1) chunk = 1;
-    if (chunk > a.num_walks) chunk = a.num_walks;
+    uint64_t chunk_mb = (a.num_walks * L * 4 >> 20) / 32;
+    if (chunk_mb < GRAPE_HOST_CHUNK_MB) chunk_mb = GRAPE_HOST_CHUNK_MB;
+    if (chunk_mb > GRAPE_HOST_CHUNK_MAX_MB) chunk_mb = GRAPE_HOST_CHUNK_MAX_MB;
+    if (const char* env = getenv("GRAPE_HOST_CHUNK_MB")) {   // tuning knob (bench A/B)
+        const long v = atol(env);
+        if (v > 0) chunk_mb = (uint64_t)v;
+    }
     uint32_t* d_starts[NB] = {};
     uint32_t* d_out[NB] = {};
     unsigned long long* d_steps = nullptr;
@@ -102,27 +114,38 @@ grape_status walks_host(const grape_graph* g, const WalkArgs& a, bool n2v, const
     cudaEvent_t ev_kernel[NB] = {}, ev_copied[NB] = {};
     grape_status st = GRAPE_OK;
     cudaError_t e = cudaSuccess;
-    const uint64_t nchunks = (a.num_walks + chunk - 1) / chunk;
-    const int nbuf = nchunks < (uint64_t)NB ? (int)nchunks : NB;
-    // one device allocation for all staging buffers: the graph's cached one when free
-    const uint64_t per = ((chunk * 4 + 255) & ~255ull) + ((chunk * L * 4 + 255) & ~255ull);
-    const uint64_t need = per * nbuf + 256;
     grape_graph* gm = const_cast<grape_graph*>(g);
     std::unique_lock<std::mutex> lk(gm->stage_mu, std::try_to_lock);
     char* base = nullptr;
     bool own = false;
-    if (lk.owns_lock()) {
-        if (gm->stage_bytes < need) {
-            cudaFree(gm->stage_buf);
-            gm->stage_buf = nullptr;
-            gm->stage_bytes = 0;
-            e = cudaMalloc(&gm->stage_buf, need);
-            if (e == cudaSuccess) gm->stage_bytes = need;
+    uint64_t chunk, nchunks, per;
+    int nbuf;
+    for (;;) {
+        chunk = (chunk_mb << 20) / (4 * L);   // walks per chunk, >= 1
+        if (chunk < 1) chunk = 1;
+        if (chunk > a.num_walks) chunk = a.num_walks;
+        nchunks = (a.num_walks + chunk - 1) / chunk;
+        nbuf = nchunks < (uint64_t)NB ? (int)nchunks : NB;
+        // one device allocation for all staging buffers: the graph's cached one when free
+        per = ((chunk * 4 + 255) & ~255ull) + ((chunk * L * 4 + 255) & ~255ull);
+        const uint64_t need = per * nbuf + 256;
+        if (lk.owns_lock()) {
+            e = cudaSuccess;
+            if (gm->stage_bytes < need) {
+                cudaFree(gm->stage_buf);
+                gm->stage_buf = nullptr;
+                gm->stage_bytes = 0;
+                e = cudaMalloc(&gm->stage_buf, need);
+                if (e == cudaSuccess) gm->stage_bytes = need;
+            }
+            base = (char*)gm->stage_buf;
+        } else {
+            e = cudaMalloc((void**)&base, need);
+            own = e == cudaSuccess;
         }
-        base = (char*)gm->stage_buf;
-    } else {
-        e = cudaMalloc((void**)&base, need);
-        own = e == cudaSuccess;
+        if (e != cudaErrorMemoryAllocation || chunk_mb <= 16 || chunk == 1) break;
+        cudaGetLastError();   // clear the allocation failure and retry smaller
+        chunk_mb /= 2;
     }
     for (int b = 0; b < nbuf && e == cudaSuccess; ++b) {
         d_starts[b] = (uint32_t*)(base + b * per);

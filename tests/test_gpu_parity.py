@@ -144,6 +144,25 @@ def test_host_buffer_path_equals_device_path(grape):
     assert int(dsteps.item()) == int(steps.item())
 
 
+@pytest.mark.parametrize("chunk_mb", ["1", "3"])
+def test_host_buffer_path_many_chunks(grape, monkeypatch, chunk_mb):
+    """The staged pipeline with many chunks (and a ragged last one), the staging buffer
+    cached in the graph reused across calls of different sizes."""
+    monkeypatch.setenv("GRAPE_HOST_CHUNK_MB", chunk_mb)
+    g = config_graph(2, scale_down=6)
+    dg = _dev_graph(grape, g)
+    for W, L in ((g.n * 4 + 7, 40), (g.n + 3, 113), (5, 3)):
+        starts = starts_per_node(g.n, 5)[:W]
+        assert starts.numel() * L * 4 > 2 * (int(chunk_mb) << 20) or W == 5
+        dev = grape.walks_node2vec(dg, starts.cuda(), L, 0.5, 2.0, seed=9, walk_id_base=3)
+        steps = torch.zeros(1, dtype=torch.int64)
+        host = grape.walks_node2vec(dg, starts, L, 0.5, 2.0, seed=9, walk_id_base=3, steps=steps)
+        assert torch.equal(dev.cpu(), host), (W, L)
+        dsteps = torch.zeros(1, dtype=torch.int64, device="cuda")
+        grape.walks_node2vec(dg, starts.cuda(), L, 0.5, 2.0, seed=9, walk_id_base=3, steps=dsteps)
+        assert int(dsteps.item()) == int(steps.item())
+
+
 def test_sharding_and_determinism(grape):
     """Rank slices [r W/G, (r+1) W/G) with walk_id_base = slice start reproduce the
     single call bit for bit; re-running is deterministic."""
