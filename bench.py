@@ -121,11 +121,22 @@ def _allreduce(x: float, op, world):
     return float(t.item())
 
 
-def _oracle_sample(g_cpu, wk, budget_s: float, first_wid: int = 0, cores: int | None = None, dT: int = 0):
+def _oracle_sample(g_cpu, wk, budget_s: float, first_wid: int = 0, cores: int | None = None, dT: int = 0,
+                   sampler: str = "rejection"):
     """Run the oracle (as it stands) on consecutive walks until ~budget_s of CPU
-    work per thread; returns (realised steps, seconds, walks, threads, attempts)."""
+    work per thread; returns (realised steps, seconds, walks, threads, attempts).
+    sampler: the node2vec rule the GPU arm runs (rejection / cdf / folded)."""
     from oracle.oracle import Oracle
     o = Oracle(*g_cpu.numpy())
+    if wk["mode"] == "node2vec" and not dT and sampler in ("cdf", "folded"):
+        alt = o.walks_cdf if sampler == "cdf" else o.walks_folded
+
+        class _O:   # the same call shape as Oracle.walks for the sampling loop below
+            @staticmethod
+            def walks(starts, L, mode, p, q, seed, base=0, with_attempts=False):
+                out, st = alt(starts, L, p=p, q=q, seed=seed, base=base)
+                return (out, st, 0) if with_attempts else (out, st)
+        o = _O()
     n = g_cpu.n
     cores = cores or os.cpu_count() or 1
     W = n * wk["walks_per_node"]
@@ -198,7 +209,7 @@ def run_reference(args):
     vals, total_steps, total_secs = [], 0, 0.0
     for i in range(args.warmup + args.steps):
         steps, secs, walks, cores, _ = _oracle_sample(g, wk, args.ref_budget, first_wid=(i * 997) % max(W - 1, 1),
-                                                      dT=args.approx)
+                                                      dT=args.approx, sampler=args.sampler)
         if i >= args.warmup:
             vals.append(steps / secs)
             total_steps += steps
@@ -208,6 +219,10 @@ def run_reference(args):
               "random-walk steps/sec (first-order)")
     if args.approx:
         metric = metric[:-1] + f", approximated: SUSS d_T={args.approx})"
+    if wk["mode"] == "node2vec" and args.sampler == "cdf":
+        metric = metric[:-1] + ", paper CDF sampler)"
+    if wk["mode"] == "node2vec" and args.sampler == "folded":
+        metric = metric[:-1] + ", outlier-folded rejection)"
     line = {"impl": "reference", "metric": metric, "value": v,
             "unit": "steps/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * total_secs / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -332,7 +347,7 @@ def run_ours(args):
     # ---- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and not args.no_cpu and world == 1:
-        s, secs, walks, cores, att = _oracle_sample(g, wk, args.cpu_budget, dT=dT)
+        s, secs, walks, cores, att = _oracle_sample(g, wk, args.cpu_budget, dT=dT, sampler=args.sampler)
         cpu = {"value": s / secs, "unit": "steps/s", "cores": cores, "kind": "oracle",
                "sample": f"first {walks} walks (wid 0..{walks - 1}) of the same workload, "
                          f"{cores} threads, {secs:.1f} s"}
