@@ -87,6 +87,17 @@ struct RowWriter {
             first = s + 1;
         }
     }
+    // entries [s, end) = PAD (a dead end or the end of an early-ending walk): the staged
+    // entries [first, s) are written out, then PAD with 16-B stores where aligned
+    __device__ __forceinline__ void pad(uint32_t s, uint32_t end)
+    {
+        finish(s);
+        uint32_t q = s;
+        for (; q < end && (((uintptr_t)(row + q)) & 15) != 0; ++q) row[q] = kPad;
+        for (; q + 4 <= end; q += 4) st_cs_v4(row + q, kPad, kPad, kPad, kPad);
+        for (; q < end; ++q) row[q] = kPad;
+        first = end;
+    }
     __device__ __forceinline__ void finish(uint32_t end)   // flush [first, end)
     {
         for (uint32_t q = first; q < end; ++q) row[q] = slot[((phase + q) & 7) * kBlock];

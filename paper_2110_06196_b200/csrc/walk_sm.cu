@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) walk_sm_kernel(const __gri
             }
         }
         if (fin) {
-            for (uint32_t q = s; q < L; ++q) w.put(q, kPad);
+            w.pad(s, L);
             w.finish(L);
             i += stride;
             st = i < P.num_walks ? ST_START : ST_DONE;

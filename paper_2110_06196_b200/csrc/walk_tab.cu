@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
             }
         }
         if (fin) {
-            for (uint32_t q = s; q < L; ++q) w.put(q, kPad);
+            w.pad(s, L);
             w.finish(L);
             // next walk: round-robin over the statically assigned prefix [0, P.nstatic),
             // then from the shared counter (balances the tail across lanes)
