@@ -692,3 +692,70 @@ int oracle_folded_steps(const uint64_t* off, const uint32_t* col, const uint64_t
         x_out[k] = oracle_folded_step(off, col, cw, T, seed, wid0 + k, s, t, v, &att_out[k]);
     return 0;
 }
+
+/* ---------------------------------------------------------------------------
+ * SkipGram consumer (readings f3-a..d): the
+ * training pairs of the shallow models the walks feed ("given a window
+ * size, these models learn ... the co-occurrence of two nodes in each window";
+ * P:399 SkipGram "predicts the contextual nodes of a sequence given its central
+ * node") and their negatives, "scale-free negative sampling, which is
+ * efficiently implemented using the Elias-Fano data structure rank method"
+ * (P:405), over the "outbound ... node degrees scale-free distribution"
+ * (P:319): a uniform arc index e in [0, m) and the node whose row holds it.
+ * ------------------------------------------------------------------------- */
+
+/* rank(e): the node v whose row holds arc index e, off[v] <= e < off[v+1]
+ * (the largest v with off[v] <= e; rows of degree 0 hold no index).  e < m. */
+uint32_t oracle_rank(uint32_t n, const uint64_t* off, uint64_t e)
+{
+    uint32_t lo = 0, hi = n - 1;   /* off[lo] <= e < off[hi + 1] throughout */
+    while (lo < hi) {
+        uint32_t mid = lo + (hi - lo + 1) / 2;
+        if (off[mid] <= e)
+            lo = mid;
+        else
+            hi = mid - 1;
+    }
+    return lo;
+}
+
+/* Pairs and negatives of walks [0, num_walks) (walk ids base + r), window w,
+ * K negatives per pair.  Slot p = ((wid * L + i) * 2w + o) - base * L * 2w,
+ * offset o = 0 .. 2w-1 standing for j = -w .. -1, 1 .. w (f3-a):
+ *   centers[p] = row[i], contexts[p] = row[i + j] if 0 <= i + j < L and both
+ *   are not PAD; otherwise both PAD (f3-b);
+ *   negs[p * K + k] = rank(BOUNDED(x64(DRAW(seed, P, 0xFFFFFFFF, k)), m)) for
+ *   a valid slot, P = its global slot index (wid * L + i) * 2w + o (f3-c);
+ *   PAD for an invalid slot, or when m = 0.
+ * Returns 0. */
+int oracle_skipgram(uint32_t n, const uint64_t* off, const uint32_t* walks, uint64_t num_walks,
+                    uint64_t base, uint32_t L, uint32_t w, uint32_t K, uint64_t seed,
+                    uint32_t* centers, uint32_t* contexts, uint32_t* negs)
+{
+    const uint64_t m = n ? off[n] : 0;
+    uint64_t r, p = 0;
+    for (r = 0; r < num_walks; r++) {
+        const uint32_t* row = walks + r * L;
+        uint32_t i, o, k;
+        for (i = 0; i < L; i++) {
+            for (o = 0; o < 2 * w; o++, p++) {
+                const int64_t j = o < w ? (int64_t)o - (int64_t)w : (int64_t)o - (int64_t)w + 1;
+                const int64_t c = (int64_t)i + j;
+                const int valid = c >= 0 && c < (int64_t)L && row[i] != ORACLE_PAD && row[c] != ORACLE_PAD;
+                const uint64_t P = ((base + r) * L + i) * (uint64_t)(2 * w) + o;
+                centers[p] = valid ? row[i] : ORACLE_PAD;
+                contexts[p] = valid ? row[c] : ORACLE_PAD;
+                for (k = 0; k < K; k++) {
+                    uint32_t d[4];
+                    if (!valid || m == 0) {
+                        negs[p * K + k] = ORACLE_PAD;
+                        continue;
+                    }
+                    oracle_draw(seed, P, 0xFFFFFFFFu, k, d);
+                    negs[p * K + k] = oracle_rank(n, off, oracle_bounded(x64_of(d), m));
+                }
+            }
+        }
+    }
+    return 0;
+}

@@ -91,6 +91,12 @@ def _load():
                 _u64p, _u32p, _u64p, ctypes.c_double, ctypes.c_double, ctypes.c_uint64,
                 ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, _u32p, _u32p]
             lib.oracle_folded_steps.restype = ctypes.c_int
+            lib.oracle_rank.argtypes = [ctypes.c_uint32, _u64p, ctypes.c_uint64]
+            lib.oracle_rank.restype = ctypes.c_uint32
+            lib.oracle_skipgram.argtypes = [
+                ctypes.c_uint32, _u64p, _u32p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32,
+                ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64, _u32p, _u32p, _u32p]
+            lib.oracle_skipgram.restype = ctypes.c_int
             _lib = lib
     return _lib
 
@@ -214,6 +220,24 @@ class Oracle:
         if rc != 0:
             raise ValueError(f"oracle rejected p={p} q={q}")
         return out, int(steps.value)
+
+    def rank(self, e: int) -> int:
+        """The node whose row holds arc index e (P:405's Elias-Fano rank; §8(f) f3)."""
+        return int(_load().oracle_rank(self.n, _p64(self.off), int(e)))
+
+    def skipgram(self, walks, window: int, negatives: int, *, seed: int = 42, base: int = 0):
+        """SkipGram pairs and scale-free negatives of a walk matrix (§8(f) f3):
+        (centers u32[S], contexts u32[S], negs u32[S, K]), S = rows * L * 2 * window."""
+        walks = np.ascontiguousarray(walks, dtype=np.uint32)
+        nw, L = walks.shape
+        S = nw * L * 2 * window
+        c = np.empty(S, dtype=np.uint32)
+        x = np.empty(S, dtype=np.uint32)
+        ng = np.empty((S, negatives), dtype=np.uint32)
+        _load().oracle_skipgram(self.n, _p64(self.off), walks.ctypes.data_as(_u32p), nw, base, L, window,
+                                negatives, seed, c.ctypes.data_as(_u32p), x.ctypes.data_as(_u32p),
+                                ng.ctypes.data_as(_u32p))
+        return c, x, ng
 
     def walks_folded(self, starts, L: int, *, p: float = 1.0, q: float = 1.0, seed: int = 42, base: int = 0,
                      with_attempts: bool = False):

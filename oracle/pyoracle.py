@@ -265,6 +265,33 @@ class PyGraph:
         return row, steps
 
 
+def skipgram(g: PyGraph, walks, window, K, seed=42, base=0):
+    """SkipGram pairs + scale-free negatives (§8(f) f3): lists (centers, contexts,
+    negatives-per-slot), slot order (row, i, j = -w..-1, 1..w)."""
+    m = g.off[-1] if g.n else 0
+    centers, contexts, negs = [], [], []
+    for r, row in enumerate(walks):
+        L = len(row)
+        for i in range(L):
+            for j in list(range(-window, 0)) + list(range(1, window + 1)):
+                o = j + window if j < 0 else j + window - 1
+                c = i + j
+                ok = 0 <= c < L and row[i] != PAD and row[c] != PAD
+                centers.append(row[i] if ok else PAD)
+                contexts.append(row[c] if ok else PAD)
+                slot = ((base + r) * L + i) * 2 * window + o
+                ks = []
+                for k in range(K):
+                    if not ok or m == 0:
+                        ks.append(PAD)
+                        continue
+                    d = draw(seed, slot, 0xFFFFFFFF, k)
+                    e = bounded(d[1] << 32 | d[0], m)
+                    ks.append(bisect.bisect_right(g.off, e) - 1)   # the row holding arc e
+                negs.append(ks)
+    return centers, contexts, negs
+
+
 def eq1_law(g: PyGraph, t, v, p, q, weights_of=None):
     """Exact node2vec step law from Eq.1 as Fractions:
     pi_vx = alpha_pq(t,x) w_vx, alpha = 1/p (x == t), 1 (x in N(t)), 1/q (else)."""
