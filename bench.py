@@ -444,6 +444,110 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_skipgram(args):
+    """--skipgram: the SkipGram consumer.  One step =
+    the config's walks for a batch of B walk ids (the walk kernel) + their window-w
+    pairs and K scale-free negatives (grape_skipgram_pairs), both on the device.
+    Reports training slots/s of the whole step, the pair kernel alone, and the pair
+    kernel's HBM roofline (its output words are written once, coalesced)."""
+    world, rank, local = _dist_setup(args)
+    import paper_2110_06196_b200 as grape
+    from paper_2110_06196_b200.shard import weak_scaling_range
+    k = args.config
+    wk = _walk_recipe(args)
+    win, K = args.window, args.negatives
+    dev = torch.device("cuda", local)
+    g = config_graph(k, device=dev)
+    torch.cuda.empty_cache()
+    dg = grape.graph_from_csr(g.off, g.col, g.w, device=local, symmetric=g.symmetric)
+    g = g.to("cpu")
+    torch.cuda.empty_cache()
+    W = g.n * wk["walks_per_node"]
+    B = min(W, args.skipgram)
+    L = wk["L"]
+    base, _ = weak_scaling_range(B, rank, world)
+    starts = starts_per_node(g.n, wk["walks_per_node"], device=dev)[:B].contiguous()
+    walks = torch.empty((B, L), dtype=torch.int32, device=dev)
+    S = B * L * 2 * win
+    outs = (torch.empty(S, dtype=torch.int32, device=dev), torch.empty(S, dtype=torch.int32, device=dev),
+            torch.empty((S, K), dtype=torch.int32, device=dev))
+    node2vec = wk["mode"] == "node2vec"
+    ctr = torch.zeros(1, dtype=torch.int64, device=dev)
+
+    def walk(c):
+        kw = dict(seed=wk["seed"], walk_id_base=base, out=walks, steps=c)
+        if node2vec:
+            grape.walks_node2vec(dg, starts, L, wk["p"], wk["q"], **kw)
+        else:
+            grape.walks_first_order(dg, starts, L, **kw)
+
+    def pairs():
+        grape.skipgram_pairs(dg, walks, win, K, seed=wk["seed"] + 1, walk_id_base=base, out=outs)
+
+    for _ in range(args.warmup):
+        walk(None)
+        pairs()
+    torch.cuda.synchronize(dev)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    with ClockSampler(local) as clk:
+        for e in evs:
+            e[0].record()
+            walk(ctr)
+            e[1].record()
+            pairs()
+            e[2].record()
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    t_walk = sum(e[0].elapsed_time(e[1]) for e in evs) / 1e3
+    t_pair = sum(e[1].elapsed_time(e[2]) for e in evs) / 1e3
+    valid = int((outs[0] != -1).sum().item())
+    steps = float(ctr.item())
+    tot = _allreduce(t_walk + t_pair, dist.ReduceOp.MAX, world)
+    slots_all = _allreduce(float(valid * args.steps), dist.ReduceOp.SUM, world)
+    peak, peak_src = _peaks()
+    bytes_pair = S * (2 + K) * 4 + B * L * 4   # outputs written once + the walk matrix read once
+    cpu = None
+    if rank == 0 and not args.no_cpu and world == 1:
+        from oracle.oracle import Oracle
+        o = Oracle(*g.numpy())
+        wn = walks.cpu().numpy().view(np.uint32)
+        t0 = time.perf_counter()
+        o.skipgram(wn[:64], win, K, seed=wk["seed"] + 1, base=base)
+        per = max(time.perf_counter() - t0, 1e-4) / 64
+        nrows = int(min(B, max(64, args.cpu_budget / per)))
+        t0 = time.perf_counter()
+        c_, _, _ = o.skipgram(wn[:nrows], win, K, seed=wk["seed"] + 1, base=base)
+        dt = time.perf_counter() - t0
+        cpu = {"value": float((c_ != 0xFFFFFFFF).sum()) / dt, "unit": "training pairs/s", "cores": 1,
+               "kind": "oracle", "sample": f"oracle_skipgram on the first {nrows} walk rows of the batch, "
+                                           f"1 thread, {dt:.1f} s (walk time not included)"}
+    if rank == 0:
+        line = {"metric": f"SkipGram training pairs/s (window {win}, {K} scale-free negatives each) from "
+                          f"{'node2vec' if node2vec else 'first-order'} walks, walk + pair kernels",
+                "value": slots_all / tot, "unit": "training pairs/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "u32 integer",
+                "data": "synthetic (seeded generator, graphgen/)",
+                "config": dict(_workload_desc(k, g, wk, B), batch_walks=B, window=win, negatives=K),
+                "gpu_launches": 2 * args.steps,
+                "walk_steps_per_s_with_pairs": steps / (t_walk + t_pair),
+                "walk_steps_per_s_alone": steps / t_walk,
+                "pair_kernel": {"ms": 1e3 * t_pair / args.steps, "slots": S, "valid_pairs": valid,
+                                "negatives_per_s": valid * K * args.steps / t_pair},
+                "roofline": {"bound": "hbm", "kernel": "skipgram_kernel (grape_skipgram_pairs)",
+                             "achieved": bytes_pair * args.steps / t_pair / 1e9, "peak": peak, "unit": "GB/s",
+                             "frac": bytes_pair * args.steps / t_pair / 1e9 / peak, "traffic": None,
+                             "peak_source": peak_src, "algorithmic_bytes_per_launch": bytes_pair},
+                "cpu_baseline": cpu, "e2e": None, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    dg.free()
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -458,6 +562,10 @@ def main():
     ap.add_argument("--traffic-per-launch", type=float, default=None,
                     help="ncu dram bytes per launch of the walk kernel (from profiles/)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--skipgram", type=int, default=0, metavar="B",
+                    help="SkipGram consumer mode (§8(f) f3): B walks per step + their pairs / negatives")
+    ap.add_argument("--window", type=int, default=5)
+    ap.add_argument("--negatives", type=int, default=5)
     ap.add_argument("--no-tables", action="store_true", help="GRAPE_NO_TABLES: the v3 fenced-search walker")
     ap.add_argument("--sampler", default="rejection", choices=["rejection", "cdf", "folded"],
                     help="node2vec sampler: the default rejection rules, or the paper's CDF sampler "
@@ -472,6 +580,8 @@ def main():
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
     if args.impl == "reference":
         run_reference(args)
+    elif args.skipgram:
+        run_skipgram(args)
     else:
         run_ours(args)
 

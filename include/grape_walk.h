@@ -266,6 +266,38 @@ grape_status grape_walks_node2vec_folded(const grape_graph* g, const uint32_t* s
                                          cudaStream_t stream);
 
 /*
+ * grape_skipgram_pairs — the SkipGram consumer of a walk matrix (SURVEY §8(f)
+ * row f3): the (center, context) pairs of the sliding window
+ * ("given a window size, these models learn ... the co-occurrence of two nodes
+ * in each window"; SkipGram "predicts the contextual nodes of a sequence
+ * given its central node") and, per pair, num_negatives negatives from
+ * the out-degree "scale-free" distribution — the node whose row holds a uniform
+ * arc index, the rank the paper implements on Elias-Fano.
+ *   walks          device u32[num_walks][walk_length], rows of walk ids
+ *                  walk_id_base + r (as written by grape_walks_*; PAD suffixes)
+ *   window         w >= 1: offsets j = -w .. -1, 1 .. w
+ *   centers, contexts  device u32[S], S = num_walks * walk_length * 2w; slot
+ *                  p = (r * walk_length + i) * 2w + o, o = 0 .. 2w-1 for
+ *                  j = -w .. -1, 1 .. w: (row[i], row[i+j]) when 0 <= i+j < L
+ *                  and both entries are not PAD, else (PAD, PAD)
+ *   negatives      device u32[S][num_negatives] (may be NULL if 0): for a valid
+ *                  slot, negative k = rank(floor(x64 * m / 2^64)), x64 = words
+ *                  o1:o0 of Philox4x32-10 with counter (P lo, P hi, 0xFFFFFFFF,
+ *                  k), key = seed, P = ((walk_id_base + r) * L + i) * 2w + o the
+ *                  global slot id (so shards reproduce slices of one call);
+ *                  rank(e) = the v with off[v] <= e < off[v+1]; PAD for an
+ *                  invalid slot or a graph without arcs.
+ * Device buffers only; asynchronous on `stream` (the first call on a graph
+ * builds its node guide, ~4 n bytes, synchronously).  Errors: EINVAL on NULL
+ * buffers, host buffers, walk_length = 0, window = 0 or > 1024, num_negatives
+ * > 1024, slot-count overflow, a device mismatch; ECUDA on launch failure.
+ */
+grape_status grape_skipgram_pairs(const grape_graph* g, const uint32_t* walks, uint64_t num_walks,
+                                  uint64_t walk_id_base, uint32_t walk_length, uint32_t window,
+                                  uint32_t num_negatives, uint64_t seed, uint32_t* centers, uint32_t* contexts,
+                                  uint32_t* negatives, cudaStream_t stream);
+
+/*
  * grape_walks_stats — diagnostics: run the same walks as grape_walks_first_order
  * (node2vec = 0) or grape_walks_node2vec (node2vec = 1) with event counters
  * compiled into the kernel, and return the counts.  `out` receives exactly the

@@ -175,6 +175,34 @@ def walks_node2vec_folded(g: Graph, starts, L: int, p: float, q: float, *, seed:
                   out, steps, stream)
 
 
+def skipgram_pairs(g: Graph, walks, window: int, num_negatives: int, *, seed: int = 42, walk_id_base: int = 0,
+                   out=None, stream=None):
+    """grape_skipgram_pairs: SkipGram (center, context) pairs of every window offset and
+    scale-free negatives.  walks: CUDA int32 [W, L] (a walk matrix).
+    Returns (centers int32[S], contexts int32[S], negatives int32[S, K]), S = W*L*2*window;
+    invalid slots hold PAD (-1)."""
+    if not (torch.is_tensor(walks) and walks.is_cuda and walks.dim() == 2):
+        raise ValueError("walks must be a 2-D CUDA tensor (a walk matrix)")
+    walks = walks.contiguous()
+    W, L = walks.shape
+    S = W * L * 2 * window
+    with torch.cuda.device(g.device):
+        if out is None:
+            out = (torch.empty(S, dtype=torch.int32, device=walks.device),
+                   torch.empty(S, dtype=torch.int32, device=walks.device),
+                   torch.empty((S, num_negatives), dtype=torch.int32, device=walks.device))
+        c, x, ng = out
+        if stream is None:
+            stream = torch.cuda.current_stream(g.device).cuda_stream
+        elif isinstance(stream, torch.cuda.Stream):
+            stream = stream.cuda_stream
+        rc = _lib.grape_skipgram_pairs(g.handle, walks.data_ptr(), W, walk_id_base, L, window, num_negatives,
+                                       seed, c.data_ptr(), x.data_ptr(), ng.data_ptr() if num_negatives else None,
+                                       ctypes.c_void_p(stream))
+    _capi.check(_lib, rc, "grape_skipgram_pairs")
+    return c, x, ng
+
+
 def walks_approx(g: Graph, starts, L: int, degree_threshold: int, *, node2vec: bool = True, p: float = 1.0,
                  q: float = 1.0, seed: int = 42, walk_id_base: int = 0, out=None, steps=None,
                  stream=None) -> torch.Tensor:

@@ -22,6 +22,7 @@ GRAPE_PAD = 0xFFFFFFFF
 EXPORTS = (
     "grape_graph_from_csr", "grape_graph_from_csr_opts", "grape_graph_free", "grape_graph_get_info",
     "grape_walks_first_order", "grape_walks_node2vec", "grape_walks_approx", "grape_walks_node2vec_cdf", "grape_walks_node2vec_folded",
+    "grape_skipgram_pairs",
     "grape_walks_stats",
     "grape_walks_stats_ex",
     "grape_status_string", "grape_last_error", "grape_version",
@@ -104,6 +105,8 @@ def load(path: str | None = None) -> ctypes.CDLL:
     lib.grape_walks_node2vec_cdf.restype = i32
     lib.grape_walks_node2vec_folded.argtypes = [vp, vp, u64, u64, u32, dbl, dbl, u64, vp, vp, vp]
     lib.grape_walks_node2vec_folded.restype = i32
+    lib.grape_skipgram_pairs.argtypes = [vp, vp, u64, u64, u32, u32, u32, u64, vp, vp, vp, vp]
+    lib.grape_skipgram_pairs.restype = i32
     lib.grape_walks_stats.argtypes = [vp, vp, u64, u64, u32, i32, dbl, dbl, u64, vp,
                                       ctypes.POINTER(WalkStats), vp]
     lib.grape_walks_stats.restype = i32

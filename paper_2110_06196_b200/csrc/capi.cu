@@ -408,6 +408,47 @@ grape_status grape_walks_node2vec_folded(const grape_graph* g, const uint32_t* s
                         stream, 0, 2);
 }
 
+grape_status grape_skipgram_pairs(const grape_graph* g, const uint32_t* walks, uint64_t num_walks,
+                                  uint64_t walk_id_base, uint32_t walk_length, uint32_t window,
+                                  uint32_t num_negatives, uint64_t seed, uint32_t* centers, uint32_t* contexts,
+                                  uint32_t* negatives, cudaStream_t stream)
+{
+    g_err[0] = 0;
+    if (g == nullptr || (num_walks > 0 && (walks == nullptr || centers == nullptr || contexts == nullptr ||
+                                           (num_negatives > 0 && negatives == nullptr)))) {
+        set_error("graph, walks, centers, contexts (and negatives when num_negatives > 0) must be non-NULL");
+        return GRAPE_EINVAL;
+    }
+    if (walk_length == 0 || window == 0 || window > 1024 || num_negatives > 1024) {
+        set_error("need walk_length >= 1, 1 <= window <= 1024, num_negatives <= 1024");
+        return GRAPE_EINVAL;
+    }
+    const uint64_t slots_per_walk = (uint64_t)walk_length * 2 * window;
+    if (num_walks > (~0ull) / slots_per_walk / 4 / (num_negatives + 1) ||
+        (walk_id_base + num_walks) > (~0ull) / slots_per_walk) {
+        set_error("the slot count (num_walks * walk_length * 2 * window * (1 + num_negatives)) overflows");
+        return GRAPE_EINVAL;
+    }
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess) { cudaGetLastError(); cur = -1; }
+    if (cur != g->device) {
+        set_error("current device %d is not the graph's device %d", cur, g->device);
+        return GRAPE_EINVAL;
+    }
+    if (num_walks == 0) return GRAPE_OK;
+    if (classify(walks) != Mem::Device || classify(centers) != Mem::Device || classify(contexts) != Mem::Device ||
+        (num_negatives > 0 && classify(negatives) != Mem::Device)) {
+        set_error("grape_skipgram_pairs needs device buffers (walks, centers, contexts, negatives)");
+        return GRAPE_EINVAL;
+    }
+    cudaError_t e = ensure_node_guide(const_cast<grape_graph*>(g), stream);
+    if (e != cudaSuccess) return cuda_fail(e, "node guide for the negatives");
+    e = launch_skipgram(g, walks, num_walks, walk_id_base, walk_length, window, num_negatives, seed, centers,
+                        contexts, negatives, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "skipgram kernel launch");
+    return GRAPE_OK;
+}
+
 grape_status grape_walks_stats(const grape_graph* g, const uint32_t* starts, uint64_t num_walks,
                                uint64_t walk_id_base, uint32_t walk_length, int node2vec, double p,
                                double q, uint64_t seed, uint32_t* out, grape_walk_stats* stats,

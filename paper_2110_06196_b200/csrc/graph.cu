@@ -195,6 +195,7 @@ void destroy_graph(grape_graph* g)
     cudaFree(g->nodes);
     destroy_tables(g);
     cudaFree(g->stage_buf);
+    cudaFree(g->node_guide);
     for (int l = 0; l < kFenceLevels; ++l) {
         cudaFree(g->col_fence[l]);
         cudaFree(g->cw_fence[l]);

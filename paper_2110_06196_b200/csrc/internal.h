@@ -53,6 +53,11 @@ struct grape_graph {
     std::mutex stage_mu;
     void* stage_buf = nullptr;
     uint64_t stage_bytes = 0;
+    // SkipGram negatives (skipgram.cu): node guide over arc-index buckets of
+    // 2^node_guide_shift arcs, built on the first grape_skipgram_pairs call
+    std::mutex node_guide_mu;
+    uint32_t* node_guide = nullptr;
+    uint32_t node_guide_shift = 0;
     uint32_t max_degree;
     uint64_t max_row_weight;
     uint64_t device_bytes;
@@ -88,6 +93,11 @@ constexpr int kStatsWords = 16;
 cudaError_t launch_walks(const grape_graph* g, const WalkArgs& a, bool node2vec,
                          const Thresholds& T, cudaStream_t stream);
 cudaError_t launch_walks_cdf(const grape_graph* g, const WalkArgs& a, const Thresholds& T, cudaStream_t stream);
+// SkipGram consumer (skipgram.cu, §8(f) f3)
+cudaError_t ensure_node_guide(grape_graph* g, cudaStream_t stream);
+cudaError_t launch_skipgram(const grape_graph* g, const uint32_t* walks, uint64_t num_walks, uint64_t base,
+                            uint32_t L, uint32_t window, uint32_t K, uint64_t seed, uint32_t* centers,
+                            uint32_t* contexts, uint32_t* negs, cudaStream_t stream);
 cudaError_t launch_walks_tab(const grape_graph* g, const WalkArgs& a, bool node2vec,
                              const Thresholds& T, cudaStream_t stream);
 cudaError_t launch_walks_sm(const grape_graph* g, const WalkArgs& a, bool node2vec,

@@ -72,6 +72,16 @@ def test_argument_errors_before_any_cuda_call(lib):
         assert lib.grape_walks_node2vec(fake, buf, 1, 0, 4, p, q, 42, buf, None, None) == 1
     # overflow of num_walks * L
     assert lib.grape_walks_first_order(fake, buf, 2 ** 62, 0, 8, 42, buf, None, None) == 1
+    # SkipGram consumer: NULL graph / buffers, L = 0, window 0 / too large, slot-count overflow
+    assert lib.grape_skipgram_pairs(None, buf, 1, 0, 4, 2, 1, 42, buf, buf, buf, None) == 1
+    assert lib.grape_skipgram_pairs(fake, buf, 1, 0, 4, 2, 1, 42, buf, buf, None, None) == 1
+    assert b"non-NULL" in lib.grape_last_error()
+    assert lib.grape_skipgram_pairs(fake, buf, 1, 0, 4, 2, 0, 42, buf, buf, None, None) != 0   # K = 0: NULL negatives ok
+    assert lib.grape_skipgram_pairs(fake, buf, 1, 0, 0, 2, 1, 42, buf, buf, buf, None) == 1
+    assert lib.grape_skipgram_pairs(fake, buf, 1, 0, 4, 0, 1, 42, buf, buf, buf, None) == 1
+    assert lib.grape_skipgram_pairs(fake, buf, 1, 0, 4, 1025, 1, 42, buf, buf, buf, None) == 1
+    assert lib.grape_skipgram_pairs(fake, buf, 2 ** 58, 0, 64, 5, 5, 42, buf, buf, buf, None) == 1
+    assert b"overflows" in lib.grape_last_error()
     # graph build: NULL out, NULL arrays, n = PAD, unknown flags
     h = vp()
     assert lib.grape_graph_from_csr(3, 0, buf, buf, None, 0, 0, None) == 1
