@@ -290,7 +290,8 @@ grape_status grape_walks_node2vec_folded(const grape_graph* g, const uint32_t* s
  * Device buffers only; asynchronous on `stream` (the first call on a graph
  * builds its node guide, ~4 n bytes, synchronously).  Errors: EINVAL on NULL
  * buffers, host buffers, walk_length = 0, window = 0 or > 1024, num_negatives
- * > 1024, slot-count overflow, a device mismatch; ECUDA on launch failure.
+ * > 1024, walk_length * 2 * window * num_negatives >= 2^32, slot-count overflow,
+ * a device mismatch; ECUDA on launch failure.
  */
 grape_status grape_skipgram_pairs(const grape_graph* g, const uint32_t* walks, uint64_t num_walks,
                                   uint64_t walk_id_base, uint32_t walk_length, uint32_t window,

@@ -424,6 +424,10 @@ grape_status grape_skipgram_pairs(const grape_graph* g, const uint32_t* walks, u
         return GRAPE_EINVAL;
     }
     const uint64_t slots_per_walk = (uint64_t)walk_length * 2 * window;
+    if (slots_per_walk * (num_negatives > 0 ? num_negatives : 1) >= (1ull << 32)) {
+        set_error("walk_length * 2 * window * num_negatives must be < 2^32 (one row's output words)");
+        return GRAPE_EINVAL;
+    }
     if (num_walks > (~0ull) / slots_per_walk / 4 / (num_negatives + 1) ||
         (walk_id_base + num_walks) > (~0ull) / slots_per_walk) {
         set_error("the slot count (num_walks * walk_length * 2 * window * (1 + num_negatives)) overflows");

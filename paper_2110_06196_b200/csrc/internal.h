@@ -56,7 +56,7 @@ struct grape_graph {
     // SkipGram negatives (skipgram.cu): node guide over arc-index buckets of
     // 2^node_guide_shift arcs, built on the first grape_skipgram_pairs call
     std::mutex node_guide_mu;
-    uint32_t* node_guide = nullptr;
+    uint2* node_guide = nullptr;
     uint32_t node_guide_shift = 0;
     uint32_t max_degree;
     uint64_t max_row_weight;

@@ -5,14 +5,15 @@
 // whose row holds a uniform arc index — the rank the paper implements on its
 // Elias-Fano arrays.
 //
-// Rank on the device: a node guide over arc-index buckets of 2^sh arcs,
-// gidx[b] = rank(b << sh), built once per graph (lazily, on the first call);
-// rank(e) starts at gidx[e >> sh] and steps over rows that end at or before e
-// (one node per bucket on average, so ~1-2 reads of off[] per negative).
+// Rank on the device: a node guide over arc-index buckets of 2^sh arcs (about
+// two per node), entry b = {rank(b << sh), where that row ends relative to the
+// bucket}, built once per graph (lazily, on the first call).  A query reads its
+// bucket's entry and is done when e falls in that row — most arcs belong to rows
+// much longer than a bucket; otherwise it steps over the rows that end at or
+// before e in off[].
 //
-// One thread per output word: slots p (center + context) in the first loop,
-// (slot, k) pairs in the second, so every store of a warp is contiguous; the
-// walk rows are re-read from L2.
+// One block per walk row (staged in shared memory); its threads write the row's
+// slots, then its negatives, in order: every store of a warp is contiguous.
 #include <mutex>
 
 #include "internal.h"
@@ -34,74 +35,109 @@ __device__ __forceinline__ uint32_t rank_search(const uint64_t* __restrict__ off
     return lo;
 }
 
+// entry b = {v = rank(b << sh), min(off[v+1] - (b << sh), 2^32 - 1)}: a query whose
+// offset into the bucket is below the second word is answered by this one read
 __global__ void build_node_guide(const uint64_t* __restrict__ off, uint32_t n, uint32_t sh, uint64_t nb,
-                                 uint32_t* __restrict__ gidx)
+                                 uint2* __restrict__ gidx)
 {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += stride)
-        gidx[b] = rank_search(off, n, b << sh);
+    for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += stride) {
+        const uint32_t v = rank_search(off, n, b << sh);
+        const uint64_t rel = off[v + 1] - (b << sh);
+        gidx[b] = make_uint2(v, rel < 0xFFFFFFFFull ? (uint32_t)rel : 0xFFFFFFFFu);
+    }
 }
+
+// n / d for 32-bit n and a divisor fixed per launch (Granlund-Montgomery, round-up
+// multiplier): two multiplies instead of a division sequence
+struct FastDiv {
+    uint32_t d, m, s1;
+    static FastDiv of(uint32_t d_)
+    {
+        FastDiv f{d_, 0, 0};
+        if (d_ > 1) {
+            uint32_t l = 0;
+            while ((1ull << l) < d_) ++l;
+            f.m = (uint32_t)((((1ull << 32) * ((1ull << l) - d_)) / d_) + 1);
+            f.s1 = l - 1;
+        }
+        return f;
+    }
+    __device__ __forceinline__ uint32_t div(uint32_t n) const
+    {
+        if (d == 1) return n;
+        const uint32_t t = __umulhi(m, n);
+        return (t + ((n - t) >> 1)) >> s1;
+    }
+};
 
 struct SgParams {
     const uint64_t* off;
-    const uint32_t* gidx;
+    const uint2* gidx;
     uint32_t sh;
     uint64_t m;
     const uint32_t* walks;
     uint64_t num_walks;
     uint64_t base;
     uint32_t L, w, K;
+    FastDiv tw_div, k_div;   // by 2w and by K
     RoundKeys rk;
     uint32_t* centers;
     uint32_t* contexts;
     uint32_t* negs;
 };
 
-// slot p (local) -> row r, position i, offset j; valid iff both ends are live
-__device__ __forceinline__ bool slot_of(const SgParams& P, uint64_t p, uint64_t& r, uint32_t& i, uint32_t& o,
-                                        uint32_t& a, uint32_t& b)
-{
-    const uint64_t per_row = (uint64_t)P.L * 2 * P.w;
-    r = p / per_row;
-    const uint32_t rem = (uint32_t)(p - r * per_row);
-    i = rem / (2 * P.w);
-    o = rem - i * 2 * P.w;
-    const int64_t j = o < P.w ? (int64_t)o - P.w : (int64_t)o - P.w + 1;
-    const int64_t c = (int64_t)i + j;
-    const uint32_t* row = P.walks + r * P.L;
-    if (c < 0 || c >= (int64_t)P.L) return false;
-    a = __ldg(row + i);
-    b = __ldg(row + c);
-    return a != kPadSg && b != kPadSg;
-}
+constexpr uint32_t kRowSmemWords = 12288;   // walk rows up to 48 KB are staged in shared memory
 
+// One block per walk row at a time (grid-stride over rows): the row is staged in
+// shared memory, then the block's threads cover the row's L*2w slots and its
+// L*2w*K negative words in order, so every store of a warp is contiguous and no
+// 64-bit division is needed (32-bit index arithmetic within a row).
 __global__ void __launch_bounds__(256) skipgram_kernel(const __grid_constant__ SgParams P)
 {
-    const uint64_t S = P.num_walks * P.L * 2 * P.w;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    for (uint64_t p = t0; p < S; p += stride) {
-        uint64_t r;
-        uint32_t i, o, a = 0, b = 0;
-        const bool ok = slot_of(P, p, r, i, o, a, b);
-        P.centers[p] = ok ? a : kPadSg;
-        P.contexts[p] = ok ? b : kPadSg;
-    }
-    const uint64_t SK = S * P.K;
-    for (uint64_t q = t0; q < SK; q += stride) {
-        const uint64_t p = q / P.K;
-        const uint32_t k = (uint32_t)(q - p * P.K);
-        uint64_t r;
-        uint32_t i, o, a = 0, b = 0;
-        uint32_t v = kPadSg;
-        if (slot_of(P, p, r, i, o, a, b) && P.m != 0) {
-            const uint64_t slot = ((P.base + r) * P.L + i) * (uint64_t)(2 * P.w) + o;   // global slot id
-            const Draw d = philox_draw_rk(P.rk, slot, 0xFFFFFFFFu, k);
-            const uint64_t e = __umul64hi(d.x64, P.m);                                   // BOUNDED(x64, m)
-            v = __ldg(P.gidx + (e >> P.sh));
-            while (__ldg(P.off + v + 1) <= e) ++v;                                       // rows ending before e
+    extern __shared__ uint32_t srow[];
+    const uint32_t L = P.L, tw = 2 * P.w, K = P.K;
+    const uint32_t per_row = L * tw;
+    const bool staged = L <= kRowSmemWords;
+    for (uint64_t r = blockIdx.x; r < P.num_walks; r += gridDim.x) {
+        const uint32_t* grow = P.walks + r * L;
+        __syncthreads();   // the previous row's readers are done
+        if (staged)
+            for (uint32_t q = threadIdx.x; q < L; q += blockDim.x) srow[q] = __ldg(grow + q);
+        __syncthreads();
+        const uint32_t* row = staged ? srow : grow;
+        auto ends = [&](uint32_t idx, uint32_t& a, uint32_t& b) {   // slot idx of this row: valid?
+            const uint32_t i = P.tw_div.div(idx), o = idx - i * tw;
+            const int32_t c = (int32_t)i + (o < P.w ? (int32_t)o - (int32_t)P.w : (int32_t)o - (int32_t)P.w + 1);
+            if (c < 0 || c >= (int32_t)L) return false;
+            a = row[i];
+            b = row[c];
+            return a != kPadSg && b != kPadSg;
+        };
+        const uint64_t o0 = r * per_row;                        // local slot offset of the row
+        const uint64_t g0 = (P.base + r) * per_row;             // global slot id of its first slot
+        for (uint32_t idx = threadIdx.x; idx < per_row; idx += blockDim.x) {
+            uint32_t a = 0, b = 0;
+            const bool ok = ends(idx, a, b);
+            P.centers[o0 + idx] = ok ? a : kPadSg;
+            P.contexts[o0 + idx] = ok ? b : kPadSg;
         }
-        P.negs[q] = v;
+        const uint32_t nk = per_row * K;
+        for (uint32_t idx = threadIdx.x; idx < nk; idx += blockDim.x) {
+            const uint32_t sl = P.k_div.div(idx), k = idx - sl * K;
+            uint32_t a = 0, b = 0, v = kPadSg;
+            if (ends(sl, a, b) && P.m != 0) {
+                const Draw d = philox_draw_rk(P.rk, g0 + sl, 0xFFFFFFFFu, k);
+                const uint64_t e = __umul64hi(d.x64, P.m);          // BOUNDED(x64, m)
+                const uint2 ge = __ldg(P.gidx + (e >> P.sh));
+                v = ge.x;
+                if (e - ((e >> P.sh) << P.sh) >= ge.y) {             // past the bucket's first row
+                    ++v;
+                    while (__ldg(P.off + v + 1) <= e) ++v;           // rows ending at or before e
+                }
+            }
+            P.negs[o0 * K + idx] = v;
+        }
     }
 }
 
@@ -112,10 +148,10 @@ cudaError_t ensure_node_guide(grape_graph* g, cudaStream_t stream)
     std::lock_guard<std::mutex> lk(g->node_guide_mu);
     if (g->node_guide != nullptr || g->m == 0) return cudaSuccess;
     uint32_t sh = 0;
-    while ((g->m >> sh) + 1 > (uint64_t)g->n) ++sh;   // about one bucket per node
+    while ((g->m >> sh) + 1 > 2 * (uint64_t)g->n) ++sh;   // about two buckets per node (16 B per node)
     const uint64_t nb = (g->m >> sh) + 1;
-    uint32_t* gidx = nullptr;
-    cudaError_t e = cudaMalloc(&gidx, nb * 4);
+    uint2* gidx = nullptr;
+    cudaError_t e = cudaMalloc(&gidx, nb * sizeof(uint2));
     if (e != cudaSuccess) return e;
     const unsigned blocks = (unsigned)((nb + 255) / 256 < 4096 ? (nb + 255) / 256 : 4096);
     build_node_guide<<<blocks, 256, 0, stream>>>(g->off, g->n, sh, nb, gidx);
@@ -145,6 +181,8 @@ cudaError_t launch_skipgram(const grape_graph* g, const uint32_t* walks, uint64_
     P.L = L;
     P.w = window;
     P.K = K;
+    P.tw_div = FastDiv::of(2 * window);
+    P.k_div = FastDiv::of(K > 0 ? K : 1);
     P.rk = philox_round_keys(seed);
     P.centers = centers;
     P.contexts = contexts;
@@ -155,11 +193,11 @@ cudaError_t launch_skipgram(const grape_graph* g, const uint32_t* walks, uint64_
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    const uint64_t work = num_walks * L * 2 * window * (K > 0 ? K : 1);
-    uint64_t blocks = (work + 255) / 256;
-    const uint64_t cap = (uint64_t)sms * 8;   // 8 resident blocks of 256 per SM, grid-stride
+    uint64_t blocks = num_walks;
+    const uint64_t cap = (uint64_t)sms * 8;   // 8 resident blocks of 256 per SM, grid-stride over rows
     if (blocks > cap) blocks = cap;
-    skipgram_kernel<<<(unsigned)blocks, 256, 0, stream>>>(P);
+    const size_t smem = L <= kRowSmemWords ? (size_t)L * 4 : 0;
+    skipgram_kernel<<<(unsigned)blocks, 256, smem, stream>>>(P);
     return cudaGetLastError();
 }
 
