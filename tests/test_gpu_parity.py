@@ -96,6 +96,30 @@ def test_fuzz_graphs_every_walk(grape, seed, n, dens, directed, weighted, mode, 
             assert steps == esteps
 
 
+@pytest.mark.parametrize("L,base", [(3001, 2 ** 32 - 7), (70000, 11), (6, 2 ** 64 - 200), (40, 2 ** 48 + 3)])
+def test_long_walks_and_wide_walk_ids(grape, L, base):
+    """Rows longer than any staging unit, and walk ids whose counter word 1 is
+    non-zero (crossing 2^32) or near 2^64: every walk bit-exact, default and folded
+    rules, and the SkipGram slots of those rows."""
+    g = tiny_graph(4242, 60, 0.08, weighted=True)
+    o = _oracle(g)
+    starts = np.concatenate([np.arange(g.n), [g.n + 5]]).astype(np.uint32)[: (3 if L > 10000 else 200)]
+    dg = _dev_graph(grape, g)
+    for mode, p, q in (("node2vec", 0.5, 2.0), ("first_order", 1, 1)):
+        exp, esteps = o.walks(starts, L, mode=mode, p=p, q=q, seed=5, base=base)
+        got, steps = _run(grape, dg, starts, L, mode, p, q, 5, base=base)
+        assert np.array_equal(got, exp) and steps == esteps, mode
+    st = torch.as_tensor(starts.view(np.int32)).cuda()
+    fo = grape.walks_node2vec_folded(dg, st, L, 0.25, 4.0, seed=5, walk_id_base=base)
+    efo, _ = o.walks_folded(starts, L, p=0.25, q=4.0, seed=5, base=base)
+    assert np.array_equal(fo.cpu().numpy().view(np.uint32), efo)
+    if L * len(starts) <= 200 * 3001 and base < 2 ** 63:
+        c, x, ng = grape.skipgram_pairs(dg, fo[:2], 3, 2, seed=1, walk_id_base=base)
+        ec, ex, eng = o.skipgram(efo[:2], 3, 2, seed=1, base=base)
+        assert np.array_equal(c.cpu().numpy().view(np.uint32), ec)
+        assert np.array_equal(ng.cpu().numpy().view(np.uint32), eng)
+
+
 def test_u64_prefix_path(grape):
     """Row sums >= 2^32 force the u64 prefix layout; results stay bit-exact."""
     g = tiny_graph(5, 40, 0.5, weighted=True)
