@@ -147,15 +147,35 @@ grape_status walks_host(const grape_graph* g, const WalkArgs& a, bool n2v, const
         cudaGetLastError();   // clear the allocation failure and retry smaller
         chunk_mb /= 2;
     }
+    const bool single = nchunks == 1;   // one chunk: everything on the caller's stream, nothing to overlap
     for (int b = 0; b < nbuf && e == cudaSuccess; ++b) {
         d_starts[b] = (uint32_t*)(base + b * per);
         d_out[b] = (uint32_t*)(base + b * per + ((chunk * 4 + 255) & ~255ull));
+        if (single) continue;
         e = cudaEventCreateWithFlags(&ev_kernel[b], cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_copied[b], cudaEventDisableTiming);
     }
     if (e == cudaSuccess) d_steps = (unsigned long long*)(base + per * nbuf);
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    if (e == cudaSuccess && !single) e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaMemsetAsync(d_steps, 0, 8, stream);
+    if (e == cudaSuccess && single) {
+        WalkArgs c = a;
+        c.starts = d_starts[0];
+        c.out = d_out[0];
+        c.steps_out = d_steps;
+        unsigned long long steps = 0;
+        e = cudaMemcpyAsync(d_starts[0], a.starts, a.num_walks * 4, cudaMemcpyHostToDevice, stream);
+        if (e == cudaSuccess) e = launch_walks(g, c, n2v, T, stream);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(a.out, d_out[0], a.num_walks * L * 4, cudaMemcpyDeviceToHost, stream);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&steps, d_steps, 8, cudaMemcpyDeviceToHost, stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+        if (e != cudaSuccess) st = cuda_fail(e, "host-buffer walks");
+        else if (steps_host) *steps_host += steps;
+        cudaStreamSynchronize(stream);
+        if (own) cudaFree(base);
+        return st;
+    }
     if (e != cudaSuccess) {
         st = cuda_fail(e, "host-buffer staging setup");
     } else {
