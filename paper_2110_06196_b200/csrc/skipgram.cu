@@ -187,12 +187,12 @@ cudaError_t launch_skipgram(const grape_graph* g, const uint32_t* walks, uint64_
     P.centers = centers;
     P.contexts = contexts;
     P.negs = negs;
-    static int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
+    static const int sms = [] {   // thread-safe static init
+        int dev = 0, n = 0;
         cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        return n > 0 ? n : 1;
+    }();
     uint64_t blocks = num_walks;
     const uint64_t cap = (uint64_t)sms * 8;   // 8 resident blocks of 256 per SM, grid-stride over rows
     if (blocks > cap) blocks = cap;
