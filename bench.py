@@ -60,6 +60,9 @@ class ClockSampler:
                 text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi's NVML start-up perturbs the GPU for ~1 ms: let it settle so the
+            # first timed step is not charged for it (sampling continues through the region)
+            time.sleep(0.3)
         except Exception:
             self.proc = None
         return self
@@ -432,6 +435,7 @@ def run_ours(args):
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32/u64 integer",
                 "data": "synthetic (seeded generator, graphgen/)", "config": _workload_desc(k, g, wk, W, flush),
                 "gpu_launches": args.steps, "realised_steps_per_gpu_step": steps_per_launch,
+                "step_ms": [round(x, 3) for x in kernel_ms],
                 "nominal_steps_per_gpu_step": W * (L - 1), "wall_s_timed": t_wall,
                 "clocks": clocks, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "graph_device_bytes": info["device_bytes"],
