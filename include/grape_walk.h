@@ -282,8 +282,9 @@ grape_status grape_walks_node2vec_folded(const grape_graph* g, const uint32_t* s
  *                  and both entries are not PAD, else (PAD, PAD)
  *   negatives      device u32[S][num_negatives] (may be NULL if 0): for a valid
  *                  slot, negative k = rank(floor(x64 * m / 2^64)), x64 = words
- *                  o1:o0 of Philox4x32-10 with counter (P lo, P hi, 0xFFFFFFFF,
- *                  k), key = seed, P = ((walk_id_base + r) * L + i) * 2w + o the
+ *                  o1:o0 (k even) or o3:o2 (k odd) of Philox4x32-10 with counter
+ *                  (P lo, P hi, 0xFFFFFFFF, floor(k/2)), key = seed,
+ *                  P = ((walk_id_base + r) * L + i) * 2w + o the
  *                  global slot id (so shards reproduce slices of one call);
  *                  rank(e) = the v with off[v] <= e < off[v+1]; PAD for an
  *                  invalid slot or a graph without arcs.

@@ -724,8 +724,9 @@ uint32_t oracle_rank(uint32_t n, const uint64_t* off, uint64_t e)
  * offset o = 0 .. 2w-1 standing for j = -w .. -1, 1 .. w (f3-a):
  *   centers[p] = row[i], contexts[p] = row[i + j] if 0 <= i + j < L and both
  *   are not PAD; otherwise both PAD (f3-b);
- *   negs[p * K + k] = rank(BOUNDED(x64(DRAW(seed, P, 0xFFFFFFFF, k)), m)) for
- *   a valid slot, P = its global slot index (wid * L + i) * 2w + o (f3-c);
+ *   negs[p * K + k] = rank(BOUNDED(x, m)) for a valid slot, x = words o1:o0
+ *   (k even) or o3:o2 (k odd) of DRAW(seed, P, 0xFFFFFFFF, floor(k / 2)),
+ *   P = its global slot index (wid * L + i) * 2w + o (f3-c);
  *   PAD for an invalid slot, or when m = 0.
  * Returns 0. */
 int oracle_skipgram(uint32_t n, const uint64_t* off, const uint32_t* walks, uint64_t num_walks,
@@ -751,8 +752,13 @@ int oracle_skipgram(uint32_t n, const uint64_t* off, const uint32_t* walks, uint
                         negs[p * K + k] = ORACLE_PAD;
                         continue;
                     }
-                    oracle_draw(seed, P, 0xFFFFFFFFu, k, d);
-                    negs[p * K + k] = oracle_rank(n, off, oracle_bounded(x64_of(d), m));
+                    /* one Philox block per two negatives (f3-c): words o1:o0 for even k,
+                     * o3:o2 for odd k */
+                    oracle_draw(seed, P, 0xFFFFFFFFu, k / 2, d);
+                    {
+                        const uint64_t x64 = (k & 1) ? ((uint64_t)d[3] << 32 | d[2]) : x64_of(d);
+                        negs[p * K + k] = oracle_rank(n, off, oracle_bounded(x64, m));
+                    }
                 }
             }
         }

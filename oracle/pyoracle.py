@@ -285,8 +285,8 @@ def skipgram(g: PyGraph, walks, window, K, seed=42, base=0):
                     if not ok or m == 0:
                         ks.append(PAD)
                         continue
-                    d = draw(seed, slot, 0xFFFFFFFF, k)
-                    e = bounded(d[1] << 32 | d[0], m)
+                    d = draw(seed, slot, 0xFFFFFFFF, k // 2)      # two negatives per block
+                    e = bounded((d[3] << 32 | d[2]) if k % 2 else (d[1] << 32 | d[0]), m)
                     ks.append(bisect.bisect_right(g.off, e) - 1)   # the row holding arc e
                 negs.append(ks)
     return centers, contexts, negs

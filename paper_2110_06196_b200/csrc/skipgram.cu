@@ -80,7 +80,7 @@ struct SgParams {
     uint64_t num_walks;
     uint64_t base;
     uint32_t L, w, K;
-    FastDiv tw_div, k_div;   // by 2w and by K
+    FastDiv tw_div, k_div;   // by 2w and by ceil(K / 2)
     RoundKeys rk;
     uint32_t* centers;
     uint32_t* contexts;
@@ -122,21 +122,32 @@ __global__ void __launch_bounds__(256) skipgram_kernel(const __grid_constant__ S
             P.centers[o0 + idx] = ok ? a : kPadSg;
             P.contexts[o0 + idx] = ok ? b : kPadSg;
         }
-        const uint32_t nk = per_row * K;
-        for (uint32_t idx = threadIdx.x; idx < nk; idx += blockDim.x) {
-            const uint32_t sl = P.k_div.div(idx), k = idx - sl * K;
-            uint32_t a = 0, b = 0, v = kPadSg;
-            if (ends(sl, a, b) && P.m != 0) {
-                const Draw d = philox_draw_rk(P.rk, g0 + sl, 0xFFFFFFFFu, k);
-                const uint64_t e = __umul64hi(d.x64, P.m);          // BOUNDED(x64, m)
-                const uint2 ge = __ldg(P.gidx + (e >> P.sh));
-                v = ge.x;
-                if (e - ((e >> P.sh) << P.sh) >= ge.y) {             // past the bucket's first row
-                    ++v;
-                    while (__ldg(P.off + v + 1) <= e) ++v;           // rows ending at or before e
-                }
+        // negatives 2kk and 2kk+1 of a slot come from one Philox block (words o1:o0 and
+        // o3:o2): one thread per block, its two words stored side by side
+        const uint32_t Kh = (K + 1) / 2;
+        const uint32_t nk = per_row * Kh;
+        auto rank = [&](uint64_t x64) {
+            const uint64_t e = __umul64hi(x64, P.m);                 // BOUNDED(x64, m)
+            const uint2 ge = __ldg(P.gidx + (e >> P.sh));
+            uint32_t v = ge.x;
+            if (e - ((e >> P.sh) << P.sh) >= ge.y) {                 // past the bucket's first row
+                ++v;
+                while (__ldg(P.off + v + 1) <= e) ++v;               // rows ending at or before e
             }
-            P.negs[o0 * K + idx] = v;
+            return v;
+        };
+        for (uint32_t idx = threadIdx.x; idx < nk; idx += blockDim.x) {
+            const uint32_t sl = P.k_div.div(idx), kk = idx - sl * Kh;
+            const uint32_t k0 = 2 * kk;
+            uint32_t a = 0, b = 0, v0 = kPadSg, v1 = kPadSg;
+            if (ends(sl, a, b) && P.m != 0) {
+                const uint4 o = philox_block_rk(P.rk, g0 + sl, 0xFFFFFFFFu, kk);
+                v0 = rank((uint64_t)o.y << 32 | o.x);
+                if (k0 + 1 < K) v1 = rank((uint64_t)o.w << 32 | o.z);
+            }
+            uint32_t* dst = P.negs + (o0 + sl) * K + k0;
+            dst[0] = v0;
+            if (k0 + 1 < K) dst[1] = v1;
         }
     }
 }
@@ -182,7 +193,7 @@ cudaError_t launch_skipgram(const grape_graph* g, const uint32_t* walks, uint64_
     P.w = window;
     P.K = K;
     P.tw_div = FastDiv::of(2 * window);
-    P.k_div = FastDiv::of(K > 0 ? K : 1);
+    P.k_div = FastDiv::of(K > 1 ? (K + 1) / 2 : 1);   // by ceil(K / 2): Philox blocks per slot
     P.rk = philox_round_keys(seed);
     P.centers = centers;
     P.contexts = contexts;
