@@ -45,7 +45,7 @@ class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_power_cap,clocks.mem,temperature.gpu,temperature.memory")
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
@@ -60,8 +60,12 @@ class ClockSampler:
                 text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
-            # nvidia-smi's NVML start-up perturbs the GPU for ~1 ms: let it settle so the
-            # first timed step is not charged for it (sampling continues through the region)
+            # nvidia-smi's NVML start-up can stall the GPU (measured: one launch of a timed
+            # region took 214 ms instead of 47): wait for its first sample, i.e. until it is
+            # up and polling, before the timed region starts
+            t0 = time.perf_counter()
+            while not self.lines and time.perf_counter() - t0 < 10.0:
+                time.sleep(0.02)
             time.sleep(0.3)
         except Exception:
             self.proc = None
@@ -81,7 +85,7 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], 0.0, set()
+        sm, mx, reasons, mem, tg, tm = [], 0.0, set(), [], [], []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
@@ -95,10 +99,16 @@ class ClockSampler:
             for nm, val in zip(names, parts[3:7]):
                 if val.lower() == "active":
                     reasons.add(nm)
+            for lst, k in ((mem, 7), (tg, 8), (tm, 9)):
+                try:
+                    lst.append(float(parts[k]))
+                except (ValueError, IndexError):
+                    pass
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        med = lambda v: float(np.median(v)) if v else None
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "mem_mhz": med(mem), "gpu_temp_c": med(tg), "mem_temp_c": med(tm)}
 
 
 def _dist_setup(args):
