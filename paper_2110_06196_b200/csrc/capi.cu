@@ -448,8 +448,9 @@ grape_status grape_skipgram_pairs(const grape_graph* g, const uint32_t* walks, u
         set_error("walk_length * 2 * window * num_negatives must be < 2^32 (one row's output words)");
         return GRAPE_EINVAL;
     }
-    if (num_walks > (~0ull) / slots_per_walk / 4 / (num_negatives + 1) ||
-        (walk_id_base + num_walks) > (~0ull) / slots_per_walk) {
+    const uint64_t max_wid = (~0ull) / slots_per_walk;   // global slot ids must fit 64 bits
+    if (num_walks > (~0ull) / slots_per_walk / 4 / (num_negatives + 1) || num_walks > max_wid ||
+        walk_id_base > max_wid - num_walks) {
         set_error("the slot count (num_walks * walk_length * 2 * window * (1 + num_negatives)) overflows");
         return GRAPE_EINVAL;
     }

@@ -82,6 +82,8 @@ def test_argument_errors_before_any_cuda_call(lib):
     assert lib.grape_skipgram_pairs(fake, buf, 1, 0, 4, 1025, 1, 42, buf, buf, buf, None) == 1
     assert lib.grape_skipgram_pairs(fake, buf, 2 ** 58, 0, 64, 5, 5, 42, buf, buf, buf, None) == 1
     assert b"overflows" in lib.grape_last_error()
+    assert lib.grape_skipgram_pairs(fake, buf, 4, 2 ** 64 - 2, 4, 2, 1, 42, buf, buf, buf, None) == 1   # wid wrap
+    assert b"overflows" in lib.grape_last_error()
     # graph build: NULL out, NULL arrays, n = PAD, unknown flags
     h = vp()
     assert lib.grape_graph_from_csr(3, 0, buf, buf, None, 0, 0, None) == 1
