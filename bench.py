@@ -311,6 +311,11 @@ def run_ours(args):
     flush = _needs_flush(g, W, L)
     scrub = torch.empty(FLUSH_BYTES // 4, dtype=torch.int32, device=dev) if flush else None
     with ClockSampler(local) as clk:
+        # ~100 ms of GPU spin queued ahead of the first start event: the host enqueues the
+        # timed launches while the GPU is busy, so a host-side pause (measured: sporadic
+        # 20-170 ms pauses of the host on these boxes) cannot open an idle gap between a
+        # start event and its launch — the events measure the kernels, not the host
+        torch.cuda._sleep(int(0.1 * 1.9e9))
         t_wall = time.perf_counter()
         for i in range(args.steps):
             if flush:
@@ -337,6 +342,8 @@ def run_ours(args):
         h_starts = starts.cpu().pin_memory()
         h_out = torch.empty((W, L), dtype=torch.int32, pin_memory=True)
         h_steps = torch.zeros(1, dtype=torch.int64)
+        time.sleep(1.0)            # the clock sampler's nvidia-smi has just exited (its NVML teardown)
+        call(h_starts, h_out, None)
         call(h_starts, h_out, None)
         if world > 1:
             dist.barrier()
@@ -506,6 +513,7 @@ def run_skipgram(args):
     if world > 1:
         dist.barrier()
     with ClockSampler(local) as clk:
+        torch.cuda._sleep(int(0.1 * 1.9e9))   # GPU busy while the timed steps are enqueued (as run_ours)
         for e in evs:
             e[0].record()
             walk(ctr)
