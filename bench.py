@@ -360,8 +360,10 @@ def run_ours(args):
         e2e_tot = _allreduce(float(h_steps.item()), dist.ReduceOp.SUM, world)
         e2e = {"value": e2e_tot / e2e_s, "unit": "steps/s", "h2d_bytes_per_step": int(W * 4),
                "d2h_bytes_per_step": int(W * L * 4 + 8), "steps_timed": e2e_steps,
-               "path": ("grape_walks_approx" if dT else "grape_walks_node2vec" if node2vec else
-                        "grape_walks_first_order") +
+               "path": ("grape_walks_approx" if dT else
+                        ("grape_walks_node2vec_cdf" if args.sampler == "cdf" else
+                         "grape_walks_node2vec_folded" if args.sampler == "folded" else
+                         "grape_walks_node2vec") if node2vec else "grape_walks_first_order") +
                        " with pinned host starts/out (library-staged, chunked H2D/kernel/D2H)"}
 
     # ---- CPU oracle baseline (rank 0, N = 1 only)
@@ -438,6 +440,36 @@ def run_ours(args):
                                   "ceiling_per_s": ceil,
                                   "frac": (rand_sectors / t_launch / ceil) if ceil else None,
                                   "ceiling_source": ceil_src}}
+    if rank == 0 and args.sampler == "cdf" and node2vec:
+        # The CDF sampler has no counting build: its compulsory reads follow from the walks
+        # themselves.  Step s >= 2 at v reads v's whole row of arc records (pass 1; pass 2
+        # rescans one chunk of <= 32 records from L1/L2); the first step reads one record
+        # and one guide entry or record.  Membership probes are not counted (a lower bound).
+        deg = torch.diff(g.off.to(dev)).to(torch.int64)
+        rb = int(info.get("record_bytes") or 32)
+        row_bytes, first = 0.0, 0.0
+        for r0 in range(0, W, 1 << 20):                      # row chunks: bounded temporaries
+            blk = out[r0:r0 + (1 << 20)]
+            vs = blk[:, 1:L - 1]                             # v of every step s >= 2
+            live = (vs != -1) & (blk[:, 2:L] != -1)
+            row_bytes += float((deg[vs[live].long()] * rb).sum().item())
+            first += float((blk[:, 1] != -1).sum().item()) * 64
+        alg_bytes = row_bytes + first + 4 * W * L + 4 * W
+        t_launch = avg_launch_ms / 1e3
+        peak, peak_src = _peaks()
+        tfile = os.path.join(ROOT, "profiles", f"traffic_cfg{k}_cdf.json")
+        traffic = json.load(open(tfile))["dram_bytes_per_launch"] if os.path.exists(tfile) else None
+        roof = {"bound": "hbm", "achieved": alg_bytes / t_launch / 1e9, "peak": peak, "unit": "GB/s",
+                "frac": alg_bytes / t_launch / 1e9 / peak, "traffic": traffic,
+                "dram_gbs": (traffic / t_launch / 1e9) if traffic else None,
+                "dram_frac": (traffic / t_launch / 1e9 / peak) if traffic else None,
+                "kernel": "walk_cdf_kernel (grape_walks_node2vec_cdf)", "peak_source": peak_src,
+                "avg_launch_ms": avg_launch_ms, "algorithmic_bytes_per_launch": alg_bytes,
+                "bytes_per_step": alg_bytes / max(steps_per_launch, 1),
+                "note": "bytes the paper's O(deg v) step touches, from the walk matrix: v's full row of "
+                        "records per node2vec step, membership probes not counted; hub rows are largely "
+                        "L2-resident, so DRAM traffic (dram_gbs) is below this"}
+        del deg
     clocks = clk.summary()
     if rank == 0:
         metric = "random-walk steps/sec (node2vec 2nd-order)" if node2vec else "random-walk steps/sec (first-order)"

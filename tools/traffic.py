@@ -1,6 +1,7 @@
 #!/usr/bin/env python
 """Write profiles/traffic_cfgK.json (DRAM bytes per launch of the walk kernel) from
-an ncu report of one timed launch:  tools/traffic.py REP K [mode]"""
+an ncu report of one timed launch:  tools/traffic.py REP K [mode [sampler]]
+(sampler cdf: profiles/traffic_cfgK_cdf.json, read by bench.py --sampler cdf)"""
 import csv, io, json, subprocess, sys
 rep, k = sys.argv[1], int(sys.argv[2])
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
@@ -19,5 +20,8 @@ kern = vals[col["Kernel Name"]]
 mode = sys.argv[3] if len(sys.argv) > 3 else "node2vec"
 out = {"dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr, "kernel": kern,
        "source": rep.split("/")[-1], "mode": mode}
-json.dump(out, open(f"profiles/traffic_cfg{k}.json", "w"), indent=1)
+sampler = sys.argv[4] if len(sys.argv) > 4 else "rejection"
+if sampler != "rejection":
+    out["sampler"] = sampler
+json.dump(out, open(f"profiles/traffic_cfg{k}{'' if sampler == 'rejection' else '_' + sampler}.json", "w"), indent=1)
 print(json.dumps(out))
