@@ -338,9 +338,17 @@ def run_ours(args):
 
     # ---- e2e: same metric through the C-ABI with HOST buffers (pinned), H2D/D2H inside
     e2e = None
+    h_out = None
     if not args.no_e2e:
         h_starts = starts.cpu().pin_memory()
-        h_out = torch.empty((W, L), dtype=torch.int32, pin_memory=True)
+        try:   # W*L*4 bytes of pinned host memory per rank (34 GB on configs[4])
+            h_out = torch.empty((W, L), dtype=torch.int32, pin_memory=True)
+        except RuntimeError as ex:
+            e2e = {"unavailable": f"pinned host buffer of {W * L * 4 / 1e9:.1f} GB: {str(ex)[:120]}"}
+        if _allreduce(1.0 if h_out is not None else 0.0, dist.ReduceOp.MIN, world) < 1.0:
+            h_out = None   # every rank skips together (no half-entered collective)
+            e2e = e2e or {"unavailable": "a rank could not pin its host buffer"}
+    if h_out is not None:
         h_steps = torch.zeros(1, dtype=torch.int64)
         time.sleep(1.0)            # the clock sampler's nvidia-smi has just exited (its NVML teardown)
         call(h_starts, h_out, None)
