@@ -273,6 +273,8 @@ def run_ours(args):
                               layout=_parse_layout(args.layout))
     g = g.to("cpu")            # the library holds its own copy; free the device CSR for the walk matrix
     torch.cuda.empty_cache()
+    if args.parts > 1:         # §8(f) f4 layout: tables in power-of-two parts (on this GPU)
+        dg.partition([local] * args.parts)
     info = dg.info
     W = g.n * wk["walks_per_node"]
     L = wk["L"]
@@ -487,6 +489,8 @@ def run_ours(args):
             metric = metric[:-1] + ", paper CDF sampler)"
         if args.sampler == "folded" and node2vec:
             metric = metric[:-1] + ", outlier-folded rejection)"
+        if args.parts > 1:
+            metric = metric[:-1] + f", tables in {args.parts} parts)"
         line = {"metric": metric, "value": value, "unit": "steps/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32/u64 integer",
@@ -498,7 +502,7 @@ def run_ours(args):
                 "graph_device_bytes": info["device_bytes"],
                 "graph_layout": {k_: info.get(k_) for k_ in ("tables", "record_bytes", "guide_bytes", "guide_factor",
                                                               "hash_h", "notri", "weights_symmetric",
-                                                              "table_bytes")}}
+                                                              "table_bytes", "parts")}}
         print(json.dumps(line), flush=True)
     dg.free()
     if world > 1:
@@ -626,6 +630,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--skipgram", type=int, default=0, metavar="B",
                     help="SkipGram consumer mode (§8(f) f3): B walks per step + their pairs / negatives")
+    ap.add_argument("--parts", type=int, default=1,
+                    help="split the tables into N parts (grape_graph_partition, §8(f) f4 layout) on this GPU")
     ap.add_argument("--window", type=int, default=5)
     ap.add_argument("--negatives", type=int, default=5)
     ap.add_argument("--no-tables", action="store_true", help="GRAPE_NO_TABLES: the v3 fenced-search walker")

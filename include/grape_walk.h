@@ -112,6 +112,7 @@ typedef struct {
     uint32_t record_bytes;    /* tables: bytes per arc record */
     uint32_t hash_h;          /* tables: arcs per edge-hash bucket (4 or 6) */
     uint32_t notri;           /* tables: records carry the no-common-neighbour flags */
+    uint32_t parts;           /* 1, or the number of parts after grape_graph_partition */
 } grape_graph_info;
 
 /*
@@ -264,6 +265,24 @@ grape_status grape_walks_node2vec_folded(const grape_graph* g, const uint32_t* s
                                          uint64_t walk_id_base, uint32_t walk_length, double p, double q,
                                          uint64_t seed, uint32_t* out, uint64_t* steps_out,
                                          cudaStream_t stream);
+
+/*
+ * grape_graph_partition — the §8(f) f4 table layout: split every
+ * sampling table of a built graph into `parts` power-of-two byte ranges, part j
+ * placed on device devices[j] (peer access from the graph's device is enabled;
+ * devices may repeat, e.g. all equal to the graph's device).  Walks then read each
+ * table entry from its part (over NVLink for a peer's part) and stay bit-identical
+ * to the unpartitioned graph.  Only the default rules run on a partitioned graph
+ * (grape_walks_first_order / _node2vec / _stats, grape_skipgram_pairs); the
+ * approximated, CDF and folded modes return EINVAL.  Synchronous.
+ *   parts     2 .. 8;   devices  host int[parts]
+ * Errors: EINVAL on a NULL graph / device list, parts out of range, a graph without
+ * tables or already partitioned, a device that does not exist or that the graph's
+ * device cannot access; ECUDA on allocation / copy failure (the graph is then
+ * unchanged).  This form partitions a graph built on one GPU; it does not build a
+ * graph larger than one GPU's memory.
+ */
+grape_status grape_graph_partition(grape_graph* g, uint32_t parts, const int* devices);
 
 /*
  * grape_skipgram_pairs — the SkipGram consumer of a walk matrix (SURVEY §8(f)

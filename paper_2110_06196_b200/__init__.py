@@ -69,6 +69,16 @@ class Graph:
     def num_arcs(self) -> int:
         return self.info["num_arcs"]
 
+    def partition(self, devices) -> "Graph":
+        """grape_graph_partition: split the sampling tables into len(devices) power-of-two
+        parts, part j on devices[j] (the §8(f) f4 layout; default walk rules only)."""
+        arr = (ctypes.c_int * len(devices))(*[int(d) for d in devices])
+        _capi.check(_lib, _lib.grape_graph_partition(self._h, len(devices), arr), "grape_graph_partition")
+        info = _capi.GraphInfo()
+        _capi.check(_lib, _lib.grape_graph_get_info(self._h, ctypes.byref(info)), "grape_graph_get_info")
+        self.info = {f: getattr(info, f) for f, _ in _capi.GraphInfo._fields_}
+        return self
+
     def free(self) -> None:
         if self._h is not None and self._h.value:
             _capi.check(_lib, _lib.grape_graph_free(self._h), "grape_graph_free")

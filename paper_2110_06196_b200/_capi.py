@@ -22,7 +22,7 @@ GRAPE_PAD = 0xFFFFFFFF
 EXPORTS = (
     "grape_graph_from_csr", "grape_graph_from_csr_opts", "grape_graph_free", "grape_graph_get_info",
     "grape_walks_first_order", "grape_walks_node2vec", "grape_walks_approx", "grape_walks_node2vec_cdf", "grape_walks_node2vec_folded",
-    "grape_skipgram_pairs",
+    "grape_skipgram_pairs", "grape_graph_partition",
     "grape_walks_stats",
     "grape_walks_stats_ex",
     "grape_status_string", "grape_last_error", "grape_version",
@@ -48,6 +48,7 @@ class GraphInfo(ctypes.Structure):
         ("record_bytes", ctypes.c_uint32),
         ("hash_h", ctypes.c_uint32),
         ("notri", ctypes.c_uint32),
+        ("parts", ctypes.c_uint32),
     ]
 
 
@@ -107,6 +108,8 @@ def load(path: str | None = None) -> ctypes.CDLL:
     lib.grape_walks_node2vec_folded.restype = i32
     lib.grape_skipgram_pairs.argtypes = [vp, vp, u64, u64, u32, u32, u32, u64, vp, vp, vp, vp]
     lib.grape_skipgram_pairs.restype = i32
+    lib.grape_graph_partition.argtypes = [vp, u32, vp]
+    lib.grape_graph_partition.restype = i32
     lib.grape_walks_stats.argtypes = [vp, vp, u64, u64, u32, i32, dbl, dbl, u64, vp,
                                       ctypes.POINTER(WalkStats), vp]
     lib.grape_walks_stats.restype = i32

@@ -253,6 +253,10 @@ grape_status walks_common(const grape_graph* g, const uint32_t* starts, uint64_t
                   "or outside their index ranges)");
         return GRAPE_EINVAL;
     }
+    if (g->parts > 1 && (dT != 0 || sampler != 0)) {
+        set_error("a partitioned graph (grape_graph_partition) serves the default walk rules only");
+        return GRAPE_EINVAL;
+    }
     int cur = -1;
     if (cudaGetDevice(&cur) != cudaSuccess) { cudaGetLastError(); cur = -1; }
     if (cur != g->device) {
@@ -383,6 +387,7 @@ grape_status grape_graph_get_info(const grape_graph* g, grape_graph_info* info)
     info->record_bytes = g->tables ? g->rec_bytes : 0;
     info->hash_h = g->hash_h;
     info->notri = g->notri ? 1u : 0u;
+    info->parts = g->parts;
     return GRAPE_OK;
 }
 
@@ -506,6 +511,10 @@ grape_status grape_walks_stats_ex(const grape_graph* g, const uint32_t* starts, 
     uint32_t dT = degree_threshold >= g->max_degree ? 0 : degree_threshold;
     if (dT != 0 && !g->tables) {
         set_error("approximated walks need the sampling tables");
+        return GRAPE_EINVAL;
+    }
+    if (g->parts > 1 && (dT != 0 || sampler != 0)) {
+        set_error("a partitioned graph (grape_graph_partition) serves the default walk rules only");
         return GRAPE_EINVAL;
     }
     if (sampler != 0 && (sampler != 2 || !g->tables || dT != 0 || !node2vec ||

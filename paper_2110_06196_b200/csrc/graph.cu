@@ -196,6 +196,13 @@ void destroy_graph(grape_graph* g)
     destroy_tables(g);
     cudaFree(g->stage_buf);
     cudaFree(g->node_guide);
+    cudaFree(g->part_map);
+    for (int t = 0; t < 4; ++t)   // partitioned tables (the contiguous pointers are NULL then)
+        for (int j = 0; j < (int)g->parts && g->parts > 1; ++j) {
+            bool dup = false;
+            for (int q = 0; q < j; ++q) dup |= g->part_mem[t][q] == g->part_mem[t][j];
+            if (!dup) cudaFree(g->part_mem[t][j]);
+        }
     for (int l = 0; l < kFenceLevels; ++l) {
         cudaFree(g->col_fence[l]);
         cudaFree(g->cw_fence[l]);

@@ -396,6 +396,9 @@ grape_status build_tables(grape_graph* g, const grape_table_options& o)
     const uint64_t rec_b = padded(m * c.rec), hash_b = padded(((m / c.H) + n + 1) * 32);
     const uint64_t guide_b = weighted ? padded((uint64_t)c.G * m * c.gb) : 0;
     const uint32_t G = c.G, gbytes = c.gb;
+    g->rec_alloc = rec_b;
+    g->guide_alloc = guide_b;
+    g->hash_alloc = hash_b;
     if ((e = cudaMalloc(&g->rec, rec_b)) != cudaSuccess) return fail(e, "cudaMalloc arc records");
     if (weighted && (e = cudaMalloc((void**)&g->guide, guide_b)) != cudaSuccess) return fail(e, "cudaMalloc guide");
     if ((e = cudaMalloc((void**)&g->ehash, hash_b)) != cudaSuccess) return fail(e, "cudaMalloc edge hash");

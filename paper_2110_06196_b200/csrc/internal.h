@@ -20,6 +20,13 @@ struct alignas(16) NodeRec {
     uint32_t deg;
     uint32_t w32;
 };
+
+// §8(f) f4 layout (partition.cu): table T (0 records, 1 guide, 2 node records,
+// 3 edge hash) in parts of 2^shift[T] bytes, part j at base[T][j]
+struct PartMap {
+    const char* base[4][8];
+    uint32_t shift[4];
+};
 }  // namespace grape
 
 struct grape_graph {
@@ -48,6 +55,14 @@ struct grape_graph {
     bool notri;              // records carry the no-common-neighbour flags (graph_tables.cu)
     uint32_t* ehash;      // per-row linear-probing sets of N(v): 2*deg(v) slots at 2*off[v]
     uint64_t table_bytes;
+    uint64_t rec_alloc = 0, guide_alloc = 0, hash_alloc = 0;   // table allocation bytes
+    // §8(f) f4 layout (partition.cu, grape_graph_partition): every table split into
+    // power-of-two parts, part j of table T at part_mem[T][j] (possibly on a peer GPU);
+    // T = 0 arc records, 1 guide, 2 node records, 3 edge hash
+    uint32_t parts = 1;
+    void* part_mem[4][8] = {};
+    uint32_t part_shift[4] = {63, 63, 63, 63};
+    grape::PartMap* part_map = nullptr;   // device copy of {part_mem, part_shift} for the walker
     // host-buffer staging (capi.cu walks_host): device buffers kept between calls;
     // a call that finds the mutex taken (a concurrent host-buffer call) allocates its own
     std::mutex stage_mu;

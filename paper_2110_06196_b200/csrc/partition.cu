@@ -1,0 +1,133 @@
+// partition.cu — the §8(f) f4 table layout: the sampling tables of
+// a built graph split into power-of-two byte ranges ("parts"), part j resident on
+// device devices[j] and read by the walker over NVLink peer access.  The walker's
+// single address computation resolves base[T][offset >> k] + (offset & (2^k - 1))
+// (walk_tab.cu, MODE 3), so every walk is the one the contiguous tables give.
+//
+// This first form partitions a graph that was built on one GPU (the build itself is
+// not distributed): it places the tables of a graph over several GPUs' memory and
+// measures the addressing; a graph larger than one HBM additionally needs the
+// build to write each part on its owner.
+#include "internal.h"
+
+namespace grape {
+namespace {
+
+struct Split {
+    void* mem[8] = {};
+    uint32_t shift = 63;
+};
+
+// copy table bytes at src (on the graph's device) into parts of 2^k bytes
+cudaError_t split(const grape_graph* g, const void* src, uint64_t bytes, uint32_t parts, const int* devices,
+                  Split& out)
+{
+    uint32_t k = 21;   // >= 2 MB parts
+    while ((1ull << k) * parts < bytes) ++k;
+    const uint64_t psz = 1ull << k;
+    out.shift = k;
+    cudaError_t e = cudaSuccess;
+    for (uint32_t j = 0; j < parts && e == cudaSuccess; ++j) {
+        const uint64_t lo = (uint64_t)j * psz;
+        const uint64_t len = lo >= bytes ? 0 : (bytes - lo < psz ? bytes - lo : psz);
+        if (len == 0) {   // past the end: never addressed; alias part 0
+            out.mem[j] = out.mem[0];
+            continue;
+        }
+        int prev = 0;
+        cudaGetDevice(&prev);
+        e = cudaSetDevice(devices[j]);
+        if (e == cudaSuccess) e = cudaMalloc(&out.mem[j], len);
+        cudaSetDevice(prev);
+        if (e == cudaSuccess) e = cudaMemcpyPeer(out.mem[j], devices[j], (const char*)src + lo, g->device, len);
+    }
+    return e;
+}
+
+void release(Split& s, uint32_t parts)
+{
+    for (uint32_t j = 0; j < parts; ++j) {
+        bool dup = false;
+        for (uint32_t q = 0; q < j; ++q) dup |= s.mem[q] == s.mem[j];
+        if (!dup && s.mem[j]) cudaFree(s.mem[j]);
+        s.mem[j] = nullptr;
+    }
+}
+
+}  // namespace
+}  // namespace grape
+
+using namespace grape;
+
+extern "C" grape_status grape_graph_partition(grape_graph* g, uint32_t parts, const int* devices)
+{
+    if (g == nullptr || parts < 2 || parts > 8 || devices == nullptr) {
+        set_error("grape_graph_partition: need a graph, 2 <= parts <= 8 and a device list");
+        return GRAPE_EINVAL;
+    }
+    if (!g->tables || g->parts != 1) {
+        set_error("grape_graph_partition: the graph has no sampling tables, or is already partitioned");
+        return GRAPE_EINVAL;
+    }
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+    for (uint32_t j = 0; j < parts; ++j) {
+        if (devices[j] < 0 || devices[j] >= ndev) {
+            set_error("grape_graph_partition: device %d does not exist", devices[j]);
+            return GRAPE_EINVAL;
+        }
+        if (devices[j] == g->device) continue;
+        int ok = 0;   // the walker on g->device reads part j over NVLink
+        cudaDeviceCanAccessPeer(&ok, g->device, devices[j]);
+        if (!ok) {
+            set_error("grape_graph_partition: device %d cannot access device %d", g->device, devices[j]);
+            return GRAPE_EINVAL;
+        }
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(g->device);
+        e = cudaDeviceEnablePeerAccess(devices[j], 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) e = cudaSuccess;
+        cudaGetLastError();
+        cudaSetDevice(prev);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+    }
+    e = cudaDeviceSynchronize();
+    // copy every table into its parts first; the graph changes only if all succeed
+    const void* src[4] = {g->rec, g->guide, g->nodes, g->ehash};
+    const uint64_t bytes[4] = {g->rec_alloc, g->guide ? g->guide_alloc : 0, (uint64_t)g->n * sizeof(NodeRec),
+                               g->hash_alloc};
+    Split sp[4];
+    for (int t = 0; t < 4 && e == cudaSuccess; ++t)
+        if (src[t] != nullptr && bytes[t] != 0) e = split(g, src[t], bytes[t], parts, devices, sp[t]);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    PartMap pm{};
+    for (int t = 0; t < 4; ++t) {
+        for (uint32_t j = 0; j < 8; ++j) pm.base[t][j] = (const char*)sp[t].mem[j < parts ? j : 0];
+        pm.shift[t] = sp[t].shift;
+    }
+    PartMap* dmap = nullptr;
+    if (e == cudaSuccess) e = cudaMalloc((void**)&dmap, sizeof(PartMap));
+    if (e == cudaSuccess) e = cudaMemcpy(dmap, &pm, sizeof(PartMap), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        for (int t = 0; t < 4; ++t) release(sp[t], parts);
+        cudaFree(dmap);
+        return cuda_fail(e, "grape_graph_partition (the graph is unchanged)");
+    }
+    cudaFree(g->rec);
+    cudaFree(g->guide);
+    cudaFree(g->nodes);
+    cudaFree(g->ehash);
+    g->rec = nullptr;
+    g->guide = nullptr;
+    g->nodes = nullptr;
+    g->ehash = nullptr;
+    for (int t = 0; t < 4; ++t) {
+        for (uint32_t j = 0; j < parts; ++j) g->part_mem[t][j] = sp[t].mem[j];
+        g->part_shift[t] = sp[t].shift;
+    }
+    g->part_map = dmap;
+    g->parts = parts;
+    return GRAPE_OK;
+}

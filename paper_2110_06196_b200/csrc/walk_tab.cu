@@ -96,6 +96,7 @@ struct TabParams {
     unsigned long long* steps_out;
     unsigned long long* stats;
     uint32_t tp_m1, t1_m1, tq_m1;   // accept iff u <= T_c - 1
+    const PartMap* pmap;            // MODE 3 (§8(f) f4 layout, partition.cu): the partition map
 };
 
 __device__ __forceinline__ uint32_t fmix32(uint32_t h)
@@ -150,6 +151,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
 {
     constexpr bool SUSS = MODE == 1;   // approximated walks (grape_walks_approx)
     constexpr bool FOLD = MODE == 2;   // outlier-folded rejection (grape_walks_node2vec_folded)
+    constexpr bool PARTS = MODE == 3;  // the default rule over partitioned tables (grape_graph_partition)
     uint32_t cnt[kStatsWords];
     if (STATS) {
 #pragma unroll
@@ -219,6 +221,13 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                 sh = 2;
             }
             const char* addr = b + (e << sh);
+            if (PARTS && st != ST_START) {   // part (offset >> k) of table T, at offset mod 2^k
+                const uint32_t T = rec ? 0u : gd ? 1u : nd ? 2u : 3u;
+                const uint64_t o = e << sh;
+                const uint32_t ps = __ldg(&P.pmap->shift[T]);
+                addr = (const char*)__ldg((const unsigned long long*)&P.pmap->base[T][o >> ps]) +
+                       (o & ((1ull << ps) - 1));
+            }
             if (load) ld8(sector_of(addr), sec);
             j = word_of(addr);
         }
@@ -670,6 +679,7 @@ template <bool WEIGHTED, bool FAT, bool COMPACT, bool NODE2VEC, bool NEED_MEMBER
 cudaError_t launch_k(const grape_graph* g, const WalkArgs& a, const Thresholds& T, cudaStream_t stream)
 {
     TabParams P{};
+    P.pmap = g->part_map;
     P.nodes = g->nodes;
     P.rec = g->rec;
     P.guide = g->guide;
@@ -754,6 +764,10 @@ cudaError_t launch_s(const grape_graph* g, const WalkArgs& a, const Thresholds& 
     if (NODE2VEC && a.sampler == 2 && T.Tp > (T.T1 > T.Tq ? T.T1 : T.Tq)) {
         if (a.stats != nullptr) return launch_k<WEIGHTED, FAT, COMPACT, NODE2VEC, true, true, 2>(g, a, T, stream);
         return launch_k<WEIGHTED, FAT, COMPACT, NODE2VEC, true, false, 2>(g, a, T, stream);
+    }
+    if (g->parts > 1) {   // partitioned tables: the default rule only (capi.cu rejects the other modes)
+        if (a.stats != nullptr) return launch_k<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, true, 3>(g, a, T, stream);
+        return launch_k<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, false, 3>(g, a, T, stream);
     }
     if (a.stats != nullptr) return launch_k<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, true, 0>(g, a, T, stream);
     return launch_k<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, false, 0>(g, a, T, stream);

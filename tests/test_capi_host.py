@@ -84,6 +84,12 @@ def test_argument_errors_before_any_cuda_call(lib):
     assert b"overflows" in lib.grape_last_error()
     assert lib.grape_skipgram_pairs(fake, buf, 4, 2 ** 64 - 2, 4, 2, 1, 42, buf, buf, buf, None) == 1   # wid wrap
     assert b"overflows" in lib.grape_last_error()
+    # partition: NULL graph / devices, parts out of range
+    devs = (ctypes.c_int * 2)(0, 0)
+    assert lib.grape_graph_partition(None, 2, devs) == 1
+    assert lib.grape_graph_partition(fake, 1, devs) == 1
+    assert lib.grape_graph_partition(fake, 9, devs) == 1
+    assert lib.grape_graph_partition(fake, 2, None) == 1
     # graph build: NULL out, NULL arrays, n = PAD, unknown flags
     h = vp()
     assert lib.grape_graph_from_csr(3, 0, buf, buf, None, 0, 0, None) == 1
