@@ -47,6 +47,51 @@ def _as_tensor(a, dtype) -> torch.Tensor:
     return t.contiguous()
 
 
+def _check_out(out: torch.Tensor, shape, device_kind: str, what: str) -> None:
+    """A caller-supplied output buffer must be exactly what the kernel writes: the library
+    writes prod(shape) u32 words through its data pointer (device path) or copies them into
+    it (host path), so a wrong size, dtype, layout or memory kind would corrupt memory."""
+    if not torch.is_tensor(out):
+        raise ValueError(f"{what} must be a torch.Tensor")
+    if out.dtype not in (torch.int32, torch.uint32):
+        raise ValueError(f"{what} must be int32 (u32 bit patterns), got {out.dtype}")
+    if tuple(out.shape) != tuple(shape):
+        raise ValueError(f"{what} must have shape {tuple(shape)}, got {tuple(out.shape)}")
+    if not out.is_contiguous():
+        raise ValueError(f"{what} must be contiguous")
+    if device_kind == "cpu" and out.is_cuda:
+        raise ValueError(f"{what} must be a host tensor (the starts are on the host)")
+    if device_kind != "cpu" and (not out.is_cuda or out.device.index != int(device_kind)):
+        raise ValueError(f"{what} must be on cuda:{device_kind}")
+
+
+def _check_steps(steps: torch.Tensor, on_device: bool, device: int) -> None:
+    """steps: a 1-element int64 counter the library adds realised transitions to (a 64-bit
+    atomicAdd on the device path)."""
+    if not torch.is_tensor(steps) or steps.dtype not in (torch.int64, torch.uint64) or steps.numel() != 1:
+        raise ValueError("steps must be a 1-element int64 tensor")
+    if not steps.is_contiguous():
+        raise ValueError("steps must be contiguous")
+    if on_device and (not steps.is_cuda or steps.device.index != device):
+        raise ValueError(f"steps must be on cuda:{device} (the starts are device memory)")
+
+
+def _stream_handle(stream, device: int, keep=()):
+    """The raw cudaStream_t to launch on.  When the caller names a stream other than the
+    current one, the tensors in `keep` (temporaries and outputs allocated on the current
+    stream) are recorded on it, so the caching allocator cannot hand their memory to
+    other work while the kernel is still queued there."""
+    if stream is None:
+        return torch.cuda.current_stream(device).cuda_stream
+    if isinstance(stream, torch.cuda.Stream):
+        if stream != torch.cuda.current_stream(device):
+            for t in keep:
+                if torch.is_tensor(t) and t.is_cuda:
+                    t.record_stream(stream)
+        return stream.cuda_stream
+    return int(stream)
+
+
 class Graph:
     """Owning handle of a device CSR (grape_graph*)."""
 
@@ -130,10 +175,11 @@ def _walks(fn_name, g: Graph, starts, L, args, seed, walk_id_base, out, steps, s
         with torch.cuda.device(g.device):
             if out is None:
                 out = torch.empty((W, L), dtype=torch.int32, device=st.device)
-            if stream is None:
-                stream = torch.cuda.current_stream(g.device).cuda_stream
-            elif isinstance(stream, torch.cuda.Stream):
-                stream = stream.cuda_stream
+            else:
+                _check_out(out, (W, L), str(g.device), "out")
+            if steps is not None:
+                _check_steps(steps, True, g.device)
+            stream = _stream_handle(stream, g.device, (st, out))
             sp = None if steps is None else steps.data_ptr()
             rc = fn(g.handle, st.data_ptr(), W, walk_id_base, L, *args, seed, out.data_ptr(), sp,
                     ctypes.c_void_p(stream))
@@ -142,12 +188,13 @@ def _walks(fn_name, g: Graph, starts, L, args, seed, walk_id_base, out, steps, s
     # host buffers: the library stages through the device itself
     if out is None:
         out = torch.empty((W, L), dtype=torch.int32, pin_memory=True)
+    else:
+        _check_out(out, (W, L), "cpu", "out")
+    if steps is not None:
+        _check_steps(steps, False, g.device)
     hs = ctypes.c_uint64(0)
     with torch.cuda.device(g.device):
-        if stream is None:
-            stream = torch.cuda.current_stream(g.device).cuda_stream
-        elif isinstance(stream, torch.cuda.Stream):
-            stream = stream.cuda_stream
+        stream = _stream_handle(stream, g.device)   # host path: synchronous, nothing to record
         rc = fn(g.handle, st.data_ptr(), W, walk_id_base, L, *args, seed, out.data_ptr(),
                 ctypes.byref(hs), ctypes.c_void_p(stream))
     _capi.check(_lib, rc, fn_name)
@@ -193,6 +240,10 @@ def skipgram_pairs(g: Graph, walks, window: int, num_negatives: int, *, seed: in
     invalid slots hold PAD (-1)."""
     if not (torch.is_tensor(walks) and walks.is_cuda and walks.dim() == 2):
         raise ValueError("walks must be a 2-D CUDA tensor (a walk matrix)")
+    if walks.dtype not in (torch.int32, torch.uint32):
+        raise ValueError(f"walks must be int32 (u32 bit patterns), got {walks.dtype}")
+    if walks.device.index != g.device:
+        raise ValueError(f"walks on cuda:{walks.device.index}, graph on cuda:{g.device}")
     walks = walks.contiguous()
     W, L = walks.shape
     S = W * L * 2 * window
@@ -201,11 +252,14 @@ def skipgram_pairs(g: Graph, walks, window: int, num_negatives: int, *, seed: in
             out = (torch.empty(S, dtype=torch.int32, device=walks.device),
                    torch.empty(S, dtype=torch.int32, device=walks.device),
                    torch.empty((S, num_negatives), dtype=torch.int32, device=walks.device))
+        else:
+            if len(out) != 3:
+                raise ValueError("out must be (centers, contexts, negatives)")
+            _check_out(out[0], (S,), str(g.device), "centers")
+            _check_out(out[1], (S,), str(g.device), "contexts")
+            _check_out(out[2], (S, num_negatives), str(g.device), "negatives")
         c, x, ng = out
-        if stream is None:
-            stream = torch.cuda.current_stream(g.device).cuda_stream
-        elif isinstance(stream, torch.cuda.Stream):
-            stream = stream.cuda_stream
+        stream = _stream_handle(stream, g.device, (walks, c, x, ng))
         rc = _lib.grape_skipgram_pairs(g.handle, walks.data_ptr(), W, walk_id_base, L, window, num_negatives,
                                        seed, c.data_ptr(), x.data_ptr(), ng.data_ptr() if num_negatives else None,
                                        ctypes.c_void_p(stream))
@@ -227,14 +281,17 @@ def _walks_approx(g, starts, L, n2v, p, q, dT, seed, walk_id_base, out, steps, s
     W = st.numel()
     fn = _lib.grape_walks_approx
     dev = st.is_cuda
+    if dev and st.device.index != g.device:
+        raise ValueError(f"starts on cuda:{st.device.index}, graph on cuda:{g.device}")
     with torch.cuda.device(g.device):
         if out is None:
             out = (torch.empty((W, L), dtype=torch.int32, device=st.device) if dev else
                    torch.empty((W, L), dtype=torch.int32, pin_memory=True))
-        if stream is None:
-            stream = torch.cuda.current_stream(g.device).cuda_stream
-        elif isinstance(stream, torch.cuda.Stream):
-            stream = stream.cuda_stream
+        else:
+            _check_out(out, (W, L), str(g.device) if dev else "cpu", "out")
+        if steps is not None:
+            _check_steps(steps, dev, g.device)
+        stream = _stream_handle(stream, g.device, (st, out) if dev else ())
         hs = ctypes.c_uint64(0)
         sp = (None if steps is None else steps.data_ptr()) if dev else ctypes.byref(hs)
         rc = fn(g.handle, st.data_ptr(), W, walk_id_base, L, n2v, p, q, dT, seed, out.data_ptr(), sp,
@@ -253,10 +310,14 @@ def walks_stats(g: Graph, starts, L: int, *, node2vec: bool, p: float = 1.0, q: 
     st = _as_tensor(starts, torch.int32)
     if not st.is_cuda:
         raise ValueError("walks_stats needs device starts")
+    if st.device.index != g.device:
+        raise ValueError(f"starts on cuda:{st.device.index}, graph on cuda:{g.device}")
     W = st.numel()
     with torch.cuda.device(g.device):
         if out is None:
             out = torch.empty((W, L), dtype=torch.int32, device=st.device)
+        else:
+            _check_out(out, (W, L), str(g.device), "out")
         stats = _capi.WalkStats()
         smp = {"rejection": 0, "cdf": 1, "folded": 2}[sampler]
         rc = _lib.grape_walks_stats_ex(g.handle, st.data_ptr(), W, walk_id_base, L, int(node2vec),

@@ -26,6 +26,28 @@ grape_status cuda_fail(cudaError_t e, const char* what)
     return e == cudaErrorMemoryAllocation ? GRAPE_ENOMEM : GRAPE_ECUDA;
 }
 
+int resident_blocks(const void* kernel, int block, size_t smem, int device)
+{
+    struct Entry { const void* k; int block; size_t smem; int dev; int blocks; };
+    static std::mutex mu;
+    static Entry cache[256];
+    static int used = 0;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        for (int i = 0; i < used; ++i)
+            if (cache[i].k == kernel && cache[i].block == block && cache[i].smem == smem && cache[i].dev == device)
+                return cache[i].blocks;
+    }
+    int sms = 0, per_sm = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem);
+    cudaGetLastError();
+    const int r = (sms > 0 ? sms : 1) * (per_sm > 0 ? per_sm : 1);
+    std::lock_guard<std::mutex> lk(mu);
+    if (used < 256) cache[used++] = Entry{kernel, block, smem, device, r};
+    return r;
+}
+
 namespace {
 
 // T_c = floor(2^32 * min(p,1,q) / c) for c in (p, 1, q), IEEE binary64
@@ -65,17 +87,6 @@ Mem classify(const void* ptr)
     default: return Mem::Host;   // unregistered (pageable) or pinned host
     }
 }
-
-struct DeviceGuard {
-    int prev = -1;
-    bool ok = true;
-    explicit DeviceGuard(int dev)
-    {
-        if (cudaGetDevice(&prev) != cudaSuccess) { prev = -1; ok = false; return; }
-        if (prev != dev && cudaSetDevice(dev) != cudaSuccess) ok = false;
-    }
-    ~DeviceGuard() { if (prev >= 0) cudaSetDevice(prev); }
-};
 
 #ifndef GRAPE_HOST_CHUNK_MB
 #define GRAPE_HOST_CHUNK_MB 256        // smallest default chunk of the walk matrix

@@ -178,12 +178,6 @@ int grid_for(uint64_t items_per_warp_rows)
 // an aligned sector load of the last (partial) block never leaves the buffer.
 uint64_t padded(uint64_t bytes) { return ((bytes + 31) / 32) * 32 + 32; }
 
-struct DeviceGuard {
-    int prev = -1;
-    explicit DeviceGuard(int dev) { cudaGetDevice(&prev); cudaSetDevice(dev); }
-    ~DeviceGuard() { if (prev >= 0) cudaSetDevice(prev); }
-};
-
 }  // namespace
 
 void destroy_graph(grape_graph* g)

@@ -15,7 +15,7 @@
 //          With it the walker knows, at x coming from v, which draws propose
 //          x' == v (the "return" class p) without reading anything, and
 //          it has x's node record without a second read.
-//   guide  weighted rows only, B_v = G deg(v) entries at G off[v] (G = 4, 2 or 1,
+//   guide  weighted rows only, B_v = G deg(v) entries at G off[v] (G = 16, 8, 4, 2 or 1,
 //          32-B "fat" or 8-B "slim" entries, by free memory; a fat entry of an
 //          unsplit bucket is a copy of the record): entry kb covers the x64 draws with
 //          floor(x64 * B_v / 2^64) = kb; it holds i_lo = the proposal index of

@@ -47,13 +47,13 @@ struct grape_graph {
     bool wsym;            // every arc with a reverse arc has the reverse's weight
     uint32_t rec_bytes;   // 32 / 16 (weighted: full / compact), 16 / 8 (unweighted), graph_tables.cu
     void* rec;            // per-arc records, arc order
-    uint32_t* guide;      // weighted: G*deg(v) 8-B guide entries per row at G*off[v]
+    uint32_t* guide;      // weighted: G*deg(v) guide entries per row at G*off[v] (guide_bytes each: 32 fat / 8 slim)
     uint32_t guide_factor;   // G (buckets per arc) of the guide
     uint32_t guide_bytes;    // 32 (fat: unsplit buckets hold a record copy) or 8 (slim)
     uint32_t hash_h;         // edge-hash buckets: floor(deg / H) + 1 per row (H = 4 or 6)
     bool compact;            // records without the head's node record (16 B weighted / 8 B)
     bool notri;              // records carry the no-common-neighbour flags (graph_tables.cu)
-    uint32_t* ehash;      // per-row linear-probing sets of N(v): 2*deg(v) slots at 2*off[v]
+    uint32_t* ehash;      // per-row bucketised sets of N(v): floor(deg/H)+1 buckets of 8 u32 slots from bucket floor(off[v]/H)+v
     uint64_t table_bytes;
     uint64_t rec_alloc = 0, guide_alloc = 0, hash_alloc = 0;   // table allocation bytes
     // §8(f) f4 layout (partition.cu, grape_graph_partition): every table split into
@@ -79,6 +79,25 @@ struct grape_graph {
 };
 
 namespace grape {
+
+// Makes `dev` current for a scope (restores the caller's device on exit).
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(int dev)
+    {
+        if (cudaGetDevice(&prev) != cudaSuccess) { prev = -1; ok = false; cudaGetLastError(); return; }
+        if (prev != dev && cudaSetDevice(dev) != cudaSuccess) { ok = false; cudaGetLastError(); }
+    }
+    ~DeviceGuard() { if (prev >= 0) cudaSetDevice(prev); }
+    DeviceGuard(const DeviceGuard&) = delete;
+    DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
+// Resident blocks of `kernel` (block threads, dynamic smem bytes) on the whole of
+// `device`: SMs x blocks per SM, cached per (kernel, device) (capi.cu).  A process
+// that walks graphs on GPUs of different SM counts sizes each grid for its own GPU.
+int resident_blocks(const void* kernel, int block, size_t smem, int device);
 
 // Thread-local error message (capi.cu).
 void set_error(const char* fmt, ...);

@@ -69,6 +69,13 @@ extern "C" grape_status grape_graph_partition(grape_graph* g, uint32_t parts, co
         set_error("grape_graph_partition: the graph has no sampling tables, or is already partitioned");
         return GRAPE_EINVAL;
     }
+    // every step below (peer access, synchronisation, the device partition map) on the
+    // graph's device, whatever device the caller has current
+    DeviceGuard guard(g->device);
+    if (!guard.ok) {
+        set_error("grape_graph_partition: cannot make the graph's device %d current", g->device);
+        return GRAPE_ECUDA;
+    }
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
@@ -84,13 +91,9 @@ extern "C" grape_status grape_graph_partition(grape_graph* g, uint32_t parts, co
             set_error("grape_graph_partition: device %d cannot access device %d", g->device, devices[j]);
             return GRAPE_EINVAL;
         }
-        int prev = 0;
-        cudaGetDevice(&prev);
-        cudaSetDevice(g->device);
-        e = cudaDeviceEnablePeerAccess(devices[j], 0);
+        e = cudaDeviceEnablePeerAccess(devices[j], 0);   // (the graph's device is current)
         if (e == cudaErrorPeerAccessAlreadyEnabled) e = cudaSuccess;
         cudaGetLastError();
-        cudaSetDevice(prev);
         if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
     }
     e = cudaDeviceSynchronize();
@@ -129,5 +132,8 @@ extern "C" grape_status grape_graph_partition(grape_graph* g, uint32_t parts, co
     }
     g->part_map = dmap;
     g->parts = parts;
+    // the same table bytes, now spread over the parts' devices (device_bytes counts the
+    // graph's bytes on every device it uses), plus the map
+    g->device_bytes += sizeof(PartMap);
     return GRAPE_OK;
 }

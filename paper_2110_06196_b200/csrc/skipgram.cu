@@ -198,12 +198,9 @@ cudaError_t launch_skipgram(const grape_graph* g, const uint32_t* walks, uint64_
     P.centers = centers;
     P.contexts = contexts;
     P.negs = negs;
-    static const int sms = [] {   // thread-safe static init
-        int dev = 0, n = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        return n > 0 ? n : 1;
-    }();
+    int sms = 0;   // of the graph's device
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
+    if (sms < 1) sms = 1;
     uint64_t blocks = num_walks;
     const uint64_t cap = (uint64_t)sms * 8;   // 8 resident blocks of 256 per SM, grid-stride over rows
     if (blocks > cap) blocks = cap;

@@ -332,13 +332,7 @@ cudaError_t launch(const grape_graph* g, const WalkArgs& a, const Thresholds& T,
     else { P.h_mul = 0x40000000u; P.h_shift = 0; }
     P.notri = g->notri;
     P.xmask = (g->notri && g->compact) ? 0x3FFFFFFFu : 0xFFFFFFFFu;
-    static const int resident = [] {   // thread-safe static init, once per instantiation
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, walk_cdf_kernel<WEIGHTED, COMPACT>, 256, 0);
-        return sms * (per_sm > 0 ? per_sm : 1);
-    }();
+    const int resident = resident_blocks((const void*)walk_cdf_kernel<WEIGHTED, COMPACT>, 256, 0, g->device);
     uint64_t blocks = (a.num_walks * 32 + 255) / 256;
     if (blocks > (uint64_t)resident) blocks = resident;
     P.chunks_max = ((uint64_t)g->max_degree + 31) / 32 + 1;

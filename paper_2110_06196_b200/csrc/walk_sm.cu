@@ -323,15 +323,9 @@ template <typename CW, typename IDX, bool NODE2VEC, bool NEED_MEMBER, bool SYM, 
 cudaError_t launch_sm_k(const grape_graph* gg, const WalkArgs& a, const Thresholds& T, cudaStream_t stream)
 {
     const Params<CW> P = make_params<CW>(gg, a, T);
-    // blocks per SM x SMs, queried once per process and instantiation (thread-safe static init)
-    static const int resident = [] {
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per_sm, walk_sm_kernel<CW, IDX, NODE2VEC, NEED_MEMBER, SYM, STATS>, kBlock, 0);
-        return sms * (per_sm > 0 ? per_sm : 1);
-    }();
+    // blocks per SM x SMs of the graph's device (cached per kernel and device)
+    const int resident = resident_blocks((const void*)walk_sm_kernel<CW, IDX, NODE2VEC, NEED_MEMBER, SYM, STATS>,
+                                         kBlock, 0, gg->device);
     uint64_t blocks = (a.num_walks + kBlock - 1) / kBlock;
     if (blocks > (uint64_t)resident) blocks = resident;   // persistent: lanes loop over walks
     walk_sm_kernel<CW, IDX, NODE2VEC, NEED_MEMBER, SYM, STATS><<<(unsigned)blocks, kBlock, 0, stream>>>(P);

@@ -715,15 +715,9 @@ cudaError_t launch_k(const grape_graph* g, const WalkArgs& a, const Thresholds& 
         P.fold_x = (uint32_t)(T.Tp - E);
     }
     P.dT = a.dT;
-    // blocks per SM x SMs, queried once per process and instantiation (thread-safe static init)
-    static const int resident = [] {
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, walk_tab_kernel<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, STATS, MODE>,
-                                                      kBlock, 0);
-        return sms * (per_sm > 0 ? per_sm : 1);
-    }();
+    // blocks per SM x SMs of the graph's device (cached per kernel and device)
+    const int resident = resident_blocks(
+        (const void*)walk_tab_kernel<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, STATS, MODE>, kBlock, 0, g->device);
     uint64_t blocks = (a.num_walks + kBlock - 1) / kBlock;
     if (blocks > (uint64_t)resident) blocks = resident;
     P.lanes = (uint32_t)(blocks * kBlock);

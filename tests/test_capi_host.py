@@ -114,3 +114,30 @@ def test_product_never_touches_the_oracle():
     mk = open(os.path.join(ROOT, "Makefile")).read()
     lib_rule = mk.split("$(LIB):")[1].split("\n\n")[0]
     assert "oracle" not in lib_rule
+
+
+def test_binding_rejects_mismatched_output_buffers():
+    """The binding checks caller-supplied outputs before handing their pointers to the
+    library (shape, dtype, contiguity, memory kind): a wrong buffer is a ValueError, never
+    a write past its end."""
+    import torch
+    import paper_2110_06196_b200 as grape
+    ok = torch.empty((4, 5), dtype=torch.int32)
+    grape._check_out(ok, (4, 5), "cpu", "out")
+    grape._check_out(ok.view(torch.uint32), (4, 5), "cpu", "out")
+    for bad, why in [(torch.empty((4, 4), dtype=torch.int32), "shape"),
+                     (torch.empty((5, 4), dtype=torch.int32), "shape"),
+                     (torch.empty((4, 5), dtype=torch.int64), "int32"),
+                     (torch.empty((5, 4), dtype=torch.int32).t(), "contiguous"),
+                     (torch.empty((4, 5, 1), dtype=torch.int32), "shape")]:
+        with pytest.raises(ValueError, match=why):
+            grape._check_out(bad, (4, 5), "cpu", "out")
+    with pytest.raises(ValueError, match="cuda:0"):
+        grape._check_out(ok, (4, 5), "0", "out")            # host tensor for a device call
+    grape._check_steps(torch.zeros(1, dtype=torch.int64), False, 0)
+    for bad in (torch.zeros(1, dtype=torch.int32), torch.zeros(2, dtype=torch.int64),
+                torch.zeros((), dtype=torch.float64)):
+        with pytest.raises(ValueError, match="int64"):
+            grape._check_steps(bad, False, 0)
+    with pytest.raises(ValueError, match="cuda:0"):
+        grape._check_steps(torch.zeros(1, dtype=torch.int64), True, 0)
