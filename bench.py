@@ -7,8 +7,13 @@ One "step" of this benchmark = one pass of the whole hot path over one batch:
 grape_walks_node2vec over every walk of the workload (BASELINE configs[1] by
 default: Chung-Lu 1M nodes / ~20M edges, weights U{1..100}, p=0.5, q=2,
 10 walks per node, L=80).  N > 1 (torchrun): every rank holds a replica of
-the graph and runs the same per-GPU workload on its own walk-id range
-(weak scaling, no collective on the data path).  Rank 0 prints one JSON line.
+the graph (BASELINE north_star: "replicated on every GPU ... walks sharded by
+start node") and walks its contiguous slice [floor(r W/N), floor((r+1) W/N)) of
+the config's fixed, iteration-major walk list with walk_id_base = the slice
+start (--scaling strong, the default: the same total work at every N, so the
+concatenated rank matrices are the N = 1 matrix bit for bit).  --scaling weak
+gives every rank the whole per-GPU workload on its own wid block instead.
+No collective is on the data path.  Rank 0 prints one JSON line.
 
 --impl reference times the CPU oracle (the only reference this paper-tier
 task has) on a bounded sample of the same workload on the host cores.
@@ -112,13 +117,18 @@ class ClockSampler:
 
 
 def _dist_setup(args):
+    """(world, rank, device index).  The device is LOCAL_RANK unless --device pins every
+    rank to one GPU (the two-process parity test: both ranks on cuda:0, which needs the
+    gloo backend — NCCL refuses two ranks on one device)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.device is not None:
+        local = args.device
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
-        if backend == "nccl":
+        backend = args.dist_backend or ("nccl" if torch.cuda.is_available() else "gloo")
+        if torch.cuda.is_available():
             torch.cuda.set_device(local)
         dist.init_process_group(backend, rank=rank, world_size=world)
     elif torch.cuda.is_available():
@@ -126,12 +136,38 @@ def _dist_setup(args):
     return world, rank, local
 
 
+def _red_device(dev):
+    """Where the small reduction tensors live: the GPU for NCCL, the host for gloo."""
+    if dist.is_initialized() and dist.get_backend() == "gloo":
+        return torch.device("cpu")
+    return dev
+
+
+def rank_slice(W_total: int, per_gpu: int, rank: int, world: int, scaling: str):
+    """(lo, hi) of the iteration-major wid list this rank walks.
+    strong: the config's W_total walks split into contiguous start-node slices;
+    weak: per_gpu walks per rank on wid block [r per_gpu, (r+1) per_gpu)."""
+    from paper_2110_06196_b200.shard import shard_range, weak_scaling_range
+    if scaling == "strong":
+        return shard_range(W_total, rank, world)
+    return weak_scaling_range(per_gpu, rank, world)
+
+
 def _allreduce(x: float, op, world):
     if world == 1:
         return x
-    t = torch.tensor([x], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    dev = "cuda" if torch.cuda.is_available() and dist.get_backend() != "gloo" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=op)
     return float(t.item())
+
+
+def _allgather(x: float, world):
+    if world == 1:
+        return [x]
+    out = [None] * world
+    dist.all_gather_object(out, float(x))
+    return out
 
 
 def _oracle_sample(g_cpu, wk, budget_s: float, first_wid: int = 0, cores: int | None = None, dT: int = 0,
@@ -238,7 +274,7 @@ def run_reference(args):
         metric = metric[:-1] + ", outlier-folded rejection)"
     line = {"impl": "reference", "metric": metric, "value": v,
             "unit": "steps/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * total_secs / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": 1e3 * total_secs / args.steps, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "u32/u64 integer", "data": "synthetic (seeded generator)",
             "config": _workload_desc(k, g, wk, W, _needs_flush(g, W, wk["L"])),
             "cpu_baseline": {"value": v, "unit": "steps/s", "cores": cores, "kind": "oracle",
@@ -263,23 +299,34 @@ def _walk_recipe(args):
 def run_ours(args):
     world, rank, local = _dist_setup(args)
     import paper_2110_06196_b200 as grape
-    from paper_2110_06196_b200.shard import reduce_step_timing, weak_scaling_range
+    from paper_2110_06196_b200.shard import reduce_step_timing
     k = args.config
     wk = _walk_recipe(args)
     dev = torch.device("cuda", local)
-    g = config_graph(k, device=dev)
+    g = config_graph(k, device=dev, scale_down=args.scale_down)
     torch.cuda.empty_cache()   # the generator's temporaries: room for the graph's tables
+    # a1 graph build (validation, prefix, node records, sampling tables): synchronous
+    # C-ABI call, timed on its own (outside the timed walk region, reported)
+    torch.cuda.synchronize(dev)
+    t_b = time.perf_counter()
     dg = grape.graph_from_csr(g.off, g.col, g.w, device=local, symmetric=g.symmetric, tables=not args.no_tables,
                               layout=_parse_layout(args.layout))
+    torch.cuda.synchronize(dev)
+    build_ms = 1e3 * (time.perf_counter() - t_b)
     g = g.to("cpu")            # the library holds its own copy; free the device CSR for the walk matrix
     torch.cuda.empty_cache()
     if args.parts > 1:         # §8(f) f4 layout: tables in power-of-two parts (on this GPU)
         dg.partition([local] * args.parts)
     info = dg.info
-    W = g.n * wk["walks_per_node"]
+    W_total = g.n * wk["walks_per_node"]          # the config's walk list (iteration-major)
     L = wk["L"]
-    base, _ = weak_scaling_range(W, rank, world)   # rank r: wids [r W, (r+1) W) of N x W walks
-    starts = starts_per_node(g.n, wk["walks_per_node"], device=dev)
+    lo, hi = rank_slice(W_total, W_total, rank, world, args.scaling)
+    base = lo
+    W = hi - lo                                   # this rank's walks
+    if args.scaling == "strong":
+        starts = starts_per_node(g.n, wk["walks_per_node"], device=dev)[lo:hi].contiguous()
+    else:
+        starts = starts_per_node(g.n, wk["walks_per_node"], device=dev)
     out = torch.empty((W, L), dtype=torch.int32, device=dev)
     steps_ctr = torch.zeros(1, dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -333,7 +380,12 @@ def run_ours(args):
     kernel_ms = [a.elapsed_time(b) for a, b in ev]
     my_ms = float(sum(kernel_ms))
     my_steps = float(steps_ctr.item())
-    max_ms, tot_steps = reduce_step_timing(my_ms, my_steps, world, device=dev)
+    max_ms, tot_steps = reduce_step_timing(my_ms, my_steps, world, device=_red_device(dev))
+    rank_ms = _allgather(my_ms / args.steps, world)     # per-rank ms per step (tail imbalance)
+    if args.dump_walks:   # the rank's walk matrix, for the multi-process parity test
+        np.save(f"{args.dump_walks}.rank{rank}.npy", out.cpu().numpy().view(np.uint32))
+        with open(f"{args.dump_walks}.rank{rank}.json", "w") as f:
+            json.dump({"lo": lo, "hi": hi, "steps": my_steps / args.steps}, f)
     value = tot_steps / (max_ms / 1e3)
     steps_per_launch = my_steps / args.steps
     avg_launch_ms = my_ms / args.steps
@@ -350,6 +402,7 @@ def run_ours(args):
         if _allreduce(1.0 if h_out is not None else 0.0, dist.ReduceOp.MIN, world) < 1.0:
             h_out = None   # every rank skips together (no half-entered collective)
             e2e = e2e or {"unavailable": "a rank could not pin its host buffer"}
+    e2e_one_ms = None
     if h_out is not None:
         h_steps = torch.zeros(1, dtype=torch.int64)
         time.sleep(1.0)            # the clock sampler's nvidia-smi has just exited (its NVML teardown)
@@ -367,6 +420,7 @@ def run_ours(args):
         torch.cuda.synchronize(dev)
         e2e_s = time.perf_counter() - t0
         e2e_s = _allreduce(e2e_s, dist.ReduceOp.MAX, world)
+        e2e_one_ms = 1e3 * e2e_s / e2e_steps
         e2e_tot = _allreduce(float(h_steps.item()), dist.ReduceOp.SUM, world)
         e2e = {"value": e2e_tot / e2e_s, "unit": "steps/s", "h2d_bytes_per_step": int(W * 4),
                "d2h_bytes_per_step": int(W * L * 4 + 8), "steps_timed": e2e_steps,
@@ -376,6 +430,7 @@ def run_ours(args):
                          "grape_walks_node2vec") if node2vec else "grape_walks_first_order") +
                        " with pinned host starts/out (library-staged, chunked H2D/kernel/D2H)"}
 
+    build_max = _allreduce(build_ms, dist.ReduceOp.MAX, world)   # every rank builds its replica
     # ---- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and not args.no_cpu and world == 1:
@@ -491,10 +546,27 @@ def run_ours(args):
             metric = metric[:-1] + ", outlier-folded rejection)"
         if args.parts > 1:
             metric = metric[:-1] + f", tables in {args.parts} parts)"
+        cfg = _workload_desc(k, g, wk, W, flush)
+        cfg.update({"walks_total": W_total if args.scaling == "strong" else W * world,
+                    "sharding": ("strong: rank r walks wids [floor(r W/N), floor((r+1) W/N)) of the config's "
+                                 "fixed list, walk_id_base = slice start (graph replicated)"
+                                 if args.scaling == "strong" else
+                                 "weak: every rank walks W wids on its own block [r W, (r+1) W)")})
+        if args.scale_down:
+            cfg["scale_down"] = args.scale_down
         line = {"metric": metric, "value": value, "unit": "steps/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32/u64 integer",
-                "data": "synthetic (seeded generator, graphgen/)", "config": _workload_desc(k, g, wk, W, flush),
+                "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "u32/u64 integer",
+                "data": "synthetic (seeded generator, graphgen/)", "config": cfg,
+                "rank_ms_per_step": [round(x, 3) for x in rank_ms],
+                "rank_spread": (max(rank_ms) / min(rank_ms) - 1.0) if min(rank_ms) > 0 else None,
+                "graph_build_ms": build_max,
+                "one_pass": {"graph_build_ms": build_max, "walk_ms": max_ms / args.steps,
+                             "e2e_walk_ms": e2e_one_ms,
+                             "steps_per_s_incl_build": tot_steps / args.steps /
+                                                       ((build_max + (e2e_one_ms or max_ms / args.steps)) / 1e3),
+                             "note": "one pass from a device CSR: build the graph (validation, prefix, tables), "
+                                     "then one walk call (host buffers when e2e ran)"},
                 "gpu_launches": args.steps, "realised_steps_per_gpu_step": steps_per_launch,
                 "step_ms": [round(x, 3) for x in kernel_ms],
                 "nominal_steps_per_gpu_step": W * (L - 1), "wall_s_timed": t_wall,
@@ -643,6 +715,16 @@ def main():
     ap.add_argument("--layout", default="", help="force table layout fields, e.g. "
                     "record_bytes=16,guide_bytes=8,guide_factor=1,hash_h=6 (grape_table_options)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle baseline (profiling runs)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="N > 1: strong = the config's fixed walk list sharded by start node (north_star); "
+                         "weak = the whole per-GPU workload on every rank")
+    ap.add_argument("--scale-down", type=int, default=0, help="shrink the config's graph by 2^k (tests)")
+    ap.add_argument("--device", type=int, default=None,
+                    help="CUDA device of every rank (default LOCAL_RANK); tests pin two ranks to cuda:0")
+    ap.add_argument("--dist-backend", default=None, choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (default nccl on GPUs)")
+    ap.add_argument("--dump-walks", default=None, metavar="PREFIX",
+                    help="save each rank's walk matrix to PREFIX.rank<r>.npy (parity tests)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

@@ -230,18 +230,22 @@ FULL = [(2, "node2vec"), (3, "node2vec"), (4, "node2vec"), (5, "node2vec"), (5, 
 @pytest.mark.parametrize("k,mode", FULL, ids=[f"cfg{k}-{m}" for k, m in FULL])
 def test_full_size_config_sampled(grape, k, mode):
     """BASELINE configs at full size, in bench.py's launch configuration (one call
-    over all walks of the config): a seeded sample of walks — random wids, every
-    walk starting at one of the 50 highest-degree nodes, and (directed graphs)
-    walks from sinks — recomputed by the oracle one by one (the counter-based RNG
-    makes walk i a function of (seed, wid) alone); plus the step counter against
-    the matrix and invariants on the whole matrix."""
+    over all walks of the config): a seeded sample of GPU rows — 10^4 random wids,
+    every walk starting at one of the 100 highest-degree nodes, and every walk
+    starting at one of 100 sinks (out-degree 0; directed configs) — each compared
+    with the oracle's walk recomputed alone (the counter-based RNG makes walk i a
+    function of (seed, wid) alone); plus the step counter against the matrix and
+    invariants on the whole matrix."""
     wk = config_walks(k)
     g = config_graph(k, device="cuda")
     torch.cuda.empty_cache()
     dg = _dev_graph(grape, g)
     deg = (g.off[1:] - g.off[:-1])
-    hubs = torch.topk(deg, 50).indices.cpu().numpy()
-    sinks = torch.nonzero(deg == 0).flatten()[:20].cpu().numpy()
+    hubs = torch.topk(deg, 100).indices.cpu().numpy()
+    sink_all = torch.nonzero(deg == 0).flatten()
+    pick = torch.randperm(sink_all.numel(), generator=torch.Generator().manual_seed(k))[:100]
+    sinks = sink_all[pick.to(sink_all.device)].cpu().numpy()
+    del sink_all
     del deg
     gc = g.to("cpu")   # the library holds its own copy: room for the walk matrix
     del g
@@ -264,12 +268,13 @@ def test_full_size_config_sampled(grape, k, mode):
         realised += int((~pad).sum(dim=1, dtype=torch.int32).sum().item()) - pad.shape[0]
     del pad
     assert realised == int(steps.item())
-    host_rows = {}
     rng = np.random.default_rng(k)
-    sample = np.concatenate([rng.integers(0, W, 1500), hubs, [0, W - 1]])
-    if wk["walks_per_node"] > 1:
-        sample = np.concatenate([sample, hubs + gc.n])
+    # every walk whose start is a hub or a sink: wid = it * n + node for every iteration it
+    special = np.concatenate([hubs, sinks]).astype(np.int64)
+    its = np.arange(wk["walks_per_node"], dtype=np.int64) * gc.n
+    sample = np.concatenate([rng.integers(0, W, 10_000), (special[None, :] + its[:, None]).ravel(), [0, W - 1]])
     sample = np.unique(sample)
+    assert len(sample) >= 10_000
     idx = torch.as_tensor(sample, device="cuda")
     host_out = out[idx].cpu().numpy().view(np.uint32)
     st_np = starts[idx].cpu().numpy().view(np.uint32)
@@ -280,10 +285,17 @@ def test_full_size_config_sampled(grape, k, mode):
     for r, i in enumerate(sample):
         exp, _ = o.walks(st_np[r:r + 1], wk["L"], mode=mode, p=wk["p"], q=wk["q"], seed=wk["seed"], base=int(i))
         assert np.array_equal(host_out[r], exp[0]), int(i)
-    # walks that start at sinks (directed configs): [start, PAD, ...]
+    # the GPU rows of walks from sinks (directed configs): [start, PAD, ...]
     if len(sinks):
-        exp, st_ = o.walks(sinks.astype(np.uint32), wk["L"], mode=mode, p=wk["p"], q=wk["q"], seed=wk["seed"])
-        assert st_ == 0 and np.all(exp[:, 1:] == PAD)
+        assert k == 5 and len(sinks) == 100
+        at = {int(i): r for r, i in enumerate(sample)}
+        for it in range(wk["walks_per_node"]):
+            for s_ in sinks:
+                row = host_out[at[int(s_) + it * gc.n]]
+                assert row[0] == s_ and np.all(row[1:] == PAD), int(s_)
+    # and the GPU rows from hubs were all compared above
+    for h in hubs:
+        assert int(h) in {int(i) for i in sample}
 
 
 def test_invalid_inputs_rejected(grape):

@@ -77,3 +77,25 @@ def test_two_rank_gloo_sharding_is_bit_exact():
         assert np.array_equal(cat, full)
         assert t == 11.0                      # max over ranks
         assert s == float(fsteps)             # sum of realised steps
+
+
+def test_bench_rank_slices_strong_and_weak():
+    """bench.py's N > 1 split: strong scaling shards the config's fixed
+    iteration-major walk list into contiguous start-node slices (the union is the
+    N = 1 list, each slice's walk_id_base is its start); weak scaling gives each rank
+    its own block of the per-GPU workload."""
+    import bench
+    W = 10_000_000
+    for world in (1, 2, 3, 4, 8):
+        sl = [bench.rank_slice(W, W, r, world, "strong") for r in range(world)]
+        assert sl[0][0] == 0 and sl[-1][1] == W
+        assert all(sl[i][1] == sl[i + 1][0] for i in range(world - 1))
+        assert sum(b - a for a, b in sl) == W
+        wk = [bench.rank_slice(W, W, r, world, "weak") for r in range(world)]
+        assert wk == [(r * W, (r + 1) * W) for r in range(world)]
+    # one walk per node (configs 3-5): a rank's slice is a contiguous start-node range
+    n = 1000
+    starts = np.arange(n)
+    for r in range(8):
+        lo, hi = bench.rank_slice(n, n, r, 8, "strong")
+        assert np.array_equal(starts[lo:hi], np.arange(lo, hi))
