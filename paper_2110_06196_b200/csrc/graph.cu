@@ -6,12 +6,14 @@
 //   cw  u32|u64[m] row-local inclusive prefix of the u32 weights ("un-normalized
 //                  cumulative distribution", built once instead of per step);
 //                  u32 when every row sum < 2^32, else u64.
-// All kernels here run once per graph (not on the timed path): one warp per row,
-// grid-stride over rows, so hub rows are scanned by a whole warp.
+// All kernels here run once per graph (not on the timed path): streaming passes
+// one warp per row (a hub row is scanned by a whole warp, coalesced); the
+// symmetric check, a search per arc, is distributed per arc (build_common.cuh).
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
 #include "internal.h"
+#include "build_common.cuh"
 
 namespace grape {
 namespace {
@@ -60,27 +62,24 @@ __global__ void check_rows(const uint64_t* __restrict__ off, const uint32_t* __r
     if (mine) atomicOr(bad, mine);
 }
 
-// Every arc v -> u needs u -> v: binary search of v in row u.
+// Every arc v -> u needs u -> v: binary search of v in row u, one thread per arc.
 __global__ void check_symmetric(const uint64_t* __restrict__ off, const uint32_t* __restrict__ col,
-                                uint32_t n, unsigned* __restrict__ bad)
+                                uint32_t n, uint64_t m, unsigned* __restrict__ bad)
 {
-    const unsigned lane = threadIdx.x & 31;
-    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     bool ok = true;
-    for (uint64_t v = warp; v < n; v += nwarps) {
-        const uint64_t lo = off[v], hi = off[v + 1];
-        for (uint64_t e = lo + lane; e < hi; e += 32) {
-            const uint32_t u = col[e];
-            uint64_t a = off[u], b = off[u + 1];
-            while (a < b) {
-                const uint64_t mid = a + ((b - a) >> 1);
-                if (col[mid] < (uint32_t)v) a = mid + 1; else b = mid;
-            }
-            if (a == off[u + 1] || col[a] != (uint32_t)v) ok = false;
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
+        const uint32_t v = build::row_of(off, n, e);
+        const uint32_t u = col[e];
+        uint64_t a = off[u], b = off[u + 1];
+        const uint64_t end = b;
+        while (a < b) {
+            const uint64_t mid = a + ((b - a) >> 1);
+            if (col[mid] < v) a = mid + 1; else b = mid;
         }
+        if (a == end || col[a] != v) ok = false;
     }
-    if (!ok) atomicOr(bad, BAD_SYM);
+    if (!__all_sync(0xffffffffu, ok) && (threadIdx.x & 31) == 0) atomicOr(bad, BAD_SYM);
 }
 
 // Row sums (W_v) and degrees -> maxima.
@@ -271,7 +270,11 @@ grape_status build_graph(uint32_t n, uint64_t m, const uint64_t* off_in, const u
         GRAPE_TRY_CUDA(cudaMemcpy(&bad, d_bad, 4, cudaMemcpyDeviceToHost), "validate offsets");
         if (!bad) {
             check_rows<<<rows_grid, kThreads>>>(g->off, g->col, w, n, d_bad);
-            if (flags & GRAPE_SYMMETRIC) check_symmetric<<<rows_grid, kThreads>>>(g->off, g->col, n, d_bad);
+            if ((flags & GRAPE_SYMMETRIC) && m) {
+                int sms = 0;
+                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+                check_symmetric<<<build::item_grid(m, sms), kThreads>>>(g->off, g->col, n, m, d_bad);
+            }
             GRAPE_TRY_CUDA(cudaMemcpy(&bad, d_bad, 4, cudaMemcpyDeviceToHost), "validate rows");
         }
         if (bad) {

@@ -37,6 +37,7 @@
 #include <algorithm>
 #include <cstring>
 #include "internal.h"
+#include "build_common.cuh"
 
 namespace grape {
 namespace {
@@ -75,92 +76,103 @@ __device__ inline uint64_t upper_bound_u32(const uint32_t* __restrict__ cw, uint
     return a;
 }
 
-// One warp per row, lanes over the row's arcs.  Each record also carries the
-// node record of its head x (start, degree, W_x), so a walk that takes the arc
-// needs no separate node load.
+// One thread per arc (build_common.cuh: hub rows do not leave a tail).  Each record
+// also carries the node record of its head x (start, degree, W_x), so a walk that
+// takes the arc needs no separate node load.
 // Flags of arc e = (v -> x) (rev = its reverse arc): NOTRI_SELF = notri[e] (used on
 // arriving at x through e), NOTRI_REV = notri[rev] (used on a register-decided return
 // x -> v).  Full records keep them in bits 29 / 28 of the degree word, compact records
 // in bits 31 / 30 of x (only when n < 2^30; else never set).
 template <bool WEIGHTED, bool COMPACT>
 __global__ void build_records(const uint64_t* __restrict__ off, const uint32_t* __restrict__ col,
-                              const uint32_t* __restrict__ cw, uint32_t n, void* __restrict__ rec,
+                              const uint32_t* __restrict__ cw, uint32_t n, uint64_t m, void* __restrict__ rec,
                               unsigned* __restrict__ asym, const uint8_t* __restrict__ notri)
 {
-    const unsigned lane = threadIdx.x & 31;
-    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     bool bad = false;
-    for (uint64_t v = warp; v < n; v += nwarps) {
-        const uint64_t lo = off[v], hi = off[v + 1];
-        for (uint64_t e = lo + lane; e < hi; e += 32) {
-            const uint32_t x = col[e];
-            const uint64_t xa = off[x], xb = off[x + 1];
-            const uint64_t j = lower_bound_u32(col, xa, xb, (uint32_t)v);
-            const bool found = j < xb && col[j] == (uint32_t)v;
-            uint32_t fl = 0;   // flag bits (0: self, 1: reverse)
-            if (notri != nullptr) fl = (notri[e] ? 1u : 0u) | (found && notri[j] ? 2u : 0u);
-            const uint32_t xf = COMPACT ? (x | (fl & 1) << 31 | (fl >> 1) << 30) : x;   // compact: bits 31 (self), 30 (rev)
-            const uint32_t df = COMPACT ? 0u : ((fl & 1) << 29 | (fl >> 1) << 28);   // full: bits 29, 28 of deg
-            if (WEIGHTED) {
-                const uint32_t own_hi = cw[e];
-                const uint32_t own_lo = e > lo ? cw[e - 1] : 0u;
-                uint32_t rlo = 0, rhi = 0;
-                if (found) {
-                    rlo = j > xa ? cw[j - 1] : 0u;
-                    rhi = cw[j];
-                    bad |= (rhi - rlo) != own_hi - own_lo;
-                }
-                if (COMPACT) {
-                    reinterpret_cast<uint4*>(rec)[e] = make_uint4(xf, own_hi, rlo, rhi);
-                } else {
-                    const uint32_t xW = xb > xa ? cw[xb - 1] : 0u;
-                    uint4* r = reinterpret_cast<uint4*>(rec) + 2 * e;
-                    r[0] = make_uint4(x, own_hi, rlo, rhi);
-                    r[1] = make_uint4((uint32_t)xa, (uint32_t)(xb - xa) | df, xW, own_lo);
-                }
-            } else {
-                const uint32_t rev = found ? (uint32_t)(j - xa) : kNone;
-                if (COMPACT)
-                    reinterpret_cast<uint2*>(rec)[e] = make_uint2(xf, rev);
-                else
-                    reinterpret_cast<uint4*>(rec)[e] = make_uint4(x, rev, (uint32_t)xa, (uint32_t)(xb - xa) | df);
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
+        const uint32_t v = build::row_of(off, n, e);
+        const uint64_t lo = off[v];
+        const uint32_t x = col[e];
+        const uint64_t xa = off[x], xb = off[x + 1];
+        const uint64_t j = lower_bound_u32(col, xa, xb, v);
+        const bool found = j < xb && col[j] == v;
+        uint32_t fl = 0;   // flag bits (0: self, 1: reverse)
+        if (notri != nullptr) fl = (notri[e] ? 1u : 0u) | (found && notri[j] ? 2u : 0u);
+        const uint32_t xf = COMPACT ? (x | (fl & 1) << 31 | (fl >> 1) << 30) : x;   // compact: bits 31 (self), 30 (rev)
+        const uint32_t df = COMPACT ? 0u : ((fl & 1) << 29 | (fl >> 1) << 28);   // full: bits 29, 28 of deg
+        if (WEIGHTED) {
+            const uint32_t own_hi = cw[e];
+            const uint32_t own_lo = e > lo ? cw[e - 1] : 0u;
+            uint32_t rlo = 0, rhi = 0;
+            if (found) {
+                rlo = j > xa ? cw[j - 1] : 0u;
+                rhi = cw[j];
+                bad |= (rhi - rlo) != own_hi - own_lo;
             }
+            if (COMPACT) {
+                reinterpret_cast<uint4*>(rec)[e] = make_uint4(xf, own_hi, rlo, rhi);
+            } else {
+                const uint32_t xW = xb > xa ? cw[xb - 1] : 0u;
+                uint4* r = reinterpret_cast<uint4*>(rec) + 2 * e;
+                r[0] = make_uint4(x, own_hi, rlo, rhi);
+                r[1] = make_uint4((uint32_t)xa, (uint32_t)(xb - xa) | df, xW, own_lo);
+            }
+        } else {
+            const uint32_t rev = found ? (uint32_t)(j - xa) : kNone;
+            if (COMPACT)
+                reinterpret_cast<uint2*>(rec)[e] = make_uint2(xf, rev);
+            else
+                reinterpret_cast<uint4*>(rec)[e] = make_uint4(x, rev, (uint32_t)xa, (uint32_t)(xb - xa) | df);
         }
     }
     if (WEIGHTED && bad) atomicOr(asym, 1u);
 }
 
-// Guide entries of one row per warp: bucket kb of B = G deg covers the draws
-// x64 in [ceil(kb 2^64 / B), ceil((kb+1) 2^64 / B)).  With 2^64 = Q B + R:
+// Guide entries, one thread per bucket (global bucket gb = G off[v] + kb, so v =
+// row_of(gb / G)): bucket kb of B = G deg covers the draws x64 in
+// [ceil(kb 2^64 / B), ceil((kb+1) 2^64 / B)).  With 2^64 = Q B + R:
 // ceil(kb 2^64 / B) = kb Q + ceil(kb R / B)  (kb R < B^2 < 2^64).
-// Entry {e0, e1}: e0 = i_lo | SPLIT (bit 31) | MULTI (bit 30), i_lo = the
-// proposal index of the bucket's smallest draw; unsplit: e1 = col[i_lo] (the
-// proposal itself); split: e1 = cw[i_lo], the upper end of i_lo's interval
-// (r < e1 -> i_lo, else i_lo + 1 unless MULTI: then scan the records).
-__global__ void build_guide(const uint64_t* __restrict__ off, const uint32_t* __restrict__ col,
-                            const uint32_t* __restrict__ cw, uint32_t n, uint32_t G, uint2* __restrict__ guide)
+// i_lo = the proposal index of the bucket's smallest draw; the bucket is "split"
+// when its largest draw proposes a later index (MULTI: more than one later).
+struct Bucket {
+    uint64_t lo;   // off[v]
+    uint32_t i;    // i_lo
+    bool split, multi;
+};
+
+__device__ __forceinline__ Bucket guide_bucket(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cw,
+                                               uint32_t n, uint32_t G, uint64_t gb)
 {
-    const unsigned lane = threadIdx.x & 31;
-    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t v = warp; v < n; v += nwarps) {
-        const uint64_t lo = off[v], hi = off[v + 1], deg = hi - lo;
-        if (deg == 0) continue;
-        const uint64_t B = G * deg;
-        const uint64_t W = cw[hi - 1];
-        uint64_t Q = ~0ull / B, R = ~0ull % B + 1;   // 2^64 = Q B + R, 0 <= R < B
-        if (R == B) { ++Q; R = 0; }
-        for (uint64_t kb = lane; kb < B; kb += 32) {
-            const uint64_t xmin = kb * Q + (kb * R + B - 1) / B;
-            const uint64_t xmax = kb + 1 == B ? ~0ull : (kb + 1) * Q + ((kb + 1) * R + B - 1) / B - 1;
-            const uint32_t rmin = (uint32_t)__umul64hi(xmin, W), rmax = (uint32_t)__umul64hi(xmax, W);
-            const uint64_t i = upper_bound_u32(cw, lo, hi, rmin) - lo;   // < deg since cw[hi-1] = W > rmin
-            const bool split = cw[lo + i] <= rmax;
-            const bool multi = split && cw[lo + i + 1] <= rmax;        // i + 1 < deg when split
-            guide[G * lo + kb] = make_uint2((uint32_t)i | (split ? 0x80000000u : 0u) | (multi ? 0x40000000u : 0u),
-                                            split ? cw[lo + i] : col[lo + i]);
-        }
+    const uint32_t v = build::row_of(off, n, gb >> (31 - __clz(G)));   // G is a power of two
+    const uint64_t lo = off[v], hi = off[v + 1], deg = hi - lo;
+    const uint64_t B = G * deg, kb = gb - G * lo;
+    const uint64_t W = cw[hi - 1];
+    uint64_t Q = ~0ull / B, R = ~0ull % B + 1;   // 2^64 = Q B + R, 0 <= R < B
+    if (R == B) { ++Q; R = 0; }
+    const uint64_t xmin = kb * Q + (kb * R + B - 1) / B;
+    const uint64_t xmax = kb + 1 == B ? ~0ull : (kb + 1) * Q + ((kb + 1) * R + B - 1) / B - 1;
+    const uint32_t rmin = (uint32_t)__umul64hi(xmin, W), rmax = (uint32_t)__umul64hi(xmax, W);
+    Bucket b;
+    b.lo = lo;
+    b.i = (uint32_t)(upper_bound_u32(cw, lo, hi, rmin) - lo);   // < deg since cw[hi-1] = W > rmin
+    b.split = cw[lo + b.i] <= rmax;
+    b.multi = b.split && cw[lo + b.i + 1] <= rmax;              // i + 1 < deg when split
+    return b;
+}
+
+// Slim guide (8-B entries) {e0, e1}: e0 = i_lo | SPLIT (bit 31) | MULTI (bit 30);
+// unsplit: e1 = col[i_lo] (the proposal itself); split: e1 = cw[i_lo], the upper end
+// of i_lo's interval (r < e1 -> i_lo, else i_lo + 1 unless MULTI: then scan the records).
+__global__ void build_guide(const uint64_t* __restrict__ off, const uint32_t* __restrict__ col,
+                            const uint32_t* __restrict__ cw, uint32_t n, uint64_t m, uint32_t G,
+                            uint2* __restrict__ guide)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t gb = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; gb < G * m; gb += stride) {
+        const Bucket b = guide_bucket(off, cw, n, G, gb);
+        guide[gb] = make_uint2(b.i | (b.split ? 0x80000000u : 0u) | (b.multi ? 0x40000000u : 0u),
+                               b.split ? cw[b.lo + b.i] : col[b.lo + b.i]);
     }
 }
 
@@ -169,33 +181,18 @@ __global__ void build_guide(const uint64_t* __restrict__ off, const uint32_t* __
 // bits 30-31 of word 5 (the degree of x, < 2^29) clear; a split bucket holds
 // {i_lo, cw[i_lo], 0, 0, 0, SPLIT | MULTI<<30, 0, 0}.
 __global__ void build_guide_fat(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cw, uint32_t n,
-                                uint32_t G, const uint4* __restrict__ rec, uint4* __restrict__ guide)
+                                uint64_t m, uint32_t G, const uint4* __restrict__ rec, uint4* __restrict__ guide)
 {
-    const unsigned lane = threadIdx.x & 31;
-    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t v = warp; v < n; v += nwarps) {
-        const uint64_t lo = off[v], hi = off[v + 1], deg = hi - lo;
-        if (deg == 0) continue;
-        const uint64_t B = G * deg;
-        const uint64_t W = cw[hi - 1];
-        uint64_t Q = ~0ull / B, R = ~0ull % B + 1;
-        if (R == B) { ++Q; R = 0; }
-        for (uint64_t kb = lane; kb < B; kb += 32) {
-            const uint64_t xmin = kb * Q + (kb * R + B - 1) / B;
-            const uint64_t xmax = kb + 1 == B ? ~0ull : (kb + 1) * Q + ((kb + 1) * R + B - 1) / B - 1;
-            const uint32_t rmin = (uint32_t)__umul64hi(xmin, W), rmax = (uint32_t)__umul64hi(xmax, W);
-            const uint64_t i = upper_bound_u32(cw, lo, hi, rmin) - lo;
-            const bool split = cw[lo + i] <= rmax;
-            const bool multi = split && cw[lo + i + 1] <= rmax;
-            uint4* d = guide + 2 * (G * lo + kb);
-            if (split) {
-                d[0] = make_uint4((uint32_t)i, cw[lo + i], 0u, 0u);
-                d[1] = make_uint4(0u, 0x80000000u | (multi ? 0x40000000u : 0u), 0u, 0u);
-            } else {
-                d[0] = rec[2 * (lo + i)];
-                d[1] = rec[2 * (lo + i) + 1];
-            }
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t gb = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; gb < G * m; gb += stride) {
+        const Bucket b = guide_bucket(off, cw, n, G, gb);
+        uint4* d = guide + 2 * gb;
+        if (b.split) {
+            d[0] = make_uint4(b.i, cw[b.lo + b.i], 0u, 0u);
+            d[1] = make_uint4(0u, 0x80000000u | (b.multi ? 0x40000000u : 0u), 0u, 0u);
+        } else {
+            d[0] = rec[2 * (b.lo + b.i)];
+            d[1] = rec[2 * (b.lo + b.i) + 1];
         }
     }
 }
@@ -206,35 +203,36 @@ __global__ void build_guide_fat(const uint64_t* __restrict__ off, const uint32_t
 // floor(d / H), and derivable from the node record.  x goes to the first empty slot
 // of bucket B_v + floor(fmix32(x) nb_v / 2^32), or of the next non-full bucket
 // (cyclically): a bucket that an item skipped is full forever (no deletions),
-// so a lookup may stop at the first bucket holding x or an empty slot.
+// so a lookup may stop at the first bucket holding x or an empty slot.  One
+// thread per arc.
 __global__ void build_ehash(const uint64_t* __restrict__ off, const uint32_t* __restrict__ col, uint32_t n,
-                            uint32_t H, uint32_t* __restrict__ ehash)
+                            uint64_t m, uint32_t H, uint32_t* __restrict__ ehash)
 {
-    const unsigned lane = threadIdx.x & 31;
-    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t v = warp; v < n; v += nwarps) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
+        const uint32_t v = build::row_of(off, n, e);
         const uint64_t lo = off[v], hi = off[v + 1];
         const uint64_t base = lo / H + v, nb = (hi - lo) / H + 1;
-        for (uint64_t e = lo + lane; e < hi; e += 32) {
-            const uint32_t x = col[e];
-            uint64_t b = ((uint64_t)fmix32(x) * nb) >> 32;
-            for (uint64_t tries = 0; tries < nb; ++tries) {   // nb * 8 slots >= deg + 1 > items: ends
-                uint32_t* slot = ehash + 8 * (base + b);
-                int q = 0;
-                while (q < 8 && atomicCAS(slot + q, kEmpty, x) != kEmpty) ++q;
-                if (q < 8) break;
-                b = b + 1 == nb ? 0 : b + 1;
-            }
+        const uint32_t x = col[e];
+        uint64_t b = ((uint64_t)fmix32(x) * nb) >> 32;
+        for (uint64_t tries = 0; tries < nb; ++tries) {   // nb * 8 slots >= deg + 1 > items: ends
+            uint32_t* slot = ehash + 8 * (base + b);
+            int q = 0;
+            while (q < 8 && atomicCAS(slot + q, kEmpty, x) != kEmpty) ++q;
+            if (q < 8) break;
+            b = b + 1 == nb ? 0 : b + 1;
         }
     }
 }
 
 // notri[e] for arc e = (t -> v): 1 iff no x != t in N(v) lies in N(t), i.e. at v
 // coming from t every proposal other than t itself is in class q (P:453-470:
-// X_beta = N(v) \ N(t) is all of N(v) \ {t}).  One warp per row t; each lane
-// scans the shorter of N(t), N(v) and probes the other's edge-hash set, stopping
-// at the first common neighbour.
+// X_beta = N(v) \ N(t) is all of N(v) \ {t}).  The shorter of N(t), N(v) is scanned
+// and each entry probed in the other's edge-hash set, stopping at the first common
+// neighbour.  One thread per arc; an arc whose shorter row exceeds kCoopLen entries
+// is scanned by its whole warp instead (the lanes stride over the row, the warp
+// stops as soon as any lane finds a common neighbour), so the work of a warp is
+// bounded by kCoopLen sequential probes per lane plus 1/32 of its long scans.
 __device__ inline bool hash_has(const uint32_t* __restrict__ ehash, uint64_t base, uint64_t nb, uint32_t x)
 {
     uint64_t b = ((uint64_t)fmix32(x) * nb) >> 32;
@@ -252,42 +250,62 @@ __device__ inline bool hash_has(const uint32_t* __restrict__ ehash, uint64_t bas
     return false;
 }
 
+constexpr uint64_t kCoopLen = 32;
+
 __global__ void build_notri(const uint64_t* __restrict__ off, const uint32_t* __restrict__ col, uint32_t n,
-                            uint32_t H, const uint32_t* __restrict__ ehash, uint8_t* __restrict__ notri)
+                            uint64_t m, uint32_t H, const uint32_t* __restrict__ ehash, uint8_t* __restrict__ notri)
 {
     const unsigned lane = threadIdx.x & 31;
-    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t t = warp; t < n; t += nwarps) {
-        const uint64_t ta = off[t], tb = off[t + 1];
-        for (uint64_t e = ta + lane; e < tb; e += 32) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    // every lane of a warp runs the same number of rounds (the warp-cooperative scans
+    // below need all 32 lanes): rounds over [0, m) rounded up to whole warps
+    const uint64_t m_pad = (m + 31) & ~31ull;
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m_pad; e += stride) {
+        const bool valid = e < m;
+        uint32_t t = 0, sx = 0;           // sx: the node whose set is probed
+        uint64_t sa = 0, sb = 0;          // the scanned (shorter) row
+        uint64_t hbase = 0, hnb = 0;      // the probed row's hash buckets
+        if (valid) {
+            t = build::row_of(off, n, e);
             const uint32_t v = col[e];
-            const uint64_t va = off[v], vb = off[v + 1];
-            bool common = false;
+            const uint64_t ta = off[t], tb = off[t + 1], va = off[v], vb = off[v + 1];
             if (vb - va <= tb - ta) {   // x in N(v), x != t: in N(t)?
-                const uint64_t base = ta / H + t, nb = (tb - ta) / H + 1;
-                for (uint64_t f = va; f < vb && !common; ++f) {
-                    const uint32_t x = col[f];
-                    common = x != (uint32_t)t && hash_has(ehash, base, nb, x);
-                }
+                sa = va; sb = vb; sx = t;
+                hbase = ta / H + t; hnb = (tb - ta) / H + 1;
             } else {                    // x in N(t), x != t: in N(v)?
-                const uint64_t base = va / H + v, nb = (vb - va) / H + 1;
-                for (uint64_t f = ta; f < tb && !common; ++f) {
-                    const uint32_t x = col[f];
-                    common = x != (uint32_t)t && hash_has(ehash, base, nb, x);
-                }
+                sa = ta; sb = tb; sx = v;
+                hbase = va / H + v; hnb = (vb - va) / H + 1;
             }
-            notri[e] = common ? 0 : 1;
         }
+        (void)sx;
+        bool common = false;
+        const bool coop = valid && sb - sa > kCoopLen;
+        if (valid && !coop)
+            for (uint64_t f = sa; f < sb && !common; ++f) {
+                const uint32_t x = col[f];
+                common = x != t && hash_has(ehash, hbase, hnb, x);
+            }
+        unsigned big = __ballot_sync(0xffffffffu, coop);
+        while (big) {   // the long scans, one at a time, by the whole warp
+            const int src = __ffs(big) - 1;
+            big &= big - 1;
+            const uint64_t a = __shfl_sync(0xffffffffu, sa, src), b = __shfl_sync(0xffffffffu, sb, src);
+            const uint64_t hb0 = __shfl_sync(0xffffffffu, hbase, src), hn = __shfl_sync(0xffffffffu, hnb, src);
+            const uint32_t tt = __shfl_sync(0xffffffffu, t, src);
+            bool found = false;
+            for (uint64_t f0 = a; f0 < b; f0 += 32) {   // uniform trip count across the warp
+                const uint64_t f = f0 + lane;
+                bool c = false;
+                if (f < b) {
+                    const uint32_t x = col[f];
+                    c = x != tt && hash_has(ehash, hb0, hn, x);
+                }
+                if (__any_sync(0xffffffffu, c)) { found = true; break; }
+            }
+            if ((int)lane == src) common = found;
+        }
+        if (valid) notri[e] = common ? 0 : 1;
     }
-}
-
-int rows_grid(uint64_t n)
-{
-    uint64_t blocks = (n + 7) / 8;
-    if (blocks < 1) blocks = 1;
-    if (blocks > 148 * 32) blocks = 148 * 32;
-    return (int)blocks;
 }
 
 uint64_t padded(uint64_t bytes) { return ((bytes + 31) / 32) * 32 + 32; }
@@ -407,34 +425,37 @@ grape_status build_tables(grape_graph* g, const grape_table_options& o)
     cudaMemset(g->rec, 0, rec_b);
     cudaMemset(g->ehash, 0xFF, hash_b);
     if (weighted) cudaMemset(g->guide, 0, guide_b);
-    const int grid = rows_grid(g->n);
-    build_ehash<<<grid, kThreads>>>(g->off, g->col, g->n, g->hash_h, g->ehash);
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
+    const int grid = build::item_grid(m, sms), ggrid = build::item_grid((uint64_t)G * m, sms);
+    if (m) build_ehash<<<grid, kThreads>>>(g->off, g->col, g->n, m, g->hash_h, g->ehash);
     // no-common-neighbour flags (a temporary byte per arc); compact records need n < 2^30
     uint8_t* d_notri = nullptr;
     const bool flags_ok = !(g->compact && n >= (1u << 30));
     if (flags_ok && cudaMalloc((void**)&d_notri, m ? m : 1) == cudaSuccess) {
-        build_notri<<<grid, kThreads>>>(g->off, g->col, g->n, g->hash_h, g->ehash, d_notri);
+        if (m) build_notri<<<grid, kThreads>>>(g->off, g->col, g->n, m, g->hash_h, g->ehash, d_notri);
     } else {
         cudaGetLastError();
         d_notri = nullptr;
     }
-    if (weighted) {
+    if (m == 0) {
+    } else if (weighted) {
         if (g->compact)
-            build_records<true, true><<<grid, kThreads>>>(g->off, g->col, (const uint32_t*)g->cw, g->n, g->rec, d_asym,
-                                                          d_notri);
+            build_records<true, true><<<grid, kThreads>>>(g->off, g->col, (const uint32_t*)g->cw, g->n, m, g->rec,
+                                                          d_asym, d_notri);
         else
-            build_records<true, false><<<grid, kThreads>>>(g->off, g->col, (const uint32_t*)g->cw, g->n, g->rec, d_asym,
-                                                           d_notri);
+            build_records<true, false><<<grid, kThreads>>>(g->off, g->col, (const uint32_t*)g->cw, g->n, m, g->rec,
+                                                           d_asym, d_notri);
         if (gbytes == 32)
-            build_guide_fat<<<grid, kThreads>>>(g->off, (const uint32_t*)g->cw, g->n, G, (const uint4*)g->rec,
-                                                (uint4*)g->guide);
+            build_guide_fat<<<ggrid, kThreads>>>(g->off, (const uint32_t*)g->cw, g->n, m, G, (const uint4*)g->rec,
+                                                 (uint4*)g->guide);
         else
-            build_guide<<<grid, kThreads>>>(g->off, g->col, (const uint32_t*)g->cw, g->n, G, (uint2*)g->guide);
+            build_guide<<<ggrid, kThreads>>>(g->off, g->col, (const uint32_t*)g->cw, g->n, m, G, (uint2*)g->guide);
     } else {
         if (g->compact)
-            build_records<false, true><<<grid, kThreads>>>(g->off, g->col, nullptr, g->n, g->rec, d_asym, d_notri);
+            build_records<false, true><<<grid, kThreads>>>(g->off, g->col, nullptr, g->n, m, g->rec, d_asym, d_notri);
         else
-            build_records<false, false><<<grid, kThreads>>>(g->off, g->col, nullptr, g->n, g->rec, d_asym, d_notri);
+            build_records<false, false><<<grid, kThreads>>>(g->off, g->col, nullptr, g->n, m, g->rec, d_asym, d_notri);
     }
     g->notri = d_notri != nullptr;
     if (d_notri) {

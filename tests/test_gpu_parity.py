@@ -287,7 +287,7 @@ def test_full_size_config_sampled(grape, k, mode):
         assert np.array_equal(host_out[r], exp[0]), int(i)
     # the GPU rows of walks from sinks (directed configs): [start, PAD, ...]
     if len(sinks):
-        assert k == 5 and len(sinks) == 100
+        assert len(sinks) == 100   # cfg3: isolated nodes; cfg5: the 5% sinks
         at = {int(i): r for r, i in enumerate(sample)}
         for it in range(wk["walks_per_node"]):
             for s_ in sinks:
