@@ -285,6 +285,59 @@ grape_status grape_walks_node2vec_folded(const grape_graph* g, const uint32_t* s
 grape_status grape_graph_partition(grape_graph* g, uint32_t parts, const int* devices);
 
 /*
+ * Distributed table build — the §8(f) f4 row for graphs whose sampling tables
+ * exceed one GPU (the paper's ClueWeb09 / sk-2005 scale, P:80,
+ * P:288).  One process per GPU ("rank" j of `parts`), each holding the whole CSR
+ * (8 bytes per arc) and owning part j of every table (records, guide, edge hash:
+ * power-of-two byte ranges, as grape_graph_partition lays them out).  The ranks
+ * exchange CUDA IPC handles of their parts and build in four stages; every rank
+ * then walks over all parts (peer parts over NVLink, or the same GPU's memory
+ * when ranks share a device), bit-identical to the single-GPU tables.  The ABI
+ * runs no collective: the caller moves the exports between ranks and puts a
+ * barrier where marked (paper_2110_06196_b200.graph_from_csr_dist does both over
+ * torch.distributed).  Sequence, on every rank:
+ *   grape_graph_dist_create(..., part = rank, parts = world)
+ *   grape_graph_dist_export -> all-gather -> grape_graph_dist_import(all exports)
+ *   for stage in 0..3: grape_graph_dist_build(stage), barrier
+ *   grape_graph_dist_finish(OR over ranks of the build's flags_out)
+ * and before any rank calls grape_graph_free: a barrier (peers read its parts).
+ * Only the default walk rules run on the result (as after grape_graph_partition).
+ */
+typedef struct { unsigned char bytes[64]; } grape_ipc_handle;   /* a cudaIpcMemHandle_t */
+
+typedef struct {
+    uint32_t part;            /* the exporting rank's part index */
+    int device;               /* its CUDA device */
+    uint64_t bytes[4];        /* bytes of its part of: 0 records, 1 guide, 2 edge hash, 3 build flags */
+    grape_ipc_handle handle[4];   /* IPC handles of those parts (valid where bytes > 0) */
+} grape_part_export;
+
+/* Rank `part` of `parts` (2..8): copy and validate the CSR (as grape_graph_from_csr_opts;
+ * same arguments on every rank), choose the table layout for parts x
+ * opts->table_budget_bytes bytes (required, equal on every rank, so every rank
+ * chooses the same layout; forced fields as in grape_table_options) and allocate
+ * this rank's parts.  Synchronous.  EINVAL: bad arguments, table_budget_bytes = 0,
+ * GRAPE_NO_TABLES, a graph outside the tables' index ranges; ENOMEM: no layout fits
+ * (or allocation failed); ECUDA. */
+grape_status grape_graph_dist_create(uint32_t num_nodes, uint64_t num_arcs, const uint64_t* row_offsets,
+                                     const uint32_t* col_indices, const uint32_t* weights, int device,
+                                     uint32_t flags, const grape_table_options* opts, uint32_t part,
+                                     uint32_t parts, grape_graph** out);
+/* IPC handles of this rank's parts into *out (host memory). */
+grape_status grape_graph_dist_export(const grape_graph* g, grape_part_export* out);
+/* Open every other rank's parts: exports[j] = rank j's export, j = 0 .. parts-1.
+ * EINVAL when an export's sizes differ from this rank's layout (different graphs). */
+grape_status grape_graph_dist_import(grape_graph* g, const grape_part_export* exports);
+/* Build stage 0 (edge hash), 1 (no-common-neighbour flags), 2 (records) or 3 (guide)
+ * of this rank's parts; synchronous; every rank must finish stage k before any
+ * starts stage k+1 (barrier).  *flags_out (may be NULL): bit 0 = a reverse arc of
+ * different weight was seen (stage 2). */
+grape_status grape_graph_dist_build(grape_graph* g, uint32_t stage, uint32_t* flags_out);
+/* flags_all = OR over ranks of stage 2's flags_out.  Releases the CSR copy; the
+ * graph then walks.  EINVAL when called twice or before import. */
+grape_status grape_graph_dist_finish(grape_graph* g, uint32_t flags_all);
+
+/*
  * grape_skipgram_pairs — the SkipGram consumer of a walk matrix (SURVEY §8(f)
  * row f3): the (center, context) pairs of the sliding window
  * ("given a window size, these models learn ... the co-occurrence of two nodes

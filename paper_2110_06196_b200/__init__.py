@@ -125,11 +125,21 @@ class Graph:
         return self
 
     def free(self) -> None:
+        """grape_graph_free.  A distributed graph (graph_from_csr_dist) waits for every rank
+        first: the peers read this rank's table parts until they are done walking."""
         if self._h is not None and self._h.value:
+            grp = getattr(self, "_group", False)
+            if grp is not False:
+                import torch.distributed as dist
+                if dist.is_initialized():
+                    torch.cuda.synchronize(self.device)
+                    dist.barrier(group=grp)
             _capi.check(_lib, _lib.grape_graph_free(self._h), "grape_graph_free")
         self._h = None
 
     def __del__(self):
+        if getattr(self, "_group", False) is not False:
+            return   # distributed: free() waits for the peers; never from a finaliser
         try:
             self.free()
         except Exception:
@@ -163,6 +173,77 @@ def graph_from_csr(row_offsets, col_indices, weights=None, *, device: int = 0,
                                         None if opts is None else ctypes.byref(opts), ctypes.byref(h))
     _capi.check(_lib, st, "grape_graph_from_csr")
     return Graph(h.value, device)
+
+
+def graph_from_csr_dist(row_offsets, col_indices, weights=None, *, device: int, symmetric: bool = False,
+                        validate: bool = True, layout: dict | None = None, table_budget_bytes: int | None = None,
+                        group=None) -> Graph:
+    """Distributed table build (grape_graph_dist_*; §8(f) f4): every rank of
+    the torch.distributed group calls this with the same CSR; rank r owns part r of the
+    sampling tables, and the returned graph walks over all parts (the peers' over
+    NVLink / CUDA IPC), bit-identical to graph_from_csr's.  table_budget_bytes: table
+    bytes per rank (default: the smallest free device memory over the ranks, less 10%
+    of the device); the layout is chosen for world x that.  This function supplies the
+    handle exchange (all_gather_object) and the barriers the C-ABI asks for; it runs
+    no collective on the walk path.  Free with Graph.free() on every rank (a barrier
+    first: peers read this rank's parts)."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    off = _as_tensor(row_offsets, torch.int64)
+    col = _as_tensor(col_indices, torch.int32)
+    w = None if weights is None else _as_tensor(weights, torch.int32)
+    n, m = off.numel() - 1, col.numel()
+    if table_budget_bytes is None:
+        with torch.cuda.device(device):
+            free, total = torch.cuda.mem_get_info(device)
+        mine = [int(free - 0.1 * total)]
+        allv = [None] * world
+        dist.all_gather_object(allv, mine[0], group=group)
+        table_budget_bytes = max(1, min(allv))
+    opts = _capi.TableOptions(**(layout or {}))
+    opts.table_budget_bytes = int(table_budget_bytes)
+    flags = (GRAPE_SYMMETRIC if symmetric else 0) | (0 if validate else GRAPE_SKIP_VALIDATION)
+    h = ctypes.c_void_p()
+    st = _lib.grape_graph_dist_create(n, m, off.data_ptr(), col.data_ptr() if m else None,
+                                      None if w is None else w.data_ptr(), device, flags, ctypes.byref(opts),
+                                      rank, world, ctypes.byref(h))
+    ok = [st == GRAPE_OK]
+    oks = [None] * world
+    dist.all_gather_object(oks, ok[0], group=group)
+    if not all(oks):   # every rank stops together (no rank left waiting in a collective)
+        if st == GRAPE_OK:
+            _lib.grape_graph_free(h)
+            raise GrapeError(GRAPE_EINVAL, "grape_graph_dist_create failed on another rank")
+        _capi.check(_lib, st, "grape_graph_dist_create")
+    g = Graph.__new__(Graph)
+    g._h = h
+    g.device = device
+    g._group = group
+    ex = _capi.PartExport()
+    _capi.check(_lib, _lib.grape_graph_dist_export(h, ctypes.byref(ex)), "grape_graph_dist_export")
+    allx = [None] * world
+    dist.all_gather_object(allx, bytes(ex), group=group)
+    arr = (_capi.PartExport * world)()
+    for x in allx:
+        e = _capi.PartExport.from_buffer_copy(x)
+        arr[e.part] = e
+    _capi.check(_lib, _lib.grape_graph_dist_import(h, arr), "grape_graph_dist_import")
+    dist.barrier(group=group)   # every rank has opened every part
+    fl = ctypes.c_uint32(0)
+    flags_all = 0
+    for stage in range(4):
+        _capi.check(_lib, _lib.grape_graph_dist_build(h, stage, ctypes.byref(fl)), "grape_graph_dist_build")
+        flv = [None] * world
+        dist.all_gather_object(flv, int(fl.value), group=group)   # (also the stage barrier)
+        for v in flv:
+            flags_all |= v
+    _capi.check(_lib, _lib.grape_graph_dist_finish(h, flags_all), "grape_graph_dist_finish")
+    info = _capi.GraphInfo()
+    _capi.check(_lib, _lib.grape_graph_get_info(h, ctypes.byref(info)), "grape_graph_get_info")
+    g.info = {f: getattr(info, f) for f, _ in _capi.GraphInfo._fields_}
+    g.info["dist_part"] = rank
+    return g
 
 
 def _walks(fn_name, g: Graph, starts, L, args, seed, walk_id_base, out, steps, stream):

@@ -23,6 +23,8 @@ EXPORTS = (
     "grape_graph_from_csr", "grape_graph_from_csr_opts", "grape_graph_free", "grape_graph_get_info",
     "grape_walks_first_order", "grape_walks_node2vec", "grape_walks_approx", "grape_walks_node2vec_cdf", "grape_walks_node2vec_folded",
     "grape_skipgram_pairs", "grape_graph_partition",
+    "grape_graph_dist_create", "grape_graph_dist_export", "grape_graph_dist_import", "grape_graph_dist_build",
+    "grape_graph_dist_finish",
     "grape_walks_stats",
     "grape_walks_stats_ex",
     "grape_status_string", "grape_last_error", "grape_version",
@@ -59,6 +61,19 @@ class TableOptions(ctypes.Structure):
         ("guide_bytes", ctypes.c_uint32),
         ("guide_factor", ctypes.c_uint32),
         ("hash_h", ctypes.c_uint32),
+    ]
+
+
+class IpcHandle(ctypes.Structure):
+    _fields_ = [("bytes", ctypes.c_ubyte * 64)]
+
+
+class PartExport(ctypes.Structure):
+    _fields_ = [
+        ("part", ctypes.c_uint32),
+        ("device", ctypes.c_int),
+        ("bytes", ctypes.c_uint64 * 4),
+        ("handle", IpcHandle * 4),
     ]
 
 
@@ -110,6 +125,17 @@ def load(path: str | None = None) -> ctypes.CDLL:
     lib.grape_skipgram_pairs.restype = i32
     lib.grape_graph_partition.argtypes = [vp, u32, vp]
     lib.grape_graph_partition.restype = i32
+    lib.grape_graph_dist_create.argtypes = [u32, u64, vp, vp, vp, i32, u32, ctypes.POINTER(TableOptions), u32, u32,
+                                            ctypes.POINTER(vp)]
+    lib.grape_graph_dist_create.restype = i32
+    lib.grape_graph_dist_export.argtypes = [vp, ctypes.POINTER(PartExport)]
+    lib.grape_graph_dist_export.restype = i32
+    lib.grape_graph_dist_import.argtypes = [vp, ctypes.POINTER(PartExport)]
+    lib.grape_graph_dist_import.restype = i32
+    lib.grape_graph_dist_build.argtypes = [vp, u32, ctypes.POINTER(u32)]
+    lib.grape_graph_dist_build.restype = i32
+    lib.grape_graph_dist_finish.argtypes = [vp, u32]
+    lib.grape_graph_dist_finish.restype = i32
     lib.grape_walks_stats.argtypes = [vp, vp, u64, u64, u32, i32, dbl, dbl, u64, vp,
                                       ctypes.POINTER(WalkStats), vp]
     lib.grape_walks_stats.restype = i32

@@ -268,6 +268,10 @@ grape_status walks_common(const grape_graph* g, const uint32_t* starts, uint64_t
         set_error("a partitioned graph (grape_graph_partition) serves the default walk rules only");
         return GRAPE_EINVAL;
     }
+    if (g->dist && !g->tables) {
+        set_error("a distributed graph walks after grape_graph_dist_finish");
+        return GRAPE_EINVAL;
+    }
     int cur = -1;
     if (cudaGetDevice(&cur) != cudaSuccess) { cudaGetLastError(); cur = -1; }
     if (cur != g->device) {
@@ -308,16 +312,13 @@ using namespace grape;
 
 extern "C" {
 
-grape_status grape_graph_from_csr_opts(uint32_t num_nodes, uint64_t num_arcs, const uint64_t* row_offsets,
-                                       const uint32_t* col_indices, const uint32_t* weights, int device,
-                                       uint32_t flags, const grape_table_options* opts, grape_graph** out)
+}  // extern "C"
+
+namespace grape {
+grape_status check_build_args(uint32_t num_nodes, uint64_t num_arcs, const uint64_t* row_offsets,
+                              const uint32_t* col_indices, const uint32_t* weights, int device, uint32_t flags,
+                              const grape_table_options* opts)
 {
-    g_err[0] = 0;
-    if (out == nullptr) {
-        set_error("out must be non-NULL");
-        return GRAPE_EINVAL;
-    }
-    *out = nullptr;
     if (row_offsets == nullptr || (num_arcs > 0 && col_indices == nullptr)) {
         set_error("row_offsets and col_indices must be non-NULL");
         return GRAPE_EINVAL;
@@ -353,6 +354,27 @@ grape_status grape_graph_from_csr_opts(uint32_t num_nodes, uint64_t num_arcs, co
             return GRAPE_EINVAL;
         }
     }
+    return GRAPE_OK;
+}
+}  // namespace grape
+
+extern "C" {
+
+grape_status grape_graph_from_csr_opts(uint32_t num_nodes, uint64_t num_arcs, const uint64_t* row_offsets,
+                                       const uint32_t* col_indices, const uint32_t* weights, int device,
+                                       uint32_t flags, const grape_table_options* opts, grape_graph** out)
+{
+    g_err[0] = 0;
+    if (out == nullptr) {
+        set_error("out must be non-NULL");
+        return GRAPE_EINVAL;
+    }
+    *out = nullptr;
+    const grape_status st = check_build_args(num_nodes, num_arcs, row_offsets, col_indices, weights, device, flags,
+                                             opts);
+    if (st != GRAPE_OK) return st;
+    grape_table_options o{};
+    if (opts != nullptr) o = *opts;
     return build_graph(num_nodes, num_arcs, row_offsets, col_indices, weights, device, flags, o, out);
 }
 
@@ -526,6 +548,10 @@ grape_status grape_walks_stats_ex(const grape_graph* g, const uint32_t* starts, 
     }
     if (g->parts > 1 && (dT != 0 || sampler != 0)) {
         set_error("a partitioned graph (grape_graph_partition) serves the default walk rules only");
+        return GRAPE_EINVAL;
+    }
+    if (g->dist && !g->tables) {
+        set_error("a distributed graph walks after grape_graph_dist_finish");
         return GRAPE_EINVAL;
     }
     if (sampler != 0 && (sampler != 2 || !g->tables || dT != 0 || !node2vec ||

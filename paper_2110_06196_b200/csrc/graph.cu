@@ -190,12 +190,25 @@ void destroy_graph(grape_graph* g)
     cudaFree(g->stage_buf);
     cudaFree(g->node_guide);
     cudaFree(g->part_map);
-    for (int t = 0; t < 4; ++t)   // partitioned tables (the contiguous pointers are NULL then)
+    // partitioned tables (the contiguous pointers are NULL then): parts this process
+    // allocated are freed; parts opened from another process (distributed build,
+    // dist.cu) are closed; aliases of an earlier part are skipped
+    static const int ipc_t[4] = {0, 1, -1, 2};   // PartMap table -> dist.cu exchange index
+    for (int t = 0; t < 4; ++t)
         for (int j = 0; j < (int)g->parts && g->parts > 1; ++j) {
-            bool dup = false;
+            bool dup = g->part_mem[t][j] == nullptr;
             for (int q = 0; q < j; ++q) dup |= g->part_mem[t][q] == g->part_mem[t][j];
-            if (!dup) cudaFree(g->part_mem[t][j]);
+            if (dup) continue;
+            if (ipc_t[t] >= 0 && g->part_ipc[ipc_t[t]][j]) cudaIpcCloseMemHandle(g->part_mem[t][j]);
+            else cudaFree(g->part_mem[t][j]);
         }
+    for (int j = 0; j < (int)g->parts && g->dist; ++j) {   // the build's flag parts
+        bool dup = g->notri_mem[j] == nullptr;
+        for (int q = 0; q < j; ++q) dup |= g->notri_mem[q] == g->notri_mem[j];
+        if (dup) continue;
+        if (g->part_ipc[3][j]) cudaIpcCloseMemHandle(g->notri_mem[j]);
+        else cudaFree(g->notri_mem[j]);
+    }
     for (int l = 0; l < kFenceLevels; ++l) {
         cudaFree(g->col_fence[l]);
         cudaFree(g->cw_fence[l]);
@@ -326,6 +339,15 @@ grape_status build_graph(uint32_t n, uint64_t m, const uint64_t* off_in, const u
     GRAPE_TRY_CUDA(cudaDeviceSynchronize(), "graph build");
     cudaFree(w);   // the prefix sums hold everything the walkers need from the weights
     w = nullptr;
+    if (flags & kCsrOnly) {   // dist.cu builds the tables; keep col / cw for it
+        cudaFree(d_bad);
+        cudaFree(d_maxw);
+        cudaFree(d_maxdeg);
+        g->device_bytes = (n + 1ull) * 8 + (uint64_t)n * sizeof(NodeRec) + padded(m * 4) +
+                          (g->cw_bytes ? padded(m * g->cw_bytes) : 0);
+        *out = g;
+        return GRAPE_OK;
+    }
     if (!(flags & GRAPE_NO_TABLES)) {
         st = build_tables(g, opts);
         if (st != GRAPE_OK) return fail(st);

@@ -76,21 +76,22 @@ __device__ inline uint64_t upper_bound_u32(const uint32_t* __restrict__ cw, uint
     return a;
 }
 
-// One thread per arc (build_common.cuh: hub rows do not leave a tail).  Each record
-// also carries the node record of its head x (start, degree, W_x), so a walk that
-// takes the arc needs no separate node load.
+// One thread per arc of [e_lo, e_hi) (build_common.cuh: hub rows do not leave a
+// tail).  Each record also carries the node record of its head x (start, degree,
+// W_x), so a walk that takes the arc needs no separate node load.
 // Flags of arc e = (v -> x) (rev = its reverse arc): NOTRI_SELF = notri[e] (used on
 // arriving at x through e), NOTRI_REV = notri[rev] (used on a register-decided return
 // x -> v).  Full records keep them in bits 29 / 28 of the degree word, compact records
 // in bits 31 / 30 of x (only when n < 2^30; else never set).
 template <bool WEIGHTED, bool COMPACT>
 __global__ void build_records(const uint64_t* __restrict__ off, const uint32_t* __restrict__ col,
-                              const uint32_t* __restrict__ cw, uint32_t n, uint64_t m, void* __restrict__ rec,
-                              unsigned* __restrict__ asym, const uint8_t* __restrict__ notri)
+                              const uint32_t* __restrict__ cw, uint32_t n, uint64_t e_lo, uint64_t e_hi,
+                              const TabRef rec, unsigned* __restrict__ asym, const TabRef notri)
 {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const bool flags = notri.base[0] != nullptr;
     bool bad = false;
-    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
+    for (uint64_t e = e_lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < e_hi; e += stride) {
         const uint32_t v = build::row_of(off, n, e);
         const uint64_t lo = off[v];
         const uint32_t x = col[e];
@@ -98,7 +99,7 @@ __global__ void build_records(const uint64_t* __restrict__ off, const uint32_t* 
         const uint64_t j = lower_bound_u32(col, xa, xb, v);
         const bool found = j < xb && col[j] == v;
         uint32_t fl = 0;   // flag bits (0: self, 1: reverse)
-        if (notri != nullptr) fl = (notri[e] ? 1u : 0u) | (found && notri[j] ? 2u : 0u);
+        if (flags) fl = (*notri.at(e) ? 1u : 0u) | (found && *notri.at(j) ? 2u : 0u);
         const uint32_t xf = COMPACT ? (x | (fl & 1) << 31 | (fl >> 1) << 30) : x;   // compact: bits 31 (self), 30 (rev)
         const uint32_t df = COMPACT ? 0u : ((fl & 1) << 29 | (fl >> 1) << 28);   // full: bits 29, 28 of deg
         if (WEIGHTED) {
@@ -111,26 +112,26 @@ __global__ void build_records(const uint64_t* __restrict__ off, const uint32_t* 
                 bad |= (rhi - rlo) != own_hi - own_lo;
             }
             if (COMPACT) {
-                reinterpret_cast<uint4*>(rec)[e] = make_uint4(xf, own_hi, rlo, rhi);
+                *reinterpret_cast<uint4*>(rec.at(16 * e)) = make_uint4(xf, own_hi, rlo, rhi);
             } else {
                 const uint32_t xW = xb > xa ? cw[xb - 1] : 0u;
-                uint4* r = reinterpret_cast<uint4*>(rec) + 2 * e;
+                uint4* r = reinterpret_cast<uint4*>(rec.at(32 * e));   // one sector: never split by a part
                 r[0] = make_uint4(x, own_hi, rlo, rhi);
                 r[1] = make_uint4((uint32_t)xa, (uint32_t)(xb - xa) | df, xW, own_lo);
             }
         } else {
             const uint32_t rev = found ? (uint32_t)(j - xa) : kNone;
             if (COMPACT)
-                reinterpret_cast<uint2*>(rec)[e] = make_uint2(xf, rev);
+                *reinterpret_cast<uint2*>(rec.at(8 * e)) = make_uint2(xf, rev);
             else
-                reinterpret_cast<uint4*>(rec)[e] = make_uint4(x, rev, (uint32_t)xa, (uint32_t)(xb - xa) | df);
+                *reinterpret_cast<uint4*>(rec.at(16 * e)) = make_uint4(x, rev, (uint32_t)xa, (uint32_t)(xb - xa) | df);
         }
     }
     if (WEIGHTED && bad) atomicOr(asym, 1u);
 }
 
-// Guide entries, one thread per bucket (global bucket gb = G off[v] + kb, so v =
-// row_of(gb / G)): bucket kb of B = G deg covers the draws x64 in
+// Guide entries, one thread per bucket of [b_lo, b_hi) (global bucket gb = G off[v]
+// + kb, so v = row_of(gb / G)): bucket kb of B = G deg covers the draws x64 in
 // [ceil(kb 2^64 / B), ceil((kb+1) 2^64 / B)).  With 2^64 = Q B + R:
 // ceil(kb 2^64 / B) = kb Q + ceil(kb R / B)  (kb R < B^2 < 2^64).
 // i_lo = the proposal index of the bucket's smallest draw; the bucket is "split"
@@ -165,14 +166,15 @@ __device__ __forceinline__ Bucket guide_bucket(const uint64_t* __restrict__ off,
 // unsplit: e1 = col[i_lo] (the proposal itself); split: e1 = cw[i_lo], the upper end
 // of i_lo's interval (r < e1 -> i_lo, else i_lo + 1 unless MULTI: then scan the records).
 __global__ void build_guide(const uint64_t* __restrict__ off, const uint32_t* __restrict__ col,
-                            const uint32_t* __restrict__ cw, uint32_t n, uint64_t m, uint32_t G,
-                            uint2* __restrict__ guide)
+                            const uint32_t* __restrict__ cw, uint32_t n, uint64_t b_lo, uint64_t b_hi, uint32_t G,
+                            const TabRef guide)
 {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t gb = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; gb < G * m; gb += stride) {
+    for (uint64_t gb = b_lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; gb < b_hi; gb += stride) {
         const Bucket b = guide_bucket(off, cw, n, G, gb);
-        guide[gb] = make_uint2(b.i | (b.split ? 0x80000000u : 0u) | (b.multi ? 0x40000000u : 0u),
-                               b.split ? cw[b.lo + b.i] : col[b.lo + b.i]);
+        *reinterpret_cast<uint2*>(guide.at(8 * gb)) =
+            make_uint2(b.i | (b.split ? 0x80000000u : 0u) | (b.multi ? 0x40000000u : 0u),
+                       b.split ? cw[b.lo + b.i] : col[b.lo + b.i]);
     }
 }
 
@@ -181,18 +183,19 @@ __global__ void build_guide(const uint64_t* __restrict__ off, const uint32_t* __
 // bits 30-31 of word 5 (the degree of x, < 2^29) clear; a split bucket holds
 // {i_lo, cw[i_lo], 0, 0, 0, SPLIT | MULTI<<30, 0, 0}.
 __global__ void build_guide_fat(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cw, uint32_t n,
-                                uint64_t m, uint32_t G, const uint4* __restrict__ rec, uint4* __restrict__ guide)
+                                uint64_t b_lo, uint64_t b_hi, uint32_t G, const TabRef rec, const TabRef guide)
 {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t gb = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; gb < G * m; gb += stride) {
+    for (uint64_t gb = b_lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; gb < b_hi; gb += stride) {
         const Bucket b = guide_bucket(off, cw, n, G, gb);
-        uint4* d = guide + 2 * gb;
+        uint4* d = reinterpret_cast<uint4*>(guide.at(32 * gb));
         if (b.split) {
             d[0] = make_uint4(b.i, cw[b.lo + b.i], 0u, 0u);
             d[1] = make_uint4(0u, 0x80000000u | (b.multi ? 0x40000000u : 0u), 0u, 0u);
         } else {
-            d[0] = rec[2 * (b.lo + b.i)];
-            d[1] = rec[2 * (b.lo + b.i) + 1];
+            const uint4* r = reinterpret_cast<const uint4*>(rec.at(32 * (b.lo + b.i)));
+            d[0] = r[0];
+            d[1] = r[1];
         }
     }
 }
@@ -204,19 +207,19 @@ __global__ void build_guide_fat(const uint64_t* __restrict__ off, const uint32_t
 // of bucket B_v + floor(fmix32(x) nb_v / 2^32), or of the next non-full bucket
 // (cyclically): a bucket that an item skipped is full forever (no deletions),
 // so a lookup may stop at the first bucket holding x or an empty slot.  One
-// thread per arc.
+// thread per arc of [h_lo, h_hi) (whole rows: one builder owns a row's buckets).
 __global__ void build_ehash(const uint64_t* __restrict__ off, const uint32_t* __restrict__ col, uint32_t n,
-                            uint64_t m, uint32_t H, uint32_t* __restrict__ ehash)
+                            uint64_t h_lo, uint64_t h_hi, uint32_t H, const TabRef ehash)
 {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
+    for (uint64_t e = h_lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < h_hi; e += stride) {
         const uint32_t v = build::row_of(off, n, e);
         const uint64_t lo = off[v], hi = off[v + 1];
         const uint64_t base = lo / H + v, nb = (hi - lo) / H + 1;
         const uint32_t x = col[e];
         uint64_t b = ((uint64_t)fmix32(x) * nb) >> 32;
         for (uint64_t tries = 0; tries < nb; ++tries) {   // nb * 8 slots >= deg + 1 > items: ends
-            uint32_t* slot = ehash + 8 * (base + b);
+            uint32_t* slot = reinterpret_cast<uint32_t*>(ehash.at(32 * (base + b)));   // a bucket is one sector
             int q = 0;
             while (q < 8 && atomicCAS(slot + q, kEmpty, x) != kEmpty) ++q;
             if (q < 8) break;
@@ -233,11 +236,11 @@ __global__ void build_ehash(const uint64_t* __restrict__ off, const uint32_t* __
 // is scanned by its whole warp instead (the lanes stride over the row, the warp
 // stops as soon as any lane finds a common neighbour), so the work of a warp is
 // bounded by kCoopLen sequential probes per lane plus 1/32 of its long scans.
-__device__ inline bool hash_has(const uint32_t* __restrict__ ehash, uint64_t base, uint64_t nb, uint32_t x)
+__device__ inline bool hash_has(const TabRef& ehash, uint64_t base, uint64_t nb, uint32_t x)
 {
     uint64_t b = ((uint64_t)fmix32(x) * nb) >> 32;
     for (uint64_t tries = 0; tries < nb; ++tries) {
-        const uint32_t* slot = ehash + 8 * (base + b);
+        const uint32_t* slot = reinterpret_cast<const uint32_t*>(ehash.at(32 * (base + b)));
         bool empty = false;
         for (int q = 0; q < 8; ++q) {
             const uint32_t y = slot[q];
@@ -253,16 +256,17 @@ __device__ inline bool hash_has(const uint32_t* __restrict__ ehash, uint64_t bas
 constexpr uint64_t kCoopLen = 32;
 
 __global__ void build_notri(const uint64_t* __restrict__ off, const uint32_t* __restrict__ col, uint32_t n,
-                            uint64_t m, uint32_t H, const uint32_t* __restrict__ ehash, uint8_t* __restrict__ notri)
+                            uint64_t e_lo, uint64_t e_hi, uint32_t H, const TabRef ehash, const TabRef notri)
 {
     const unsigned lane = threadIdx.x & 31;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     // every lane of a warp runs the same number of rounds (the warp-cooperative scans
-    // below need all 32 lanes): rounds over [0, m) rounded up to whole warps
-    const uint64_t m_pad = (m + 31) & ~31ull;
-    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m_pad; e += stride) {
-        const bool valid = e < m;
-        uint32_t t = 0, sx = 0;           // sx: the node whose set is probed
+    // below need all 32 lanes): rounds over [e_lo, e_hi) rounded up to whole warps
+    const uint64_t span = ((e_hi - e_lo) + 31) & ~31ull;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < span; k += stride) {
+        const uint64_t e = e_lo + k;
+        const bool valid = e < e_hi;
+        uint32_t t = 0;
         uint64_t sa = 0, sb = 0;          // the scanned (shorter) row
         uint64_t hbase = 0, hnb = 0;      // the probed row's hash buckets
         if (valid) {
@@ -270,14 +274,13 @@ __global__ void build_notri(const uint64_t* __restrict__ off, const uint32_t* __
             const uint32_t v = col[e];
             const uint64_t ta = off[t], tb = off[t + 1], va = off[v], vb = off[v + 1];
             if (vb - va <= tb - ta) {   // x in N(v), x != t: in N(t)?
-                sa = va; sb = vb; sx = t;
+                sa = va; sb = vb;
                 hbase = ta / H + t; hnb = (tb - ta) / H + 1;
             } else {                    // x in N(t), x != t: in N(v)?
-                sa = ta; sb = tb; sx = v;
+                sa = ta; sb = tb;
                 hbase = va / H + v; hnb = (vb - va) / H + 1;
             }
         }
-        (void)sx;
         bool common = false;
         const bool coop = valid && sb - sa > kCoopLen;
         if (valid && !coop)
@@ -304,11 +307,19 @@ __global__ void build_notri(const uint64_t* __restrict__ off, const uint32_t* __
             }
             if ((int)lane == src) common = found;
         }
-        if (valid) notri[e] = common ? 0 : 1;
+        if (valid) *reinterpret_cast<uint8_t*>(notri.at(e)) = common ? 0 : 1;
     }
 }
 
 uint64_t padded(uint64_t bytes) { return ((bytes + 31) / 32) * 32 + 32; }
+
+TabRef flat(void* p)
+{
+    TabRef t{};
+    t.base[0] = (char*)p;
+    t.shift = 63;
+    return t;
+}
 
 }  // namespace
 
@@ -332,36 +343,26 @@ void destroy_tables(grape_graph* g)
 // Random-sector gather rate falls off a cliff once the randomly read footprint
 // exceeds ~68 GB on B200 (36 G sectors/s up to 68 GB, 28 at 80 GB, 10.5 at 128 GB;
 // tools/gather_footprint.cu, profiles/gather_footprint.txt; page size does not
-// move it, tools/gather_vmm.cu).  The layout is chosen to stay below it.
+// move it, tools/gather_vmm.cu).  The automatic layout stays below it.
 constexpr double kReachBytes = 68e9;
 
-grape_status build_tables(grape_graph* g, const grape_table_options& o)
+bool tables_in_range(const grape_graph* g)
+{
+    const uint64_t m = g->m, n = g->n;
+    return !(2 * m >= (1ull << 32) - 64 || (m >> 2) + n + 2 >= (1ull << 32) || g->max_degree >= (1u << 28) ||
+             g->cw_bytes == 8);
+}
+
+// Layout, in order of preference (fewest reads per step first): records with the
+// head's node record (32 / 16 B) or compact (16 / 8 B, the head's node record read
+// separately); fat (32-B) or slim (8-B) guide entries with G = 16 / 8 / 4 / 2 / 1
+// buckets per arc; edge-hash load 1/2 (H = 4) or 3/4 (H = 6).  The first that fits
+// `budget` wins (grape_table_options may force any part).  Results do not depend
+// on the choice; the number and spread of the reads do.
+int choose_layout(grape_graph* g, const grape_table_options& o, double budget)
 {
     const uint64_t m = g->m, n = g->n;
     const bool weighted = g->cw_bytes != 0;
-    if (2 * m >= (1ull << 32) - 64 || (m >> 2) + n + 2 >= (1ull << 32) || g->max_degree >= (1u << 28) ||
-        g->cw_bytes == 8)
-        return GRAPE_OK;
-    cudaError_t e = cudaSuccess;
-    unsigned* d_asym = nullptr;
-    auto fail = [&](cudaError_t err, const char* what) {
-        cudaFree(d_asym);
-        destroy_tables(g);
-        return cuda_fail(err, what);
-    };
-    // Layout, in order of preference (fewest reads per step first): records
-    // with the head's node record (32 / 16 B) or compact (16 / 8 B, the head's
-    // node record read separately); fat (32-B) or slim (8-B) guide entries with
-    // G = 16 / 8 / 4 / 2 / 1 buckets per arc; edge-hash load 1/2 (H = 4) or 3/4 (H = 6).
-    // The first that fits both the device (leaving 10% free: the caller still
-    // needs its walk matrices) and the gather reach wins (grape_table_options
-    // may force any part).  Results do not depend on the choice; the number and
-    // spread of the reads do.
-    size_t free_b = 0, total_b = 0;
-    cudaMemGetInfo(&free_b, &total_b);
-    const double base_b = (double)(n + 1) * 8 + (double)n * sizeof(NodeRec);
-    const double cap = o.table_budget_bytes ? (double)o.table_budget_bytes : kReachBytes - base_b;
-    const double budget = std::min((double)free_b - 0.1 * (double)total_b, cap);
     struct Choice { uint32_t rec, gb, G, H; };
     Choice c{0, 0, 0, 0};
     auto size_of = [&](const Choice& k) {
@@ -402,72 +403,123 @@ grape_status build_tables(grape_graph* g, const grape_table_options& o)
     if (!found) {
         if (forced && any_allowed) {
             set_error("the requested table layout does not fit (%.3g bytes available)", budget);
-            return GRAPE_ENOMEM;
+            return -1;
         }
-        return GRAPE_OK;   // does not fit: v3 walker
+        return 0;
     }
     g->rec_bytes = c.rec;
     g->compact = weighted ? c.rec == 16 : c.rec == 8;
     g->guide_factor = c.G;
     g->guide_bytes = c.gb;
     g->hash_h = c.H;
-    const uint64_t rec_b = padded(m * c.rec), hash_b = padded(((m / c.H) + n + 1) * 32);
-    const uint64_t guide_b = weighted ? padded((uint64_t)c.G * m * c.gb) : 0;
-    const uint32_t G = c.G, gbytes = c.gb;
-    g->rec_alloc = rec_b;
-    g->guide_alloc = guide_b;
-    g->hash_alloc = hash_b;
-    if ((e = cudaMalloc(&g->rec, rec_b)) != cudaSuccess) return fail(e, "cudaMalloc arc records");
-    if (weighted && (e = cudaMalloc((void**)&g->guide, guide_b)) != cudaSuccess) return fail(e, "cudaMalloc guide");
-    if ((e = cudaMalloc((void**)&g->ehash, hash_b)) != cudaSuccess) return fail(e, "cudaMalloc edge hash");
-    if ((e = cudaMalloc((void**)&d_asym, 4)) != cudaSuccess) return fail(e, "cudaMalloc");
-    cudaMemset(d_asym, 0, 4);
-    cudaMemset(g->rec, 0, rec_b);
-    cudaMemset(g->ehash, 0xFF, hash_b);
-    if (weighted) cudaMemset(g->guide, 0, guide_b);
+    g->rec_alloc = padded(m * c.rec);
+    g->hash_alloc = padded(((m / c.H) + n + 1) * 32);
+    g->guide_alloc = weighted ? padded((uint64_t)c.G * m * c.gb) : 0;
+    return 1;
+}
+
+cudaError_t run_table_stage(const grape_graph* g, const TableJob& j, int stage, unsigned* asym)
+{
+    const bool weighted = g->cw_bytes != 0;
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
-    const int grid = build::item_grid(m, sms), ggrid = build::item_grid((uint64_t)G * m, sms);
-    if (m) build_ehash<<<grid, kThreads>>>(g->off, g->col, g->n, m, g->hash_h, g->ehash);
-    // no-common-neighbour flags (a temporary byte per arc); compact records need n < 2^30
+    const uint32_t* cw = (const uint32_t*)g->cw;
+    switch (stage) {
+    case 0:
+        if (j.h_hi > j.h_lo)
+            build_ehash<<<build::item_grid(j.h_hi - j.h_lo, sms), kThreads>>>(g->off, g->col, g->n, j.h_lo, j.h_hi,
+                                                                              g->hash_h, j.ehash);
+        break;
+    case 1:
+        if (j.notri.base[0] != nullptr && j.e_hi > j.e_lo)
+            build_notri<<<build::item_grid(j.e_hi - j.e_lo, sms), kThreads>>>(g->off, g->col, g->n, j.e_lo, j.e_hi,
+                                                                              g->hash_h, j.ehash, j.notri);
+        break;
+    case 2: {
+        if (j.e_hi <= j.e_lo) break;
+        const int grid = build::item_grid(j.e_hi - j.e_lo, sms);
+        if (weighted && g->compact)
+            build_records<true, true><<<grid, kThreads>>>(g->off, g->col, cw, g->n, j.e_lo, j.e_hi, j.rec, asym, j.notri);
+        else if (weighted)
+            build_records<true, false><<<grid, kThreads>>>(g->off, g->col, cw, g->n, j.e_lo, j.e_hi, j.rec, asym, j.notri);
+        else if (g->compact)
+            build_records<false, true><<<grid, kThreads>>>(g->off, g->col, nullptr, g->n, j.e_lo, j.e_hi, j.rec, asym,
+                                                           j.notri);
+        else
+            build_records<false, false><<<grid, kThreads>>>(g->off, g->col, nullptr, g->n, j.e_lo, j.e_hi, j.rec, asym,
+                                                            j.notri);
+        break;
+    }
+    case 3:
+        if (!weighted || j.b_hi <= j.b_lo) break;
+        if (g->guide_bytes == 32)
+            build_guide_fat<<<build::item_grid(j.b_hi - j.b_lo, sms), kThreads>>>(g->off, cw, g->n, j.b_lo, j.b_hi,
+                                                                                  g->guide_factor, j.rec, j.guide);
+        else
+            build_guide<<<build::item_grid(j.b_hi - j.b_lo, sms), kThreads>>>(g->off, g->col, cw, g->n, j.b_lo, j.b_hi,
+                                                                              g->guide_factor, j.guide);
+        break;
+    default: break;
+    }
+    return cudaGetLastError();
+}
+
+grape_status build_tables(grape_graph* g, const grape_table_options& o)
+{
+    const uint64_t m = g->m, n = g->n;
+    const bool weighted = g->cw_bytes != 0;
+    if (!tables_in_range(g)) return GRAPE_OK;
+    cudaError_t e = cudaSuccess;
+    unsigned* d_asym = nullptr;
     uint8_t* d_notri = nullptr;
+    auto fail = [&](cudaError_t err, const char* what) {
+        cudaFree(d_asym);
+        cudaFree(d_notri);
+        destroy_tables(g);
+        return cuda_fail(err, what);
+    };
+    // The layout must fit the device (leaving 10% free: the caller still needs its walk
+    // matrices) and the gather reach, or table_budget_bytes when given.
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const double base_b = (double)(n + 1) * 8 + (double)n * sizeof(NodeRec);
+    const double cap = o.table_budget_bytes ? (double)o.table_budget_bytes : kReachBytes - base_b;
+    const double budget = std::min((double)free_b - 0.1 * (double)total_b, cap);
+    const int ch = choose_layout(g, o, budget);
+    if (ch < 0) return GRAPE_ENOMEM;
+    if (ch == 0) return GRAPE_OK;   // does not fit: v3 walker
+    if ((e = cudaMalloc(&g->rec, g->rec_alloc)) != cudaSuccess) return fail(e, "cudaMalloc arc records");
+    if (weighted && (e = cudaMalloc((void**)&g->guide, g->guide_alloc)) != cudaSuccess)
+        return fail(e, "cudaMalloc guide");
+    if ((e = cudaMalloc((void**)&g->ehash, g->hash_alloc)) != cudaSuccess) return fail(e, "cudaMalloc edge hash");
+    if ((e = cudaMalloc((void**)&d_asym, 4)) != cudaSuccess) return fail(e, "cudaMalloc");
+    cudaMemset(d_asym, 0, 4);
+    cudaMemset(g->rec, 0, g->rec_alloc);
+    cudaMemset(g->ehash, 0xFF, g->hash_alloc);
+    if (weighted) cudaMemset(g->guide, 0, g->guide_alloc);
+    // no-common-neighbour flags (a temporary byte per arc); compact records need n < 2^30
     const bool flags_ok = !(g->compact && n >= (1u << 30));
-    if (flags_ok && cudaMalloc((void**)&d_notri, m ? m : 1) == cudaSuccess) {
-        if (m) build_notri<<<grid, kThreads>>>(g->off, g->col, g->n, m, g->hash_h, g->ehash, d_notri);
-    } else {
+    if (flags_ok && cudaMalloc((void**)&d_notri, m ? m : 1) != cudaSuccess) {
         cudaGetLastError();
         d_notri = nullptr;
     }
-    if (m == 0) {
-    } else if (weighted) {
-        if (g->compact)
-            build_records<true, true><<<grid, kThreads>>>(g->off, g->col, (const uint32_t*)g->cw, g->n, m, g->rec,
-                                                          d_asym, d_notri);
-        else
-            build_records<true, false><<<grid, kThreads>>>(g->off, g->col, (const uint32_t*)g->cw, g->n, m, g->rec,
-                                                           d_asym, d_notri);
-        if (gbytes == 32)
-            build_guide_fat<<<ggrid, kThreads>>>(g->off, (const uint32_t*)g->cw, g->n, m, G, (const uint4*)g->rec,
-                                                 (uint4*)g->guide);
-        else
-            build_guide<<<ggrid, kThreads>>>(g->off, g->col, (const uint32_t*)g->cw, g->n, m, G, (uint2*)g->guide);
-    } else {
-        if (g->compact)
-            build_records<false, true><<<grid, kThreads>>>(g->off, g->col, nullptr, g->n, m, g->rec, d_asym, d_notri);
-        else
-            build_records<false, false><<<grid, kThreads>>>(g->off, g->col, nullptr, g->n, m, g->rec, d_asym, d_notri);
-    }
+    TableJob j{};
+    j.e_lo = j.h_lo = j.b_lo = 0;
+    j.e_hi = j.h_hi = m;
+    j.b_hi = weighted ? (uint64_t)g->guide_factor * m : 0;
+    j.rec = flat(g->rec);
+    j.guide = flat(g->guide);
+    j.ehash = flat(g->ehash);
+    j.notri = flat(d_notri);
+    for (int stage = 0; stage < 4 && e == cudaSuccess; ++stage) e = run_table_stage(g, j, stage, d_asym);
+    if (e != cudaSuccess) return fail(e, "table kernels");
     g->notri = d_notri != nullptr;
-    if (d_notri) {
-        cudaDeviceSynchronize();
-        cudaFree(d_notri);
-    }
-    if ((e = cudaGetLastError()) != cudaSuccess) return fail(e, "table kernels");
     unsigned asym = 0;
     if ((e = cudaMemcpy(&asym, d_asym, 4, cudaMemcpyDeviceToHost)) != cudaSuccess) return fail(e, "table build");
     cudaFree(d_asym);
+    cudaFree(d_notri);
     g->wsym = !weighted || asym == 0;
-    g->table_bytes = rec_b + guide_b + hash_b;
+    g->table_bytes = g->rec_alloc + g->guide_alloc + g->hash_alloc;
     g->tables = true;
     return GRAPE_OK;
 }

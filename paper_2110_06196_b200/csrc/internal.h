@@ -21,11 +21,63 @@ struct alignas(16) NodeRec {
     uint32_t w32;
 };
 
-// §8(f) f4 layout (partition.cu): table T (0 records, 1 guide, 2 node records,
-// 3 edge hash) in parts of 2^shift[T] bytes, part j at base[T][j]
+// §8(f) f4 layout (partition.cu, dist.cu): table T (0 records, 1 guide, 2 node
+// records, 3 edge hash) in chunks of 2^shift[T] bytes, chunk c at base[T][c].  A
+// table has at most kChunks chunks; owner j of `parts` holds the contiguous chunk
+// range [floor(C j / parts), floor(C (j+1) / parts)) of its C chunks (one
+// allocation per owner), so owners differ by at most one chunk.
+constexpr int kChunks = 64;
 struct PartMap {
-    const char* base[4][8];
+    const char* base[4][kChunks];
     uint32_t shift[4];
+};
+inline uint32_t chunk_shift(uint64_t bytes)   // >= 2 MB chunks (a multiple of every entry size)
+{
+    uint32_t k = 21;
+    while ((1ull << k) * kChunks < bytes) ++k;
+    return k;
+}
+inline uint64_t chunk_count(uint64_t bytes, uint32_t k) { return (bytes + (1ull << k) - 1) >> k; }
+// owner j's byte range [*lo, *hi) of a table of `bytes` bytes in chunks of 2^k
+inline void owner_range(uint64_t bytes, uint32_t k, uint32_t j, uint32_t parts, uint64_t* lo, uint64_t* hi)
+{
+    const uint64_t C = chunk_count(bytes, k);
+    const uint64_t a = (C * j / parts) << k, b = (C * (j + 1) / parts) << k;
+    *lo = a < bytes ? a : bytes;
+    *hi = b < bytes ? b : bytes;
+}
+
+// Chunk c of a table at owner_base[owner(c)] + (c's offset within that owner's range)
+inline void map_chunks(char* const* owner_base, uint64_t bytes, uint32_t k, uint32_t parts, char** out)
+{
+    const uint64_t C = chunk_count(bytes, k);
+    for (uint32_t j = 0; j < parts; ++j) {
+        uint64_t lo, hi;
+        owner_range(bytes, k, j, parts, &lo, &hi);
+        for (uint64_t c = lo >> k; (c << k) < hi; ++c) out[c] = owner_base[j] + ((c << k) - lo);
+    }
+    for (uint64_t c = C; c < (uint64_t)kChunks; ++c) out[c] = C ? out[0] : nullptr;   // never addressed
+}
+
+// A table as the build kernels address it: contiguous (shift = 63: everything at
+// base[0]) or in parts of 2^shift bytes, part j at base[j] (local, on a peer GPU,
+// or opened from another process by CUDA IPC; graph_tables.cu, dist.cu).
+struct TabRef {
+    char* base[kChunks];
+    uint32_t shift;
+    __host__ __device__ char* at(uint64_t byte) const
+    {
+        return base[byte >> shift] + (byte & ((1ull << shift) - 1));
+    }
+};
+
+// The share of the table build one builder runs (the whole graph, or one rank's
+// parts in a distributed build, dist.cu): arc records and no-common-neighbour
+// flags of arcs [e_lo, e_hi), edge-hash sets of the rows whose arcs are
+// [h_lo, h_hi) (row-aligned), guide buckets [b_lo, b_hi).
+struct TableJob {
+    uint64_t e_lo, e_hi, h_lo, h_hi, b_lo, b_hi;
+    TabRef rec, guide, ehash, notri;   // notri.base[0] == nullptr: no flags
 };
 }  // namespace grape
 
@@ -57,12 +109,21 @@ struct grape_graph {
     uint64_t table_bytes;
     uint64_t rec_alloc = 0, guide_alloc = 0, hash_alloc = 0;   // table allocation bytes
     // §8(f) f4 layout (partition.cu, grape_graph_partition): every table split into
-    // power-of-two parts, part j of table T at part_mem[T][j] (possibly on a peer GPU);
+    // chunks of 2^part_shift[T] bytes, owner j's contiguous range of table T at
+    // part_mem[T][j] (possibly on a peer GPU, or opened from another process);
     // T = 0 arc records, 1 guide, 2 node records, 3 edge hash
     uint32_t parts = 1;
     void* part_mem[4][8] = {};
     uint32_t part_shift[4] = {63, 63, 63, 63};
     grape::PartMap* part_map = nullptr;   // device copy of {part_mem, part_shift} for the walker
+    // distributed build (dist.cu): this process owns part dist_part of every table; the
+    // others were opened by CUDA IPC (closed, not freed, by destroy_graph); the
+    // no-common-neighbour flags live in parts of 2^notri_shift bytes while building
+    bool dist = false;
+    uint32_t dist_part = 0;
+    bool part_ipc[5][8] = {};
+    void* notri_mem[8] = {};
+    uint64_t part_len[5] = {};            // bytes of this process's part of table T (T = 4: flags)
     // host-buffer staging (capi.cu walks_host): device buffers kept between calls;
     // a call that finds the mutex taken (a concurrent host-buffer call) allocates its own
     std::mutex stage_mu;
@@ -79,6 +140,10 @@ struct grape_graph {
 };
 
 namespace grape {
+
+// build_graph flag (internal, above the ABI's flags): stop after the CSR, its prefix
+// sums and the node records (no tables, no fence levels) — dist.cu builds the tables.
+constexpr uint32_t kCsrOnly = 1u << 30;
 
 // Makes `dev` current for a scope (restores the caller's device on exit).
 struct DeviceGuard {
@@ -137,6 +202,10 @@ cudaError_t launch_walks_tab(const grape_graph* g, const WalkArgs& a, bool node2
 cudaError_t launch_walks_sm(const grape_graph* g, const WalkArgs& a, bool node2vec,
                             const Thresholds& T, cudaStream_t stream);
 
+// capi.cu: the argument checks of grape_graph_from_csr_opts (pointers, n, flags,
+// device, table option values)
+grape_status check_build_args(uint32_t n, uint64_t m, const uint64_t* off, const uint32_t* col, const uint32_t* w,
+                              int device, uint32_t flags, const grape_table_options* opts);
 // graph.cu
 grape_status build_graph(uint32_t n, uint64_t m, const uint64_t* off, const uint32_t* col,
                          const uint32_t* w, int device, uint32_t flags, const grape_table_options& opts,
@@ -147,5 +216,16 @@ void destroy_graph(grape_graph* g);
 // returns GRAPE_OK) when the graph is outside the tables' index ranges.
 grape_status build_tables(grape_graph* g, const grape_table_options& opts);
 void destroy_tables(grape_graph* g);
+// graph_tables.cu: the layout (record / guide / hash sizes) whose tables fit `budget`
+// bytes; sets g->rec_bytes, compact, guide_factor, guide_bytes, hash_h and the
+// table sizes g->rec_alloc, guide_alloc, hash_alloc.  1: chosen, 0: none fits
+// (automatic layout: the caller keeps the v3 walker), -1: a forced layout does not
+// fit (error message set).  in_range: the graph is inside the tables' index ranges.
+bool tables_in_range(const grape_graph* g);
+int choose_layout(grape_graph* g, const grape_table_options& o, double budget);
+// graph_tables.cu: one stage of the table build over a job's share (0 edge hash,
+// 1 no-common-neighbour flags, 2 arc records, 3 guide); asynchronous on the
+// default stream; *asym (device) gets bit 0 when a reverse arc's weight differs.
+cudaError_t run_table_stage(const grape_graph* g, const TableJob& j, int stage, unsigned* asym);
 
 }  // namespace grape

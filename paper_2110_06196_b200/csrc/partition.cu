@@ -1,8 +1,9 @@
 // partition.cu — the §8(f) f4 table layout: the sampling tables of
-// a built graph split into power-of-two byte ranges ("parts"), part j resident on
-// device devices[j] and read by the walker over NVLink peer access.  The walker's
-// single address computation resolves base[T][offset >> k] + (offset & (2^k - 1))
-// (walk_tab.cu, MODE 3), so every walk is the one the contiguous tables give.
+// a built graph split into chunks of 2^k bytes (at most kChunks per table), owner j
+// of `parts` holding a contiguous range of chunks on device devices[j], read by
+// the walker over NVLink peer access.  The walker's single address computation
+// resolves base[T][offset >> k] + (offset & (2^k - 1)) (walk_tab.cu, MODE 3), so
+// every walk is the one the contiguous tables give.
 //
 // This first form partitions a graph that was built on one GPU (the build itself is
 // not distributed): it places the tables of a graph over several GPUs' memory and
@@ -14,32 +15,26 @@ namespace grape {
 namespace {
 
 struct Split {
-    void* mem[8] = {};
-    uint32_t shift = 63;
+    void* mem[8] = {};    // owner j's contiguous range (chunks [C j / parts, C (j+1) / parts))
+    uint32_t shift = 63;  // chunk size 2^shift
 };
 
-// copy table bytes at src (on the graph's device) into parts of 2^k bytes
+// copy table bytes at src (on the graph's device) into owner ranges of 2^k-byte chunks
 cudaError_t split(const grape_graph* g, const void* src, uint64_t bytes, uint32_t parts, const int* devices,
                   Split& out)
 {
-    uint32_t k = 21;   // >= 2 MB parts
-    while ((1ull << k) * parts < bytes) ++k;
-    const uint64_t psz = 1ull << k;
+    const uint32_t k = chunk_shift(bytes);
     out.shift = k;
     cudaError_t e = cudaSuccess;
     for (uint32_t j = 0; j < parts && e == cudaSuccess; ++j) {
-        const uint64_t lo = (uint64_t)j * psz;
-        const uint64_t len = lo >= bytes ? 0 : (bytes - lo < psz ? bytes - lo : psz);
-        if (len == 0) {   // past the end: never addressed; alias part 0
-            out.mem[j] = out.mem[0];
-            continue;
+        uint64_t lo, hi;
+        owner_range(bytes, k, j, parts, &lo, &hi);
+        if (hi == lo) continue;   // (fewer chunks than owners) never addressed
+        {
+            DeviceGuard on(devices[j]);
+            e = cudaMalloc(&out.mem[j], hi - lo);
         }
-        int prev = 0;
-        cudaGetDevice(&prev);
-        e = cudaSetDevice(devices[j]);
-        if (e == cudaSuccess) e = cudaMalloc(&out.mem[j], len);
-        cudaSetDevice(prev);
-        if (e == cudaSuccess) e = cudaMemcpyPeer(out.mem[j], devices[j], (const char*)src + lo, g->device, len);
+        if (e == cudaSuccess) e = cudaMemcpyPeer(out.mem[j], devices[j], (const char*)src + lo, g->device, hi - lo);
     }
     return e;
 }
@@ -47,9 +42,7 @@ cudaError_t split(const grape_graph* g, const void* src, uint64_t bytes, uint32_
 void release(Split& s, uint32_t parts)
 {
     for (uint32_t j = 0; j < parts; ++j) {
-        bool dup = false;
-        for (uint32_t q = 0; q < j; ++q) dup |= s.mem[q] == s.mem[j];
-        if (!dup && s.mem[j]) cudaFree(s.mem[j]);
+        if (s.mem[j]) cudaFree(s.mem[j]);
         s.mem[j] = nullptr;
     }
 }
@@ -107,7 +100,7 @@ extern "C" grape_status grape_graph_partition(grape_graph* g, uint32_t parts, co
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     PartMap pm{};
     for (int t = 0; t < 4; ++t) {
-        for (uint32_t j = 0; j < 8; ++j) pm.base[t][j] = (const char*)sp[t].mem[j < parts ? j : 0];
+        map_chunks((char* const*)sp[t].mem, bytes[t], sp[t].shift, parts, (char**)pm.base[t]);
         pm.shift[t] = sp[t].shift;
     }
     PartMap* dmap = nullptr;

@@ -1,0 +1,120 @@
+"""§8(f) f4, distributed: sampling tables larger than one process's budget, built
+by two processes (one part each) and walked over both parts.
+
+Both ranks run on cuda:0 with the gloo backend (CUDA IPC works between processes
+on one device; the build stages and walks never wait on each other inside a
+kernel — the ranks meet only at host barriers).  Checks: with a per-rank table
+budget below the layout's total, the single-process build refuses the layout
+(ENOMEM) while the two-rank build succeeds; every walk each rank computes over the
+distributed tables equals the oracle's and the contiguous single-GPU tables'
+(bit for bit, default and first-order rules, strong-scaling slices)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+CASES = [  # (graph, layout forced, walk mode, p, q, L)
+    ("cfg2/4", {"record_bytes": 32, "guide_bytes": 32, "guide_factor": 4}, "node2vec", 0.5, 2.0, 40),
+    ("cfg2/4", {"record_bytes": 16, "guide_bytes": 8, "guide_factor": 1, "hash_h": 6}, "node2vec", 2.0, 0.5, 40),
+    ("cfg5/8", {"record_bytes": 32, "guide_bytes": 8, "guide_factor": 2}, "node2vec", 0.25, 4.0, 30),
+    ("cfg3/8", {"record_bytes": 16}, "node2vec", 1.0, 0.25, 30),
+    ("cfg3/8", {"record_bytes": 8, "hash_h": 6}, "first_order", 1.0, 1.0, 30),
+    ("tiny", {}, "node2vec", 0.5, 2.0, 20),
+]
+
+
+def _graph(name):
+    from graphgen import config_graph, tiny_graph
+    if name == "tiny":
+        return tiny_graph(77, 50, 0.1, weighted=True)
+    k, sd = name[3], name.split("/")[1]
+    return config_graph(int(k), scale_down={"4": 4, "8": 8}[sd] if sd in ("4", "8") else 0)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, case, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        import paper_2110_06196_b200 as grape
+        from graphgen import starts_per_node
+        name, layout, mode, p, qq, L = case
+        g = _graph(name)
+        ref = grape.graph_from_csr(g.off, g.col, g.w, device=0, symmetric=g.symmetric, layout=layout)
+        total = ref.info["table_bytes"]
+        budget = int(total * 0.6)   # one rank cannot hold the tables; two can
+        refused = None
+        try:
+            grape.graph_from_csr(g.off, g.col, g.w, device=0, symmetric=g.symmetric,
+                                 layout=dict(layout, table_budget_bytes=budget)).free()
+            refused = False
+        except grape.GrapeError as ex:
+            refused = ex.status == grape.GRAPE_ENOMEM
+        dg = grape.graph_from_csr_dist(g.off, g.col, g.w, device=0, symmetric=g.symmetric, layout=layout,
+                                       table_budget_bytes=budget)
+        info = dg.info
+        W = g.n
+        lo, hi = W * rank // world, W * (rank + 1) // world
+        st = starts_per_node(g.n, 1)[lo:hi].cuda()
+        steps = torch.zeros(1, dtype=torch.int64, device="cuda")
+        if mode == "node2vec":
+            mine = grape.walks_node2vec(dg, st, L, p, qq, seed=42, walk_id_base=lo, steps=steps)
+            exp = grape.walks_node2vec(ref, st, L, p, qq, seed=42, walk_id_base=lo)
+        else:
+            mine = grape.walks_first_order(dg, st, L, seed=42, walk_id_base=lo, steps=steps)
+            exp = grape.walks_first_order(ref, st, L, seed=42, walk_id_base=lo)
+        torch.cuda.synchronize()
+        same = bool(torch.equal(mine, exp))
+        rows = mine.cpu().numpy().view(np.uint32)
+        # a sample against the oracle
+        from oracle.oracle import Oracle
+        o = Oracle(*g.numpy())
+        rng = np.random.default_rng(rank)
+        bad = []
+        for i in np.unique(np.concatenate([rng.integers(0, hi - lo, 64), [0, hi - lo - 1]])):
+            e, _ = o.walks(np.array([lo + i], dtype=np.uint32), L, mode=mode, p=p, q=qq, seed=42, base=int(lo + i))
+            if not np.array_equal(rows[i], e[0]):
+                bad.append(int(lo + i))
+        q.put((rank, refused, same, bad, info["parts"], info["table_bytes"], total, budget, int(steps.item())))
+        dg.free()
+        ref.free()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case", CASES, ids=[f"{c[0]}-{'-'.join(f'{k}{v}' for k, v in c[1].items()) or 'auto'}-{c[2]}"
+                                           for c in CASES])
+def test_two_process_distributed_tables(case):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, case, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = sorted([q.get(timeout=600) for _ in range(2)])
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    for rank, refused, same, bad, parts, part_bytes, total, budget, steps in res:
+        assert parts == 2
+        assert same, f"rank {rank}: walks over the distributed tables differ from the contiguous tables"
+        assert not bad, f"rank {rank}: walks differ from the oracle at wids {bad[:5]}"
+        assert part_bytes <= budget or case[0] == "tiny"
+        if case[0] != "tiny":
+            assert refused, "the single-process build should not fit the per-rank budget"
+            assert part_bytes < total

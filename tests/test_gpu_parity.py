@@ -243,7 +243,8 @@ def test_full_size_config_sampled(grape, k, mode):
     deg = (g.off[1:] - g.off[:-1])
     hubs = torch.topk(deg, 100).indices.cpu().numpy()
     sink_all = torch.nonzero(deg == 0).flatten()
-    pick = torch.randperm(sink_all.numel(), generator=torch.Generator().manual_seed(k))[:100]
+    n_sinks = sink_all.numel()
+    pick = torch.randperm(n_sinks, generator=torch.Generator().manual_seed(k))[:100]
     sinks = sink_all[pick.to(sink_all.device)].cpu().numpy()
     del sink_all
     del deg
@@ -287,7 +288,7 @@ def test_full_size_config_sampled(grape, k, mode):
         assert np.array_equal(host_out[r], exp[0]), int(i)
     # the GPU rows of walks from sinks (directed configs): [start, PAD, ...]
     if len(sinks):
-        assert len(sinks) == 100   # cfg3: isolated nodes; cfg5: the 5% sinks
+        assert len(sinks) == min(100, n_sinks)   # cfg3: isolated nodes; cfg4: a few; cfg5: the 5% sinks
         at = {int(i): r for r, i in enumerate(sample)}
         for it in range(wk["walks_per_node"]):
             for s_ in sinks:
