@@ -309,8 +309,15 @@ def run_ours(args):
     # C-ABI call, timed on its own (outside the timed walk region, reported)
     torch.cuda.synchronize(dev)
     t_b = time.perf_counter()
-    dg = grape.graph_from_csr(g.off, g.col, g.w, device=local, symmetric=g.symmetric, tables=not args.no_tables,
-                              layout=_parse_layout(args.layout))
+    if args.dist_tables:   # §8(f) f4: part r of the tables on rank r, built by all ranks together
+        if world < 2:
+            raise SystemExit("--dist-tables needs N > 1 ranks (torchrun)")
+        dg = grape.graph_from_csr_dist(g.off, g.col, g.w, device=local, symmetric=g.symmetric,
+                                       layout=_parse_layout(args.layout),
+                                       table_budget_bytes=int(args.table_budget * 1e9) if args.table_budget else None)
+    else:
+        dg = grape.graph_from_csr(g.off, g.col, g.w, device=local, symmetric=g.symmetric, tables=not args.no_tables,
+                                  layout=_parse_layout(args.layout))
     torch.cuda.synchronize(dev)
     build_ms = 1e3 * (time.perf_counter() - t_b)
     g = g.to("cpu")            # the library holds its own copy; free the device CSR for the walk matrix
@@ -546,6 +553,8 @@ def run_ours(args):
             metric = metric[:-1] + ", outlier-folded rejection)"
         if args.parts > 1:
             metric = metric[:-1] + f", tables in {args.parts} parts)"
+        if args.dist_tables:
+            metric = metric[:-1] + f", tables distributed over {world} GPUs)"
         cfg = _workload_desc(k, g, wk, W, flush)
         cfg.update({"walks_total": W_total if args.scaling == "strong" else W * world,
                     "sharding": ("strong: rank r walks wids [floor(r W/N), floor((r+1) W/N)) of the config's "
@@ -554,6 +563,9 @@ def run_ours(args):
                                  "weak: every rank walks W wids on its own block [r W, (r+1) W)")})
         if args.scale_down:
             cfg["scale_down"] = args.scale_down
+        if args.dist_tables:
+            cfg["tables"] = (f"distributed: rank r owns part r of the sampling tables ({world} parts, CUDA IPC), "
+                             f"every rank walks over all parts")
         line = {"metric": metric, "value": value, "unit": "steps/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
                 "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "u32/u64 integer",
@@ -723,6 +735,11 @@ def main():
                     help="CUDA device of every rank (default LOCAL_RANK); tests pin two ranks to cuda:0")
     ap.add_argument("--dist-backend", default=None, choices=["nccl", "gloo"],
                     help="process-group backend for N > 1 (default nccl on GPUs)")
+    ap.add_argument("--dist-tables", action="store_true",
+                    help="N > 1: build the sampling tables distributed over the ranks (grape_graph_dist_*, "
+                         "§8(f) f4), one part per rank; walks read every part")
+    ap.add_argument("--table-budget", type=float, default=0.0,
+                    help="--dist-tables: table GB per rank (default: the smallest free memory over the ranks)")
     ap.add_argument("--dump-walks", default=None, metavar="PREFIX",
                     help="save each rank's walk matrix to PREFIX.rank<r>.npy (parity tests)")
     args = ap.parse_args()

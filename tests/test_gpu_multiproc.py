@@ -42,12 +42,18 @@ def _bench(nproc, extra, port, tmp, tag):
 
 
 @pytest.mark.parametrize("cfg,extra", [(1, []), (2, ["--scale-down", "5", "--no-e2e"]),
-                                       (5, ["--scale-down", "8", "--no-e2e"])],
-                         ids=["cfg1", "cfg2-scaled", "cfg5-scaled"])
+                                       (5, ["--scale-down", "8", "--no-e2e"]),
+                                       (2, ["--scale-down", "4", "--no-e2e", "--dist-tables", "--table-budget", "0.3"])],
+                         ids=["cfg1", "cfg2-scaled", "cfg5-scaled", "cfg2-scaled-dist-tables"])
 def test_two_ranks_strong_scaling_equals_one_rank(tmp_path, cfg, extra):
+    """(last case: the tables built distributed over the two ranks, 0.3 GB each, bench
+    --dist-tables; the N = 1 reference run builds them on one GPU)"""
     extra = ["--config", str(cfg)] + extra
-    one, p1 = _bench(1, extra, 0, str(tmp_path), "n1")
-    two, p2 = _bench(2, extra, 29600 + cfg, str(tmp_path), "n2")
+    one_extra = [a for a in extra if a not in ("--dist-tables", "--table-budget", "0.3")]
+    one, p1 = _bench(1, one_extra, 0, str(tmp_path), "n1")
+    two, p2 = _bench(2, extra, 29600 + cfg + 10 * len(extra), str(tmp_path), "n2")
+    if "--dist-tables" in extra:
+        assert "distributed" in two["config"]["tables"] and "distributed over 2 GPUs" in two["metric"]
     assert one["scaling"] == two["scaling"] == "strong"
     assert one["n_gpus"] == 1 and two["n_gpus"] == 2
     W = one["config"]["walks_total"]
