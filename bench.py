@@ -633,11 +633,17 @@ def run_skipgram(args):
     def pairs():
         grape.skipgram_pairs(dg, walks, win, K, seed=wk["seed"] + 1, walk_id_base=base, out=outs)
 
+    def fused(c):   # grape_walks_skipgram: walks streamed into the pair kernel (no walk matrix)
+        grape.walks_skipgram(dg, starts, L, win, K, node2vec=node2vec, p=wk["p"], q=wk["q"], seed=wk["seed"],
+                             pair_seed=wk["seed"] + 1, walk_id_base=base, out=outs, steps=c)
+
     for _ in range(args.warmup):
         walk(None)
         pairs()
+        fused(None)
     torch.cuda.synchronize(dev)
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    fctr = torch.zeros(1, dtype=torch.int64, device=dev)
     if world > 1:
         dist.barrier()
     with ClockSampler(local) as clk:
@@ -648,11 +654,14 @@ def run_skipgram(args):
             e[1].record()
             pairs()
             e[2].record()
+            fused(fctr)
+            e[3].record()
         torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     t_walk = sum(e[0].elapsed_time(e[1]) for e in evs) / 1e3
     t_pair = sum(e[1].elapsed_time(e[2]) for e in evs) / 1e3
+    t_fused = sum(e[2].elapsed_time(e[3]) for e in evs) / 1e3
     valid = int((outs[0] != -1).sum().item())
     steps = float(ctr.item())
     tot = _allreduce(t_walk + t_pair, dist.ReduceOp.MAX, world)
@@ -684,6 +693,13 @@ def run_skipgram(args):
                 "config": dict(_workload_desc(k, g, wk, B), batch_walks=B, window=win, negatives=K),
                 "gpu_launches": 2 * args.steps,
                 "walk_steps_per_s_with_pairs": steps / (t_walk + t_pair),
+                "streamed": {"path": "grape_walks_skipgram (walk rows streamed chunk by chunk through an "
+                                     "L2-resident buffer into the pair kernel; no walk matrix)",
+                             "ms": 1e3 * t_fused / args.steps,
+                             "training_pairs_per_s": valid * args.steps / t_fused,
+                             "vs_two_calls": (t_walk + t_pair) / t_fused,
+                             "walk_matrix_bytes_not_materialised": B * L * 4,
+                             "steps_equal": float(fctr.item()) == steps},
                 "walk_steps_per_s_alone": steps / t_walk,
                 "pair_kernel": {"ms": 1e3 * t_pair / args.steps, "slots": S, "valid_pairs": valid,
                                 "negatives_per_s": valid * K * args.steps / t_pair},

@@ -372,6 +372,31 @@ grape_status grape_skipgram_pairs(const grape_graph* g, const uint32_t* walks, u
                                   uint32_t* negatives, cudaStream_t stream);
 
 /*
+ * grape_walks_skipgram — walks streamed straight into the SkipGram consumer
+ * (DESIGN.md §7e): exactly grape_walks_first_order /
+ * grape_walks_node2vec (walk_seed) followed by grape_skipgram_pairs (pair_seed) on
+ * the same walk ids, bit for bit, without materialising the walk matrix: walks are
+ * generated chunk_walks rows at a time (0 = automatic, 24 MB of rows) into an
+ * internal device buffer held in L2 (persisting access-policy window, best
+ * effort), and the pair kernel consumes each chunk while the walker fills the
+ * next (two internal streams).  The walks exist to feed this; the paper
+ * generates them lazily for the same reason ("static generation ... tens of
+ * terabytes").
+ *   starts        device u32[num_walks]; walk ids walk_id_base + i
+ *   node2vec      0: first order (p, q ignored), else node2vec(p, q)
+ *   centers, contexts, negatives, window, num_negatives: as grape_skipgram_pairs
+ *   steps_out     device u64 or NULL: realised transitions are added to it
+ * Asynchronous on `stream` (the internal streams are ordered after the work already
+ * on it, and `stream` is ordered after them).  Device buffers only (EINVAL
+ * otherwise); the other errors as grape_walks_node2vec and grape_skipgram_pairs.
+ */
+grape_status grape_walks_skipgram(const grape_graph* g, const uint32_t* starts, uint64_t num_walks,
+                                  uint64_t walk_id_base, uint32_t walk_length, int node2vec, double p, double q,
+                                  uint64_t walk_seed, uint32_t window, uint32_t num_negatives, uint64_t pair_seed,
+                                  uint32_t* centers, uint32_t* contexts, uint32_t* negatives, uint64_t* steps_out,
+                                  uint64_t chunk_walks, cudaStream_t stream);
+
+/*
  * grape_walks_stats — diagnostics: run the same walks as grape_walks_first_order
  * (node2vec = 0) or grape_walks_node2vec (node2vec = 1) with event counters
  * compiled into the kernel, and return the counts.  `out` receives exactly the

@@ -348,6 +348,42 @@ def skipgram_pairs(g: Graph, walks, window: int, num_negatives: int, *, seed: in
     return c, x, ng
 
 
+def walks_skipgram(g: Graph, starts, L: int, window: int, num_negatives: int, *, node2vec: bool = True,
+                   p: float = 1.0, q: float = 1.0, seed: int = 42, pair_seed: int = 43, walk_id_base: int = 0,
+                   out=None, steps=None, chunk_walks: int = 0, stream=None):
+    """grape_walks_skipgram: the walks of walks_node2vec / walks_first_order streamed into
+    skipgram_pairs without materialising the walk matrix (bit-identical to the two calls).
+    starts: CUDA int32 [W].  Returns (centers int32[S], contexts int32[S], negatives
+    int32[S, K]), S = W*L*2*window."""
+    st = _as_tensor(starts, torch.int32)
+    if not st.is_cuda or st.device.index != g.device:
+        raise ValueError(f"starts must be a CUDA tensor on cuda:{g.device}")
+    W = st.numel()
+    S = W * L * 2 * window
+    with torch.cuda.device(g.device):
+        if out is None:
+            out = (torch.empty(S, dtype=torch.int32, device=st.device),
+                   torch.empty(S, dtype=torch.int32, device=st.device),
+                   torch.empty((S, num_negatives), dtype=torch.int32, device=st.device))
+        else:
+            if len(out) != 3:
+                raise ValueError("out must be (centers, contexts, negatives)")
+            _check_out(out[0], (S,), str(g.device), "centers")
+            _check_out(out[1], (S,), str(g.device), "contexts")
+            _check_out(out[2], (S, num_negatives), str(g.device), "negatives")
+        if steps is not None:
+            _check_steps(steps, True, g.device)
+        c, x, ng = out
+        sh = _stream_handle(stream, g.device, (st, c, x, ng))
+        rc = _lib.grape_walks_skipgram(g.handle, st.data_ptr(), W, walk_id_base, L, int(node2vec), float(p),
+                                       float(q), seed, window, num_negatives, pair_seed, c.data_ptr(), x.data_ptr(),
+                                       ng.data_ptr() if num_negatives else None,
+                                       None if steps is None else steps.data_ptr(), int(chunk_walks),
+                                       ctypes.c_void_p(sh))
+    _capi.check(_lib, rc, "grape_walks_skipgram")
+    return c, x, ng
+
+
 def walks_approx(g: Graph, starts, L: int, degree_threshold: int, *, node2vec: bool = True, p: float = 1.0,
                  q: float = 1.0, seed: int = 42, walk_id_base: int = 0, out=None, steps=None,
                  stream=None) -> torch.Tensor:

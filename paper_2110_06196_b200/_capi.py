@@ -22,7 +22,7 @@ GRAPE_PAD = 0xFFFFFFFF
 EXPORTS = (
     "grape_graph_from_csr", "grape_graph_from_csr_opts", "grape_graph_free", "grape_graph_get_info",
     "grape_walks_first_order", "grape_walks_node2vec", "grape_walks_approx", "grape_walks_node2vec_cdf", "grape_walks_node2vec_folded",
-    "grape_skipgram_pairs", "grape_graph_partition",
+    "grape_skipgram_pairs", "grape_walks_skipgram", "grape_graph_partition",
     "grape_graph_dist_create", "grape_graph_dist_export", "grape_graph_dist_import", "grape_graph_dist_build",
     "grape_graph_dist_finish",
     "grape_walks_stats",
@@ -123,6 +123,9 @@ def load(path: str | None = None) -> ctypes.CDLL:
     lib.grape_walks_node2vec_folded.restype = i32
     lib.grape_skipgram_pairs.argtypes = [vp, vp, u64, u64, u32, u32, u32, u64, vp, vp, vp, vp]
     lib.grape_skipgram_pairs.restype = i32
+    lib.grape_walks_skipgram.argtypes = [vp, vp, u64, u64, u32, i32, dbl, dbl, u64, u32, u32, u64, vp, vp, vp, vp,
+                                         u64, vp]
+    lib.grape_walks_skipgram.restype = i32
     lib.grape_graph_partition.argtypes = [vp, u32, vp]
     lib.grape_graph_partition.restype = i32
     lib.grape_graph_dist_create.argtypes = [u32, u64, vp, vp, vp, i32, u32, ctypes.POINTER(TableOptions), u32, u32,

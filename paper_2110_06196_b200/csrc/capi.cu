@@ -512,6 +512,71 @@ grape_status grape_skipgram_pairs(const grape_graph* g, const uint32_t* walks, u
     return GRAPE_OK;
 }
 
+grape_status grape_walks_skipgram(const grape_graph* g, const uint32_t* starts, uint64_t num_walks,
+                                  uint64_t walk_id_base, uint32_t walk_length, int node2vec, double p, double q,
+                                  uint64_t walk_seed, uint32_t window, uint32_t num_negatives, uint64_t pair_seed,
+                                  uint32_t* centers, uint32_t* contexts, uint32_t* negatives, uint64_t* steps_out,
+                                  uint64_t chunk_walks, cudaStream_t stream)
+{
+    g_err[0] = 0;
+    if (g == nullptr || (num_walks > 0 && (starts == nullptr || centers == nullptr || contexts == nullptr ||
+                                           (num_negatives > 0 && negatives == nullptr)))) {
+        set_error("graph, starts, centers, contexts (and negatives when num_negatives > 0) must be non-NULL");
+        return GRAPE_EINVAL;
+    }
+    if (walk_length == 0 || window == 0 || window > 1024 || num_negatives > 1024) {
+        set_error("need walk_length >= 1, 1 <= window <= 1024, num_negatives <= 1024");
+        return GRAPE_EINVAL;
+    }
+    const uint64_t slots_per_walk = (uint64_t)walk_length * 2 * window;
+    if (slots_per_walk * (num_negatives > 0 ? num_negatives : 1) >= (1ull << 32)) {
+        set_error("walk_length * 2 * window * num_negatives must be < 2^32 (one row's output words)");
+        return GRAPE_EINVAL;
+    }
+    const uint64_t max_wid = (~0ull) / slots_per_walk;
+    if (num_walks > (~0ull) / slots_per_walk / 4 / (num_negatives + 1) || num_walks > max_wid ||
+        walk_id_base > max_wid - num_walks) {
+        set_error("the slot count (num_walks * walk_length * 2 * window * (1 + num_negatives)) overflows");
+        return GRAPE_EINVAL;
+    }
+    Thresholds T{1ull << 32, 1ull << 32, 1ull << 32};
+    if (node2vec && !node2vec_thresholds(p, q, &T)) return GRAPE_EINVAL;
+    if (g->dist && !g->tables) {
+        set_error("a distributed graph walks after grape_graph_dist_finish");
+        return GRAPE_EINVAL;
+    }
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess) { cudaGetLastError(); cur = -1; }
+    if (cur != g->device) {
+        set_error("current device %d is not the graph's device %d", cur, g->device);
+        return GRAPE_EINVAL;
+    }
+    if (num_walks == 0) return GRAPE_OK;
+    if (classify(starts) != Mem::Device || classify(centers) != Mem::Device || classify(contexts) != Mem::Device ||
+        (num_negatives > 0 && classify(negatives) != Mem::Device) ||
+        (steps_out != nullptr && classify(steps_out) != Mem::Device)) {
+        set_error("grape_walks_skipgram needs device buffers (starts, centers, contexts, negatives, steps_out)");
+        return GRAPE_EINVAL;
+    }
+    cudaError_t e = ensure_node_guide(const_cast<grape_graph*>(g), stream);
+    if (e != cudaSuccess) return cuda_fail(e, "node guide for the negatives");
+    WalkArgs a{};
+    a.starts = starts;
+    a.num_walks = num_walks;
+    a.walk_id_base = walk_id_base;
+    a.L = walk_length;
+    a.seed = walk_seed;
+    a.steps_out = (unsigned long long*)steps_out;
+    if (chunk_walks == 0) {   // an L2-sized chunk: 24 MB of walk rows (two are in flight)
+        chunk_walks = (24ull << 20) / (4ull * walk_length);
+        if (chunk_walks < 1024) chunk_walks = 1024;
+    }
+    e = launch_walks_skipgram(g, a, node2vec != 0, T, window, num_negatives, pair_seed, centers, contexts,
+                              num_negatives ? negatives : nullptr, chunk_walks, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "grape_walks_skipgram");
+    return GRAPE_OK;
+}
+
 grape_status grape_walks_stats(const grape_graph* g, const uint32_t* starts, uint64_t num_walks,
                                uint64_t walk_id_base, uint32_t walk_length, int node2vec, double p,
                                double q, uint64_t seed, uint32_t* out, grape_walk_stats* stats,

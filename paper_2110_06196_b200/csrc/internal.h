@@ -197,6 +197,10 @@ cudaError_t ensure_node_guide(grape_graph* g, cudaStream_t stream);
 cudaError_t launch_skipgram(const grape_graph* g, const uint32_t* walks, uint64_t num_walks, uint64_t base,
                             uint32_t L, uint32_t window, uint32_t K, uint64_t seed, uint32_t* centers,
                             uint32_t* contexts, uint32_t* negs, cudaStream_t stream);
+// skipgram.cu: walks streamed chunk by chunk into the SkipGram consumer (grape_walks_skipgram)
+cudaError_t launch_walks_skipgram(const grape_graph* g, const WalkArgs& a, bool node2vec, const Thresholds& T,
+                                  uint32_t window, uint32_t K, uint64_t pair_seed, uint32_t* centers,
+                                  uint32_t* contexts, uint32_t* negs, uint64_t chunk_walks, cudaStream_t stream);
 cudaError_t launch_walks_tab(const grape_graph* g, const WalkArgs& a, bool node2vec,
                              const Thresholds& T, cudaStream_t stream);
 cudaError_t launch_walks_sm(const grape_graph* g, const WalkArgs& a, bool node2vec,

@@ -209,4 +209,108 @@ cudaError_t launch_skipgram(const grape_graph* g, const uint32_t* walks, uint64_
     return cudaGetLastError();
 }
 
+
+// ---- walks streamed into the SkipGram consumer (grape_walks_skipgram; §8(f) f3) ----
+//
+// The walk matrix is an intermediate of the pair stream: the walker fills one
+// L2-sized chunk of rows at a time into a device buffer under a persisting L2
+// access-policy window, and the pair kernel consumes the chunk from L2 while the
+// walker fills the other buffer (two internal streams, events between them).  The
+// rows never make the full round trip through HBM that walks -> grape_skipgram_pairs
+// costs (one write + one read of W*L*4 bytes), and the walker's partial last wave
+// of each chunk overlaps the pair kernel of the previous chunk.  Results are the
+// two-call results bit for bit: the same walk ids and slot ids.
+cudaError_t launch_walks_skipgram(const grape_graph* g, const WalkArgs& a, bool node2vec, const Thresholds& T,
+                                  uint32_t window, uint32_t K, uint64_t pair_seed, uint32_t* centers,
+                                  uint32_t* contexts, uint32_t* negs, uint64_t chunk_walks, cudaStream_t stream)
+{
+    const uint64_t L = a.L;
+    uint64_t B = chunk_walks ? chunk_walks : a.num_walks;
+    if (B > a.num_walks) B = a.num_walks;
+    if (B == 0) return cudaSuccess;
+    const uint64_t buf_bytes = ((B * L * 4 + 255) / 256) * 256;
+    cudaStream_t sw = nullptr, sp = nullptr;
+    cudaEvent_t start = nullptr, walked[2] = {}, paired[2] = {};
+    char* buf = nullptr;
+    cudaError_t e = cudaStreamCreateWithFlags(&sw, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&sp, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
+    for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+        e = cudaEventCreateWithFlags(&walked[b], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&paired[b], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(start, stream);   // the caller's prior work (starts, outputs)
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sw, start, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sp, start, 0);
+    if (e == cudaSuccess) e = cudaMallocAsync((void**)&buf, 2 * buf_bytes, sw);
+    if (e == cudaSuccess) e = cudaEventRecord(walked[0], sw);   // the buffer exists before sp uses it
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sp, walked[0], 0);
+    // keep the chunk buffers resident in L2 between the walker's stores and the pair
+    // kernel's loads (best effort: a device without a persisting set-aside ignores it)
+    int max_persist = 0, max_window = 0;
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, g->device);
+    cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, g->device);
+    if (e == cudaSuccess && max_persist > 0 && max_window > 0) {
+        size_t want = 2 * buf_bytes < (size_t)max_persist ? 2 * buf_bytes : (size_t)max_persist;
+        size_t cur = 0;
+        cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+        if (cur < want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+        cudaStreamAttrValue v{};
+        v.accessPolicyWindow.base_ptr = buf;
+        v.accessPolicyWindow.num_bytes = 2 * buf_bytes < (size_t)max_window ? 2 * buf_bytes : (size_t)max_window;
+        v.accessPolicyWindow.hitRatio = 1.0f;
+        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cudaStreamSetAttribute(sw, cudaStreamAttributeAccessPolicyWindow, &v);
+        cudaStreamSetAttribute(sp, cudaStreamAttributeAccessPolicyWindow, &v);
+        cudaGetLastError();   // best effort
+    }
+    const uint64_t per_row = L * 2 * window;
+    uint64_t k = 0;
+    for (uint64_t lo = 0; lo < a.num_walks && e == cudaSuccess; lo += B, ++k) {
+        const int b = (int)(k & 1);
+        const uint64_t cnt = a.num_walks - lo < B ? a.num_walks - lo : B;
+        uint32_t* rows = (uint32_t*)(buf + b * buf_bytes);
+        if (k >= 2) e = cudaStreamWaitEvent(sw, paired[b], 0);   // the pair kernel has read this buffer
+        WalkArgs c = a;
+        c.starts = a.starts + lo;
+        c.num_walks = cnt;
+        c.walk_id_base = a.walk_id_base + lo;
+        c.out = rows;
+        if (e == cudaSuccess) e = launch_walks(g, c, node2vec, T, sw);
+        if (e == cudaSuccess) e = cudaEventRecord(walked[b], sw);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(sp, walked[b], 0);
+        if (e == cudaSuccess)
+            e = launch_skipgram(g, rows, cnt, a.walk_id_base + lo, a.L, window, K, pair_seed, centers + lo * per_row,
+                                contexts + lo * per_row, negs ? negs + lo * per_row * K : nullptr, sp);
+        if (e == cudaSuccess) e = cudaEventRecord(paired[b], sp);
+    }
+    // the caller's stream continues after the last pair kernel; the buffer is released
+    // on the pair stream after its last reader
+    // (the pair stream waited for every walker launch, so its end orders everything)
+    cudaEvent_t done = nullptr;
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+    if (buf) cudaFreeAsync(buf, sp);
+    if (e == cudaSuccess) e = cudaEventRecord(done, sp);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, done, 0);
+    if (max_persist > 0) {   // the policy belongs to these streams only; they go away below
+        cudaStreamAttrValue v{};
+        v.accessPolicyWindow.num_bytes = 0;
+        cudaStreamSetAttribute(sw, cudaStreamAttributeAccessPolicyWindow, &v);
+        cudaStreamSetAttribute(sp, cudaStreamAttributeAccessPolicyWindow, &v);
+        cudaGetLastError();
+    }
+    // destroying streams / events with work pending is allowed: resources are released
+    // once the work completes
+    if (sw) cudaStreamDestroy(sw);
+    if (sp) cudaStreamDestroy(sp);
+    if (start) cudaEventDestroy(start);
+    for (int b = 0; b < 2; ++b) {
+        if (walked[b]) cudaEventDestroy(walked[b]);
+        if (paired[b]) cudaEventDestroy(paired[b]);
+    }
+    if (done) cudaEventDestroy(done);
+    return e;
+}
+
 }  // namespace grape

@@ -108,3 +108,36 @@ def test_cfg2_batch_sampled(grape):
     want = float((deg.astype(np.float64) ** 2).sum() / deg.sum())
     got = float(deg[neg].mean())
     assert abs(got - want) / want < 0.02
+
+
+@pytest.mark.parametrize("seed,directed", [(11, False), (12, True)])
+@pytest.mark.parametrize("mode,p,q", [("node2vec", 0.5, 2.0), ("first_order", 1.0, 1.0), ("node2vec", 0.25, 4.0)])
+@pytest.mark.parametrize("chunk", [1, 7, 100, 0])
+def test_walks_skipgram_streamed_equals_two_calls(grape, seed, directed, mode, p, q, chunk):
+    """grape_walks_skipgram (walks streamed chunk by chunk into the pair kernel, no walk
+    matrix) == grape_walks_* then grape_skipgram_pairs, bit for bit, and == the oracle;
+    chunk sizes of 1, 7, 100 rows and the automatic one; the step counter adds up."""
+    g = _with_isolated(900 + seed, 150, 0.04, directed)
+    dg = grape.graph_from_csr(g.off, g.col, g.w, device=0, symmetric=not directed)
+    starts = np.concatenate([np.arange(g.n), [g.n + 3], np.arange(g.n)[::-1]]).astype(np.uint32)
+    st = torch.as_tensor(starts.view(np.int32)).cuda()
+    L, win, K, base = 17, 3, 4, 2 ** 32 - 40
+    n2v = mode == "node2vec"
+    s1 = torch.zeros(1, dtype=torch.int64, device="cuda")
+    s2 = torch.zeros(1, dtype=torch.int64, device="cuda")
+    if n2v:
+        walks = grape.walks_node2vec(dg, st, L, p, q, seed=42, walk_id_base=base, steps=s1)
+    else:
+        walks = grape.walks_first_order(dg, st, L, seed=42, walk_id_base=base, steps=s1)
+    c1, x1, n1 = grape.skipgram_pairs(dg, walks, win, K, seed=9, walk_id_base=base)
+    c2, x2, n2 = grape.walks_skipgram(dg, st, L, win, K, node2vec=n2v, p=p, q=q, seed=42, pair_seed=9,
+                                      walk_id_base=base, steps=s2, chunk_walks=chunk)
+    torch.cuda.synchronize()
+    assert torch.equal(c1, c2) and torch.equal(x1, x2) and torch.equal(n1, n2)
+    assert int(s1.item()) == int(s2.item())
+    o = Oracle(*g.numpy())
+    ew, _ = o.walks(starts, L, mode=mode, p=p, q=q, seed=42, base=base)
+    ec, ex, en = o.skipgram(ew, win, K, seed=9, base=base)
+    assert np.array_equal(c2.cpu().numpy().view(np.uint32), ec)
+    assert np.array_equal(x2.cpu().numpy().view(np.uint32), ex)
+    assert np.array_equal(n2.cpu().numpy().view(np.uint32), en)
