@@ -240,7 +240,9 @@ def _needs_flush(g, W, L):
 
 
 def _workload_desc(k, g, wk, W, flush=False):
-    return {"workload": f"BASELINE configs[{k - 1}]: {CONFIGS[k]['name']}", "mode": wk["mode"], "graph": g.name,
+    wl = (f"BASELINE configs[{k - 1}]: {CONFIGS[k]['name']}" if k <= 5 else
+          f"beyond BASELINE (index-range demonstration): {CONFIGS[k]['name']}")
+    return {"workload": wl, "mode": wk["mode"], "graph": g.name,
             "nodes": g.n, "arcs": g.m, "weighted": g.w is not None, "walks_per_gpu": W, "L": wk["L"],
             "p": wk["p"], "q": wk["q"], "seed": wk["seed"],
             "l2": ("flushed: a 512 MB buffer is written between timed steps (graph + output fit in the 126 MB L2)"

@@ -19,6 +19,11 @@ CONFIGS = {
     5: dict(name="cfg5_rmat26_directed_n2v_p0.25_q4", graph=dict(kind="rmat", scale=26, ef=16, symmetric=False,
                                                                 weights=("geometric", 10.0), sinks=0.05),
             mode="node2vec", p=0.25, q=4.0, walks_per_node=2, L=64, seed=42),
+    # beyond BASELINE (not a BASELINE config): configs[3]'s recipe at 2.2e9 arcs, past the 2^31-arc
+    # range the round-1 tables stopped at (index ranges); bench.py --config 6
+    6: dict(name="x6_chunglu_55M_2.2Garcs_n2v_p2_q0.5", graph=dict(kind="chung_lu", n=55_000_000, m=1_110_000_000,
+                                                                  weights=1000),
+            mode="node2vec", p=2.0, q=0.5, walks_per_node=1, L=100, seed=42),
 }
 
 

@@ -567,9 +567,18 @@ grape_status grape_walks_skipgram(const grape_graph* g, const uint32_t* starts, 
     a.L = walk_length;
     a.seed = walk_seed;
     a.steps_out = (unsigned long long*)steps_out;
-    if (chunk_walks == 0) {   // an L2-sized chunk: 24 MB of walk rows (two are in flight)
-        chunk_walks = (24ull << 20) / (4ull * walk_length);
-        if (chunk_walks < 1024) chunk_walks = 1024;
+    if (chunk_walks == 0) {
+        // Automatic chunk: 4 rounds of the walker's resident lanes (1024 per SM), so each
+        // walker launch has few partial waves, and at least two chunks so that the walker
+        // of chunk k+1 overlaps the pair kernel of chunk k (measured: chunks of 24 MB of
+        // rows, ~half a wave each, ran 0.87x the two separate calls on configs[1]; the
+        // rows' HBM round trip, 4L bytes written and read per walk, is small next to the
+        // pair kernel's 4 (2 + K) 2wL bytes of output per walk).
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
+        chunk_walks = 4ull * 1024 * (uint64_t)(sms > 0 ? sms : 148);
+        if (chunk_walks > (num_walks + 1) / 2) chunk_walks = (num_walks + 1) / 2;
+        if (chunk_walks < 1) chunk_walks = 1;
     }
     e = launch_walks_skipgram(g, a, node2vec != 0, T, window, num_negatives, pair_seed, centers, contexts,
                               num_negatives ? negatives : nullptr, chunk_walks, stream);

@@ -327,7 +327,10 @@ grape_status build_graph(uint32_t n, uint64_t m, const uint64_t* off_in, const u
         int gn = (int)((n + 255ull) / 256);
         if (gn > 148 * 32) gn = 148 * 32;
         if (gn < 1) gn = 1;
-        GRAPE_TRY_ALLOC(g->nodes, (uint64_t)n * sizeof(NodeRec));
+        // whole 32-B sectors plus one (the walker reads a node record as part of an
+        // aligned sector), zeroed: every byte a sector load can touch is initialised
+        GRAPE_TRY_ALLOC(g->nodes, padded((uint64_t)n * sizeof(NodeRec)));
+        GRAPE_TRY_CUDA(cudaMemset(g->nodes, 0, padded((uint64_t)n * sizeof(NodeRec))), "memset");
         if (g->cw_bytes == 4)
             build_nodes<uint32_t><<<gn, 256>>>(g->off, (const uint32_t*)g->cw, n, g->nodes);
         else if (g->cw_bytes == 8)

@@ -30,8 +30,9 @@
 //          bucketised linear probing from bucket floor(fmix32(x) nb / 2^32);
 //          empty = 0xFFFFFFFF (never a node id).  Load factor <= 1/2, so a
 //          lookup reads one sector unless its home bucket is full.
-// Index ranges: 2m < 2^32 - 64 (u32 arc and slot indices), max degree < 2^28 (flag bits, guide
-// bits 30-31, G deg < 2^32), row sums < 2^32 (u32 prefix).  When the tables are
+// Index ranges: m < 2^32 - 64 (u32 arc offsets in node records and records), m/4 + n < 2^32
+// (u32 edge-hash bucket indices), max degree < 2^28 (flag bits, guide bits 30-31,
+// G deg < 2^32), row sums < 2^32 (u32 prefix).  When the tables are
 // built, col / cw / fences are released (graph.cu): nothing reads them after.  Outside them the tables are not built and
 // the v3 walker (fenced searches) runs.
 #include <algorithm>
@@ -349,7 +350,10 @@ constexpr double kReachBytes = 68e9;
 bool tables_in_range(const grape_graph* g)
 {
     const uint64_t m = g->m, n = g->n;
-    return !(2 * m >= (1ull << 32) - 64 || (m >> 2) + n + 2 >= (1ull << 32) || g->max_degree >= (1u << 28) ||
+    // arc offsets (node records, the records' copy of off[x]) are u32 in the walker; edge-hash
+    // bucket indices floor(off / H) + v are u32; degrees leave 4 flag bits in their word;
+    // the guide's per-row bucket index G deg is u32; row sums are u32 prefix values
+    return !(m >= (1ull << 32) - 64 || (m >> 2) + n + 2 >= (1ull << 32) || g->max_degree >= (1u << 28) ||
              g->cw_bytes == 8);
 }
 
@@ -390,7 +394,7 @@ int choose_layout(grape_graph* g, const grape_table_options& o, double budget)
                     const Choice k{recs[ri], gbs[gi], Gs[fi], Hs[hi]};
                     if (found || !allowed(k)) continue;
                     any_allowed = true;
-                    if ((!weighted || ((uint64_t)k.G * m < (1ull << 32) && (uint64_t)k.G * g->max_degree < (1ull << 32))) &&
+                    if ((!weighted || (uint64_t)k.G * g->max_degree < (1ull << 32)) &&
                         size_of(k) <= budget) {
                         c = k;
                         found = true;

@@ -14,6 +14,7 @@
 //
 // One block per walk row (staged in shared memory); its threads write the row's
 // slots, then its negatives, in order: every store of a warp is contiguous.
+#include <cstdlib>
 #include <mutex>
 
 #include "internal.h"
@@ -158,8 +159,10 @@ cudaError_t ensure_node_guide(grape_graph* g, cudaStream_t stream)
 {
     std::lock_guard<std::mutex> lk(g->node_guide_mu);
     if (g->node_guide != nullptr || g->m == 0) return cudaSuccess;
+    uint32_t per_node = 2;   // about two buckets per node (16 B per node)
+    if (const char* s = getenv("GRAPE_SG_GUIDE_PER_NODE")) per_node = (uint32_t)atoi(s) > 0 ? (uint32_t)atoi(s) : 2;
     uint32_t sh = 0;
-    while ((g->m >> sh) + 1 > 2 * (uint64_t)g->n) ++sh;   // about two buckets per node (16 B per node)
+    while ((g->m >> sh) + 1 > (uint64_t)per_node * g->n) ++sh;
     const uint64_t nb = (g->m >> sh) + 1;
     uint2* gidx = nullptr;
     cudaError_t e = cudaMalloc(&gidx, nb * sizeof(uint2));

@@ -224,7 +224,8 @@ def test_specialisation_identities(grape):
         assert torch.equal(x, y) and torch.equal(x, z) and torch.equal(x, v)
 
 
-FULL = [(2, "node2vec"), (3, "node2vec"), (4, "node2vec"), (5, "node2vec"), (5, "first_order")]
+FULL = [(2, "node2vec"), (3, "node2vec"), (4, "node2vec"), (5, "node2vec"), (5, "first_order"),
+        (6, "node2vec")]   # 6: beyond BASELINE, 2.2e9 arcs (> 2^31: the lifted index range)
 
 
 @pytest.mark.parametrize("k,mode", FULL, ids=[f"cfg{k}-{m}" for k, m in FULL])
@@ -240,6 +241,8 @@ def test_full_size_config_sampled(grape, k, mode):
     g = config_graph(k, device="cuda")
     torch.cuda.empty_cache()
     dg = _dev_graph(grape, g)
+    if k == 6:
+        assert g.m > 2 ** 31 and dg.info["tables"] == 1   # the table walker, past the old 2^31-arc range
     deg = (g.off[1:] - g.off[:-1])
     hubs = torch.topk(deg, 100).indices.cpu().numpy()
     sink_all = torch.nonzero(deg == 0).flatten()
