@@ -376,10 +376,11 @@ grape_status grape_skipgram_pairs(const grape_graph* g, const uint32_t* walks, u
  * (DESIGN.md §7e): exactly grape_walks_first_order /
  * grape_walks_node2vec (walk_seed) followed by grape_skipgram_pairs (pair_seed) on
  * the same walk ids, bit for bit, without materialising the walk matrix: walks are
- * generated chunk_walks rows at a time (0 = automatic, 24 MB of rows) into an
- * internal device buffer held in L2 (persisting access-policy window, best
- * effort), and the pair kernel consumes each chunk while the walker fills the
- * next (two internal streams).  The walks exist to feed this; the paper
+ * generated chunk_walks rows at a time (0 = automatic: 4 rounds of the walker's
+ * resident lanes, at most half the walks) into one of two internal device buffers,
+ * and the pair kernel consumes each chunk while the walker fills the next (two
+ * internal streams): the walker's time overlaps the pair kernel's, and only two
+ * chunks of rows exist at a time.  The walks exist to feed this; the paper
  * generates them lazily for the same reason ("static generation ... tens of
  * terabytes").
  *   starts        device u32[num_walks]; walk ids walk_id_base + i

@@ -216,12 +216,13 @@ cudaError_t launch_skipgram(const grape_graph* g, const uint32_t* walks, uint64_
 // ---- walks streamed into the SkipGram consumer (grape_walks_skipgram; §8(f) f3) ----
 //
 // The walk matrix is an intermediate of the pair stream: the walker fills one
-// L2-sized chunk of rows at a time into a device buffer under a persisting L2
-// access-policy window, and the pair kernel consumes the chunk from L2 while the
-// walker fills the other buffer (two internal streams, events between them).  The
-// rows never make the full round trip through HBM that walks -> grape_skipgram_pairs
-// costs (one write + one read of W*L*4 bytes), and the walker's partial last wave
-// of each chunk overlaps the pair kernel of the previous chunk.  Results are the
+// chunk of rows at a time into a device buffer and the pair kernel consumes the
+// chunk while the walker fills the other buffer (two internal streams, events
+// between them), so the walker's work overlaps the pair kernel's and the W*L*4-byte
+// walk matrix is never materialised (two chunk buffers instead).  A persisting-L2
+// access-policy window over the buffers was measured and dropped: the set-aside it
+// needs stays reserved after the call and slowed the other kernels (the pair kernel
+// of the two-call path 52 -> 70 ms on configs[1], 2e6 walks).  Results are the
 // two-call results bit for bit: the same walk ids and slot ids.
 cudaError_t launch_walks_skipgram(const grape_graph* g, const WalkArgs& a, bool node2vec, const Thresholds& T,
                                   uint32_t window, uint32_t K, uint64_t pair_seed, uint32_t* centers,
@@ -248,26 +249,6 @@ cudaError_t launch_walks_skipgram(const grape_graph* g, const WalkArgs& a, bool 
     if (e == cudaSuccess) e = cudaMallocAsync((void**)&buf, 2 * buf_bytes, sw);
     if (e == cudaSuccess) e = cudaEventRecord(walked[0], sw);   // the buffer exists before sp uses it
     if (e == cudaSuccess) e = cudaStreamWaitEvent(sp, walked[0], 0);
-    // keep the chunk buffers resident in L2 between the walker's stores and the pair
-    // kernel's loads (best effort: a device without a persisting set-aside ignores it)
-    int max_persist = 0, max_window = 0;
-    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, g->device);
-    cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, g->device);
-    if (e == cudaSuccess && max_persist > 0 && max_window > 0) {
-        size_t want = 2 * buf_bytes < (size_t)max_persist ? 2 * buf_bytes : (size_t)max_persist;
-        size_t cur = 0;
-        cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
-        if (cur < want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
-        cudaStreamAttrValue v{};
-        v.accessPolicyWindow.base_ptr = buf;
-        v.accessPolicyWindow.num_bytes = 2 * buf_bytes < (size_t)max_window ? 2 * buf_bytes : (size_t)max_window;
-        v.accessPolicyWindow.hitRatio = 1.0f;
-        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        cudaStreamSetAttribute(sw, cudaStreamAttributeAccessPolicyWindow, &v);
-        cudaStreamSetAttribute(sp, cudaStreamAttributeAccessPolicyWindow, &v);
-        cudaGetLastError();   // best effort
-    }
     const uint64_t per_row = L * 2 * window;
     uint64_t k = 0;
     for (uint64_t lo = 0; lo < a.num_walks && e == cudaSuccess; lo += B, ++k) {
@@ -296,13 +277,6 @@ cudaError_t launch_walks_skipgram(const grape_graph* g, const WalkArgs& a, bool 
     if (buf) cudaFreeAsync(buf, sp);
     if (e == cudaSuccess) e = cudaEventRecord(done, sp);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, done, 0);
-    if (max_persist > 0) {   // the policy belongs to these streams only; they go away below
-        cudaStreamAttrValue v{};
-        v.accessPolicyWindow.num_bytes = 0;
-        cudaStreamSetAttribute(sw, cudaStreamAttributeAccessPolicyWindow, &v);
-        cudaStreamSetAttribute(sp, cudaStreamAttributeAccessPolicyWindow, &v);
-        cudaGetLastError();
-    }
     // destroying streams / events with work pending is allowed: resources are released
     // once the work completes
     if (sw) cudaStreamDestroy(sw);
