@@ -9,7 +9,21 @@ HDRS      := $(wildcard $(PKG)/csrc/*.h $(PKG)/csrc/*.cuh) include/grape_walk.h
 OBJS      := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRCS))
 LIB       := $(PKG)/libgrape_walk.so
 
-all: $(LIB) oracle/liboracle.so
+LIBCHK    := $(PKG)/libgrape_walk_checked.so
+OBJSCHK   := $(patsubst $(PKG)/csrc/%.cu,build_checked/%.o,$(SRCS))
+
+all: $(LIB) $(LIBCHK) oracle/liboracle.so
+
+# bounds-checked build (GRAPE_CHECKED: every table access, row write and derived index
+# checked in the kernels; tests/test_gpu_checked.py) — same sources, same ABI
+checked: $(LIBCHK)
+
+build_checked/%.o: $(PKG)/csrc/%.cu $(HDRS)
+	@mkdir -p build_checked
+	$(NVCC) $(NVFLAGS) -DGRAPE_CHECKED=1 -c $< -o $@ 2> build_checked/$*.ptxas.log || (cat build_checked/$*.ptxas.log; false)
+
+$(LIBCHK): $(OBJSCHK)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJSCHK) -cudart static
 
 build/%.o: $(PKG)/csrc/%.cu $(HDRS)
 	@mkdir -p build
@@ -22,6 +36,6 @@ oracle/liboracle.so: oracle/grape_oracle.c
 	gcc -O2 -std=gnu99 -fPIC -shared -ffp-contract=off -fno-fast-math -Wall -o $@ $< -lm
 
 clean:
-	rm -rf build $(LIB) oracle/liboracle.so
+	rm -rf build build_checked $(LIB) $(LIBCHK) oracle/liboracle.so
 
-.PHONY: all clean
+.PHONY: all clean checked

@@ -104,6 +104,7 @@ TabRef tab_of(grape_graph* g, const Layout& L, int t)
     uint64_t bytes = L.bytes[t];
     if (t == 3) bytes = L.bytes[0] >> (L.shift[0] - L.shift[3]);
     map_chunks(owners, bytes, r.shift, g->parts, r.base);
+    r.bytes = t == 3 ? L.bytes[3] : bytes;
     return r;
 }
 

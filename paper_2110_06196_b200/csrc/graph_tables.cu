@@ -314,11 +314,12 @@ __global__ void build_notri(const uint64_t* __restrict__ off, const uint32_t* __
 
 uint64_t padded(uint64_t bytes) { return ((bytes + 31) / 32) * 32 + 32; }
 
-TabRef flat(void* p)
+TabRef flat(void* p, uint64_t bytes)
 {
     TabRef t{};
     t.base[0] = (char*)p;
     t.shift = 63;
+    t.bytes = p ? bytes : 0;
     return t;
 }
 
@@ -511,10 +512,10 @@ grape_status build_tables(grape_graph* g, const grape_table_options& o)
     j.e_lo = j.h_lo = j.b_lo = 0;
     j.e_hi = j.h_hi = m;
     j.b_hi = weighted ? (uint64_t)g->guide_factor * m : 0;
-    j.rec = flat(g->rec);
-    j.guide = flat(g->guide);
-    j.ehash = flat(g->ehash);
-    j.notri = flat(d_notri);
+    j.rec = flat(g->rec, g->rec_alloc);
+    j.guide = flat(g->guide, g->guide_alloc);
+    j.ehash = flat(g->ehash, g->hash_alloc);
+    j.notri = flat(d_notri, m);
     for (int stage = 0; stage < 4 && e == cudaSuccess; ++stage) e = run_table_stage(g, j, stage, d_asym);
     if (e != cudaSuccess) return fail(e, "table kernels");
     g->notri = d_notri != nullptr;

@@ -6,6 +6,32 @@
 #include <cuda_runtime.h>
 #include "grape_walk.h"
 
+// Bounds-checked build (make checked -> libgrape_walk_checked.so, -DGRAPE_CHECKED=1):
+// every table read, row write and index the kernels derive is checked against the
+// allocation it belongs to; a failed check prints the condition and traps (the
+// launch fails with an error the caller sees).  compute-sanitizer is closed on the
+// GPU pool this was developed on; the checked build plus the oracle comparison is
+// what stands in for it (tests/test_gpu_checked.py).  The product
+// build compiles every check away.
+#ifndef GRAPE_CHECKED
+#define GRAPE_CHECKED 0
+#endif
+#if GRAPE_CHECKED
+#include <cstdio>
+#define GRAPE_DCHECK(cond, what)                                                                    \
+    do {                                                                                            \
+        if (!(cond)) {                                                                              \
+            printf("GRAPE_CHECKED: %s failed at %s:%d (block %d thread %d)\n", what, __FILE__,       \
+                   __LINE__, (int)blockIdx.x, (int)threadIdx.x);                                    \
+            __trap();                                                                               \
+        }                                                                                           \
+    } while (0)
+#else
+#define GRAPE_DCHECK(cond, what) \
+    do {                         \
+    } while (0)
+#endif
+
 namespace grape {
 // Fence levels over col and cw: level l+1 holds the last entry of
 // every full 32-byte block of level l, so a search reads one sector per level
@@ -65,8 +91,13 @@ inline void map_chunks(char* const* owner_base, uint64_t bytes, uint32_t k, uint
 struct TabRef {
     char* base[kChunks];
     uint32_t shift;
+    uint64_t bytes;   // table size (checked builds compare every access with it)
     __host__ __device__ char* at(uint64_t byte) const
     {
+#if GRAPE_CHECKED && defined(__CUDA_ARCH__)
+        GRAPE_DCHECK(byte < bytes && (byte >> shift) < (uint64_t)kChunks && base[byte >> shift] != nullptr,
+                     "table access within the table (TabRef)");
+#endif
         return base[byte >> shift] + (byte & ((1ull << shift) - 1));
     }
 };

@@ -74,6 +74,7 @@ struct FastDiv {
 
 struct SgParams {
     const uint64_t* off;
+    uint32_t n;
     const uint2* gidx;
     uint32_t sh;
     uint64_t m;
@@ -135,6 +136,8 @@ __global__ void __launch_bounds__(256) skipgram_kernel(const __grid_constant__ S
                 ++v;
                 while (__ldg(P.off + v + 1) <= e) ++v;               // rows ending at or before e
             }
+            GRAPE_DCHECK(e < P.m && v < P.n && __ldg(P.off + v) <= e && e < __ldg(P.off + v + 1),
+                         "negative = the row holding arc e");
             return v;
         };
         for (uint32_t idx = threadIdx.x; idx < nk; idx += blockDim.x) {
@@ -186,6 +189,7 @@ cudaError_t launch_skipgram(const grape_graph* g, const uint32_t* walks, uint64_
 {
     SgParams P{};
     P.off = g->off;
+    P.n = g->n;
     P.gidx = g->node_guide;
     P.sh = g->node_guide_shift;
     P.m = g->m;

@@ -44,6 +44,7 @@ struct CdfParams {
     bool notri;
     uint4* chunk_scratch;          // per resident warp: chunks_max x {sum lo, sum mid, sum hi, carry}
     uint64_t chunks_max;           // ceil(max degree / 32)
+    uint64_t m_chk;                // arcs (checked build)
 };
 
 __device__ __forceinline__ uint32_t fmix32(uint32_t h)
@@ -117,6 +118,7 @@ __device__ __forceinline__ bool hash_has(const uint32_t* ehash, uint32_t base, u
 template <bool WEIGHTED, bool COMPACT>
 __device__ __forceinline__ void read_rec(const CdfParams& P, uint64_t e, uint32_t& x, uint32_t& hi, bool& nt)
 {
+    GRAPE_DCHECK(e < P.m_chk, "CDF sampler: arc record within the table");
     if constexpr (WEIGHTED && !COMPACT) {
         const uint4* r = reinterpret_cast<const uint4*>(P.rec) + 2 * e;
         const uint4 a = __ldg(r), b = __ldg(r + 1);
@@ -316,6 +318,7 @@ cudaError_t launch(const grape_graph* g, const WalkArgs& a, const Thresholds& T,
     CdfParams P{};
     P.nodes = g->nodes;
     P.rec = g->rec;
+    P.m_chk = g->m;
     P.ehash = g->ehash;
     P.n = g->n;
     P.starts = a.starts;

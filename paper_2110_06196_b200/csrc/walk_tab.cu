@@ -97,6 +97,10 @@ struct TabParams {
     unsigned long long* stats;
     uint32_t tp_m1, t1_m1, tq_m1;   // accept iff u <= T_c - 1
     const PartMap* pmap;            // MODE 3 (§8(f) f4 layout, partition.cu): the partition map
+#if GRAPE_CHECKED
+    uint64_t lim[4];                // checked build: bytes of records, guide, node records, edge hash
+    uint64_t m;
+#endif
 };
 
 __device__ __forceinline__ uint32_t fmix32(uint32_t h)
@@ -228,6 +232,22 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                 addr = (const char*)__ldg((const unsigned long long*)&P.pmap->base[T][o >> ps]) +
                        (o & ((1ull << ps) - 1));
             }
+#if GRAPE_CHECKED
+            if (load) {
+                if (st == ST_START) {
+                    GRAPE_DCHECK(i < P.num_walks, "start index < num_walks");
+                } else {
+                    const uint32_t T = rec ? 0u : gd ? 1u : nd ? 2u : 3u;
+                    GRAPE_DCHECK((e << sh) < P.lim[T], "table read within its table");
+                    if (rec) GRAPE_DCHECK(ri < vdeg && e < P.m, "arc record within the row");
+                    if (gd) GRAPE_DCHECK(idx < P.G * vdeg, "guide bucket within the row");
+                    if (nd) GRAPE_DCHECK(idx < P.n, "node record of a node");
+                    if (st == ST_HASH)
+                        GRAPE_DCHECK(hb >= divH(tstart) + tid && hb < divH(tstart) + tid + divH(tdeg) + 1,
+                                     "hash bucket within t's buckets");
+                }
+            }
+#endif
             if (load) ld8(sector_of(addr), sec);
             j = word_of(addr);
         }
@@ -430,6 +450,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
         // return to t (back, decided by the previous iteration's draw)
         if (GRAPE_TAB_SYNC_EMIT) __syncwarp();
         if (emit || back) {
+            GRAPE_DCHECK(s < L && x < P.n, "walk entry within the row, a node id");
             w.put(s, x);
             ++steps;
             bool need_node = false;
@@ -602,6 +623,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                 draw = false;
                 if (ret) {          // return to t, no read
                     if (k + 1 < GRAPE_TAB_DRAWS && s + 1 < L) {   // emit now; t's row is not empty
+                        GRAPE_DCHECK(s < L && tid < P.n, "returned walk entry within the row");
                         w.put(s, tid);
                         ++steps;
                         uint32_t q;
@@ -715,6 +737,13 @@ cudaError_t launch_k(const grape_graph* g, const WalkArgs& a, const Thresholds& 
         P.fold_x = (uint32_t)(T.Tp - E);
     }
     P.dT = a.dT;
+#if GRAPE_CHECKED
+    P.lim[0] = g->rec_alloc;
+    P.lim[1] = g->guide_alloc;
+    P.lim[2] = ((uint64_t)g->n * sizeof(NodeRec) + 31) / 32 * 32 + 32;
+    P.lim[3] = g->hash_alloc;
+    P.m = g->m;
+#endif
     // blocks per SM x SMs of the graph's device (cached per kernel and device)
     const int resident = resident_blocks(
         (const void*)walk_tab_kernel<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, STATS, MODE>, kBlock, 0, g->device);
