@@ -6,7 +6,7 @@
 // Elias-Fano arrays.
 //
 // Rank on the device: a node guide over arc-index buckets of 2^sh arcs (about
-// two per node), entry b = {rank(b << sh), where that row ends relative to the
+// 2 or 8 per node, ensure_node_guide), entry b = {rank(b << sh), where that row ends relative to the
 // bucket}, built once per graph (lazily, on the first call).  A query reads its
 // bucket's entry and is done when e falls in that row — most arcs belong to rows
 // much longer than a bucket; otherwise it steps over the rows that end at or
@@ -162,8 +162,13 @@ cudaError_t ensure_node_guide(grape_graph* g, cudaStream_t stream)
 {
     std::lock_guard<std::mutex> lk(g->node_guide_mu);
     if (g->node_guide != nullptr || g->m == 0) return cudaSuccess;
-    uint32_t per_node = 2;   // about two buckets per node (16 B per node)
-    if (const char* s = getenv("GRAPE_SG_GUIDE_PER_NODE")) per_node = (uint32_t)atoi(s) > 0 ? (uint32_t)atoi(s) : 2;
+    // buckets per node: 8 (64 B per node; a query past its bucket's first row steps
+    // over fewer rows) while that guide stays L2-sized (<= 128 MB), else 2 (16 B per
+    // node).  Measured on the pair kernel, 2e6 walks x 80, w = 5, K = 5: configs[1]
+    // (1M nodes) 52.5 -> 47.9 ms with 8; configs[4] (67M nodes, the guide in DRAM either
+    // way) 153 -> 164 ms with 8, so 2 there.  GRAPE_SG_GUIDE_PER_NODE overrides (A/B).
+    uint32_t per_node = (uint64_t)g->n * 64 <= (128ull << 20) ? 8 : 2;
+    if (const char* s = getenv("GRAPE_SG_GUIDE_PER_NODE")) per_node = (uint32_t)atoi(s) > 0 ? (uint32_t)atoi(s) : per_node;
     uint32_t sh = 0;
     while ((g->m >> sh) + 1 > (uint64_t)per_node * g->n) ++sh;
     const uint64_t nb = (g->m >> sh) + 1;
