@@ -415,8 +415,11 @@ def run_ours(args):
     if h_out is not None:
         h_steps = torch.zeros(1, dtype=torch.int64)
         time.sleep(1.0)            # the clock sampler's nvidia-smi has just exited (its NVML teardown)
-        call(h_starts, h_out, None)
-        call(h_starts, h_out, None)
+        # warm-up of the host path, as many calls as the device warm-up (at least 2): the first
+        # calls on a freshly pinned multi-GB buffer ran 450-730 ms instead of 65 ms on a box
+        # whose host memory a previous process had just used
+        for _ in range(max(2, args.warmup)):
+            call(h_starts, h_out, None)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize(dev)
