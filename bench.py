@@ -232,6 +232,19 @@ L2_BYTES = 126 * 2 ** 20
 FLUSH_BYTES = 512 * 2 ** 20
 
 
+def _cpu_model() -> str:
+    """The host CPU's model name (lscpu), for the cpu_baseline record."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def _needs_flush(g, W, L):
     """Workloads whose CSR and output fit twice in L2 get an L2 flush between timed steps
     (decided from the CSR, so both arms state the same config)."""
@@ -280,6 +293,7 @@ def run_reference(args):
             "vs_baseline": None, "dtype": "u32/u64 integer", "data": "synthetic (seeded generator)",
             "config": _workload_desc(k, g, wk, W, _needs_flush(g, W, wk["L"])),
             "cpu_baseline": {"value": v, "unit": "steps/s", "cores": cores, "kind": "oracle",
+                             "cpu_model": _cpu_model(),
                              "sample": f"{walks} consecutive walks per step of the workload (bounded sample)"},
             "e2e": {"value": v, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -447,9 +461,14 @@ def run_ours(args):
     cpu = None
     if rank == 0 and not args.no_cpu and world == 1:
         s, secs, walks, cores, att = _oracle_sample(g, wk, args.cpu_budget, dT=dT, sampler=args.sampler)
+        s1, secs1, walks1, _, _ = _oracle_sample(g, wk, max(1.0, args.cpu_budget / 4), dT=dT, sampler=args.sampler,
+                                                 cores=1)
         cpu = {"value": s / secs, "unit": "steps/s", "cores": cores, "kind": "oracle",
+               "cpu_model": _cpu_model(),
+               "single_thread": {"value": s1 / secs1, "unit": "steps/s", "walks": walks1,
+                                 "seconds": round(secs1, 2)},
                "sample": f"first {walks} walks (wid 0..{walks - 1}) of the same workload, "
-                         f"{cores} threads, {secs:.1f} s"}
+                         f"{cores} threads, {secs:.1f} s; single thread: first {walks1} walks, {secs1:.1f} s"}
     # ---- roofline of the walk kernel: event counts from the counting
     # build of the same kernel (grape_walks_stats, untimed), times the measured time.
     roof = None
