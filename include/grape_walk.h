@@ -331,10 +331,12 @@ grape_status grape_graph_dist_import(grape_graph* g, const grape_part_export* ex
 /* Build stage 0 (edge hash), 1 (no-common-neighbour flags), 2 (records) or 3 (guide)
  * of this rank's parts; synchronous; every rank must finish stage k before any
  * starts stage k+1 (barrier).  *flags_out (may be NULL): bit 0 = a reverse arc of
- * different weight was seen (stage 2). */
+ * different weight was seen, bit 1 = an arc has no reverse although GRAPE_SYMMETRIC
+ * was asserted (stage 2). */
 grape_status grape_graph_dist_build(grape_graph* g, uint32_t stage, uint32_t* flags_out);
 /* flags_all = OR over ranks of stage 2's flags_out.  Releases the CSR copy; the
- * graph then walks.  EINVAL when called twice or before import. */
+ * graph then walks.  EINVAL when called twice or before import, or when a rank saw
+ * an arc without its reverse under GRAPE_SYMMETRIC (bit 1). */
 grape_status grape_graph_dist_finish(grape_graph* g, uint32_t flags_all);
 
 /*

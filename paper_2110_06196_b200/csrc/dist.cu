@@ -316,7 +316,7 @@ grape_status grape_graph_dist_build(grape_graph* g, uint32_t stage, uint32_t* fl
     if (e == cudaSuccess) e = cudaMemcpy(&asym, d, 4, cudaMemcpyDeviceToHost);
     cudaFree(d);
     if (e != cudaSuccess) return cuda_fail(e, "grape_graph_dist_build");
-    if (flags_out) *flags_out = asym ? 1u : 0u;
+    if (flags_out) *flags_out = asym;   // bit 0: asymmetric weights; bit 1: GRAPE_SYMMETRIC violated
     return GRAPE_OK;
 }
 
@@ -329,6 +329,10 @@ grape_status grape_graph_dist_finish(grape_graph* g, uint32_t flags_all)
     DeviceGuard guard(g->device);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return cuda_fail(e, "grape_graph_dist_finish");
+    if (flags_all & 2u) {
+        set_error("invalid CSR: GRAPE_SYMMETRIC asserted but an arc has no reverse arc");
+        return GRAPE_EINVAL;
+    }
     g->wsym = g->cw_bytes == 0 || (flags_all & 1u) == 0;
     // the walker reads only the node records and the table parts: drop the CSR copy
     cudaFree(g->col);

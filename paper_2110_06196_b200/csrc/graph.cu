@@ -29,6 +29,8 @@ enum : unsigned {
     BAD_SORT = 1u << 4,        // row not strictly increasing
     BAD_W = 1u << 5,           // weight == 0
     BAD_SYM = 1u << 6,         // GRAPE_SYMMETRIC asserted but an arc has no reverse
+    SELF_LOOP = 1u << 7,       // (not an error) some row holds its own node
+    BAD_MASK = 0x7Fu,
 };
 
 __global__ void check_offsets(const uint64_t* __restrict__ off, uint32_t n, uint64_t m,
@@ -56,6 +58,7 @@ __global__ void check_rows(const uint64_t* __restrict__ off, const uint32_t* __r
             const uint32_t c = col[e];
             if (c >= n) mine |= BAD_COL;
             if (e > lo && col[e - 1] >= c) mine |= BAD_SORT;
+            if (c == (uint32_t)v) mine |= SELF_LOOP;
             if (w != nullptr && w[e] == 0) mine |= BAD_W;
         }
     }
@@ -283,12 +286,18 @@ grape_status build_graph(uint32_t n, uint64_t m, const uint64_t* off_in, const u
         GRAPE_TRY_CUDA(cudaMemcpy(&bad, d_bad, 4, cudaMemcpyDeviceToHost), "validate offsets");
         if (!bad) {
             check_rows<<<rows_grid, kThreads>>>(g->off, g->col, w, n, d_bad);
-            if ((flags & GRAPE_SYMMETRIC) && m) {
+            // GRAPE_SYMMETRIC: when the tables will be built, their record kernel finds every
+            // reverse arc anyway and checks it there (build_tables); else check here
+            g->sym_checked_by_tables = (flags & GRAPE_SYMMETRIC) && !(flags & GRAPE_NO_TABLES);
+            if ((flags & GRAPE_SYMMETRIC) && m && !g->sym_checked_by_tables) {
                 int sms = 0;
                 cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
                 check_symmetric<<<build::item_grid(m, sms), kThreads>>>(g->off, g->col, n, m, d_bad);
             }
             GRAPE_TRY_CUDA(cudaMemcpy(&bad, d_bad, 4, cudaMemcpyDeviceToHost), "validate rows");
+            g->validated = true;
+            g->self_loops = (bad & SELF_LOOP) != 0;
+            bad &= BAD_MASK;
         }
         if (bad) {
             const char* what = (bad & BAD_OFF0)   ? "row_offsets[0] != 0"
@@ -355,6 +364,17 @@ grape_status build_graph(uint32_t n, uint64_t m, const uint64_t* off_in, const u
         st = build_tables(g, opts);
         if (st != GRAPE_OK) return fail(st);
         GRAPE_TRY_CUDA(cudaDeviceSynchronize(), "table build");
+    }
+    if (g->sym_checked_by_tables && !g->tables && m) {   // no tables after all: check GRAPE_SYMMETRIC here
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+        GRAPE_TRY_CUDA(cudaMemset(d_bad, 0, 4), "memset");
+        check_symmetric<<<build::item_grid(m, sms), kThreads>>>(g->off, g->col, n, m, d_bad);
+        GRAPE_TRY_CUDA(cudaMemcpy(&bad, d_bad, 4, cudaMemcpyDeviceToHost), "validate symmetry");
+        if (bad) {
+            set_error("invalid CSR: GRAPE_SYMMETRIC asserted but an arc has no reverse arc");
+            return fail(GRAPE_EINVAL);
+        }
     }
     if (g->tables) {   // the table walker reads only nodes / rec / guide / ehash
         cudaFree(g->col);

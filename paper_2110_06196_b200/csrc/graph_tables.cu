@@ -84,14 +84,19 @@ __device__ inline uint64_t upper_bound_u32(const uint32_t* __restrict__ cw, uint
 // arriving at x through e), NOTRI_REV = notri[rev] (used on a register-decided return
 // x -> v).  Full records keep them in bits 29 / 28 of the degree word, compact records
 // in bits 31 / 30 of x (only when n < 2^30; else never set).
+// sym_half: the flags were computed for arcs t -> v with t < v only (build_notri) and
+// are read from that canonical arc for both directions.  need_rev: every arc must
+// have its reverse (GRAPE_SYMMETRIC, checked here instead of a separate pass;
+// bit 1 of *asym when one has none).
 template <bool WEIGHTED, bool COMPACT>
 __global__ void build_records(const uint64_t* __restrict__ off, const uint32_t* __restrict__ col,
                               const uint32_t* __restrict__ cw, uint32_t n, uint64_t e_lo, uint64_t e_hi,
-                              const TabRef rec, unsigned* __restrict__ asym, const TabRef notri)
+                              const TabRef rec, unsigned* __restrict__ asym, const TabRef notri, bool sym_half,
+                              bool need_rev)
 {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const bool flags = notri.base[0] != nullptr;
-    bool bad = false;
+    bool bad = false, norev = false;
     for (uint64_t e = e_lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < e_hi; e += stride) {
         const uint32_t v = build::row_of(off, n, e);
         const uint64_t lo = off[v];
@@ -99,8 +104,13 @@ __global__ void build_records(const uint64_t* __restrict__ off, const uint32_t* 
         const uint64_t xa = off[x], xb = off[x + 1];
         const uint64_t j = lower_bound_u32(col, xa, xb, v);
         const bool found = j < xb && col[j] == v;
+        norev |= !found;
         uint32_t fl = 0;   // flag bits (0: self, 1: reverse)
-        if (flags) fl = (*notri.at(e) ? 1u : 0u) | (found && *notri.at(j) ? 2u : 0u);
+        if (flags && sym_half && found) {   // one flag per undirected edge, on the arc from the smaller id
+            fl = *notri.at(v < x ? e : j) ? 3u : 0u;
+        } else if (flags) {
+            fl = (*notri.at(e) ? 1u : 0u) | (found && *notri.at(j) ? 2u : 0u);
+        }
         const uint32_t xf = COMPACT ? (x | (fl & 1) << 31 | (fl >> 1) << 30) : x;   // compact: bits 31 (self), 30 (rev)
         const uint32_t df = COMPACT ? 0u : ((fl & 1) << 29 | (fl >> 1) << 28);   // full: bits 29, 28 of deg
         if (WEIGHTED) {
@@ -129,6 +139,7 @@ __global__ void build_records(const uint64_t* __restrict__ off, const uint32_t* 
         }
     }
     if (WEIGHTED && bad) atomicOr(asym, 1u);
+    if (need_rev && norev) atomicOr(asym, 2u);
 }
 
 // Guide entries, one thread per bucket of [b_lo, b_hi) (global bucket gb = G off[v]
@@ -256,8 +267,12 @@ __device__ inline bool hash_has(const TabRef& ehash, uint64_t base, uint64_t nb,
 
 constexpr uint64_t kCoopLen = 32;
 
+// sym_half (a symmetric graph without self-loops): the common neighbours of t and v
+// other than t are those other than v (t is not in N(t), v is not in N(v)), so the
+// flag of t -> v equals that of v -> t: only arcs with t < v are computed.
 __global__ void build_notri(const uint64_t* __restrict__ off, const uint32_t* __restrict__ col, uint32_t n,
-                            uint64_t e_lo, uint64_t e_hi, uint32_t H, const TabRef ehash, const TabRef notri)
+                            uint64_t e_lo, uint64_t e_hi, uint32_t H, const TabRef ehash, const TabRef notri,
+                            bool sym_half)
 {
     const unsigned lane = threadIdx.x & 31;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -270,9 +285,11 @@ __global__ void build_notri(const uint64_t* __restrict__ off, const uint32_t* __
         uint32_t t = 0;
         uint64_t sa = 0, sb = 0;          // the scanned (shorter) row
         uint64_t hbase = 0, hnb = 0;      // the probed row's hash buckets
+        bool skip = false;
         if (valid) {
             t = build::row_of(off, n, e);
             const uint32_t v = col[e];
+            skip = sym_half && v < t;   // the reverse arc carries this edge's flag
             const uint64_t ta = off[t], tb = off[t + 1], va = off[v], vb = off[v + 1];
             if (vb - va <= tb - ta) {   // x in N(v), x != t: in N(t)?
                 sa = va; sb = vb;
@@ -283,8 +300,9 @@ __global__ void build_notri(const uint64_t* __restrict__ off, const uint32_t* __
             }
         }
         bool common = false;
-        const bool coop = valid && sb - sa > kCoopLen;
-        if (valid && !coop)
+        if (skip) sa = sb = 0;   // nothing to scan
+        const bool coop = valid && !skip && sb - sa > kCoopLen;
+        if (valid && !skip && !coop)
             for (uint64_t f = sa; f < sb && !common; ++f) {
                 const uint32_t x = col[f];
                 common = x != t && hash_has(ehash, hbase, hnb, x);
@@ -308,7 +326,7 @@ __global__ void build_notri(const uint64_t* __restrict__ off, const uint32_t* __
             }
             if ((int)lane == src) common = found;
         }
-        if (valid) *reinterpret_cast<uint8_t*>(notri.at(e)) = common ? 0 : 1;
+        if (valid && !skip) *reinterpret_cast<uint8_t*>(notri.at(e)) = common ? 0 : 1;
     }
 }
 
@@ -426,6 +444,10 @@ int choose_layout(grape_graph* g, const grape_table_options& o, double budget)
 cudaError_t run_table_stage(const grape_graph* g, const TableJob& j, int stage, unsigned* asym)
 {
     const bool weighted = g->cw_bytes != 0;
+    // one no-common-neighbour flag per undirected edge: a symmetric graph (validated, or
+    // validated by this very build: need_rev) without self-loops
+    const bool sym_half = (g->flags & GRAPE_SYMMETRIC) && g->validated && !g->self_loops;
+    const bool need_rev = g->sym_checked_by_tables;
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
     const uint32_t* cw = (const uint32_t*)g->cw;
@@ -438,21 +460,23 @@ cudaError_t run_table_stage(const grape_graph* g, const TableJob& j, int stage, 
     case 1:
         if (j.notri.base[0] != nullptr && j.e_hi > j.e_lo)
             build_notri<<<build::item_grid(j.e_hi - j.e_lo, sms), kThreads>>>(g->off, g->col, g->n, j.e_lo, j.e_hi,
-                                                                              g->hash_h, j.ehash, j.notri);
+                                                                              g->hash_h, j.ehash, j.notri, sym_half);
         break;
     case 2: {
         if (j.e_hi <= j.e_lo) break;
         const int grid = build::item_grid(j.e_hi - j.e_lo, sms);
         if (weighted && g->compact)
-            build_records<true, true><<<grid, kThreads>>>(g->off, g->col, cw, g->n, j.e_lo, j.e_hi, j.rec, asym, j.notri);
+            build_records<true, true><<<grid, kThreads>>>(g->off, g->col, cw, g->n, j.e_lo, j.e_hi, j.rec, asym, j.notri, sym_half,
+                                                          need_rev);
         else if (weighted)
-            build_records<true, false><<<grid, kThreads>>>(g->off, g->col, cw, g->n, j.e_lo, j.e_hi, j.rec, asym, j.notri);
+            build_records<true, false><<<grid, kThreads>>>(g->off, g->col, cw, g->n, j.e_lo, j.e_hi, j.rec, asym, j.notri, sym_half,
+                                                          need_rev);
         else if (g->compact)
             build_records<false, true><<<grid, kThreads>>>(g->off, g->col, nullptr, g->n, j.e_lo, j.e_hi, j.rec, asym,
-                                                           j.notri);
+                                                           j.notri, sym_half, need_rev);
         else
             build_records<false, false><<<grid, kThreads>>>(g->off, g->col, nullptr, g->n, j.e_lo, j.e_hi, j.rec, asym,
-                                                            j.notri);
+                                                            j.notri, sym_half, need_rev);
         break;
     }
     case 3:
@@ -521,6 +545,15 @@ grape_status build_tables(grape_graph* g, const grape_table_options& o)
     g->notri = d_notri != nullptr;
     unsigned asym = 0;
     if ((e = cudaMemcpy(&asym, d_asym, 4, cudaMemcpyDeviceToHost)) != cudaSuccess) return fail(e, "table build");
+    if (asym & 2u) {   // GRAPE_SYMMETRIC asserted, checked by the record kernel
+        cudaFree(d_asym);
+        cudaFree(d_notri);
+        d_asym = nullptr;
+        d_notri = nullptr;
+        destroy_tables(g);
+        set_error("invalid CSR: GRAPE_SYMMETRIC asserted but an arc has no reverse arc");
+        return GRAPE_EINVAL;
+    }
     cudaFree(d_asym);
     cudaFree(d_notri);
     g->wsym = !weighted || asym == 0;

@@ -150,6 +150,12 @@ struct grape_graph {
     // distributed build (dist.cu): this process owns part dist_part of every table; the
     // others were opened by CUDA IPC (closed, not freed, by destroy_graph); the
     // no-common-neighbour flags live in parts of 2^notri_shift bytes while building
+    // validation state (graph.cu): the CSR was validated; some row holds its own node;
+    // GRAPE_SYMMETRIC is checked by the table build (its record kernel finds every
+    // reverse arc) instead of a separate pass
+    bool validated = false;
+    bool self_loops = true;
+    bool sym_checked_by_tables = false;
     bool dist = false;
     uint32_t dist_part = 0;
     bool part_ipc[5][8] = {};
