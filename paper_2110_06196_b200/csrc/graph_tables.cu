@@ -266,6 +266,14 @@ __device__ inline bool hash_has(const TabRef& ehash, uint64_t base, uint64_t nb,
 }
 
 constexpr uint64_t kCoopLen = 32;
+// Scans of more than kNotriScanCap entries stop there with the flag clear ("may share a
+// neighbour": the walker then tests membership as usual).  The flag only enables a
+// shortcut, so clearing it never changes a walk; it bounds the build's cost on pairs
+// of high-degree nodes with no common neighbour (full scans of long rows).
+#ifndef GRAPE_NOTRI_SCAN_CAP
+#define GRAPE_NOTRI_SCAN_CAP (1ull << 62)
+#endif
+constexpr uint64_t kNotriScanCap = GRAPE_NOTRI_SCAN_CAP;
 
 // sym_half (a symmetric graph without self-loops): the common neighbours of t and v
 // other than t are those other than v (t is not in N(t), v is not in N(v)), so the
@@ -299,6 +307,8 @@ __global__ void build_notri(const uint64_t* __restrict__ off, const uint32_t* __
                 hbase = va / H + v; hnb = (vb - va) / H + 1;
             }
         }
+        const bool capped = sb - sa > kNotriScanCap;   // too long to scan: the flag stays clear
+        if (capped) sb = sa;
         bool common = false;
         if (skip) sa = sb = 0;   // nothing to scan
         const bool coop = valid && !skip && sb - sa > kCoopLen;
@@ -326,7 +336,7 @@ __global__ void build_notri(const uint64_t* __restrict__ off, const uint32_t* __
             }
             if ((int)lane == src) common = found;
         }
-        if (valid && !skip) *reinterpret_cast<uint8_t*>(notri.at(e)) = common ? 0 : 1;
+        if (valid && !skip) *reinterpret_cast<uint8_t*>(notri.at(e)) = (common || capped) ? 0 : 1;
     }
 }
 

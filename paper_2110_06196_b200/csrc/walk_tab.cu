@@ -69,9 +69,7 @@ constexpr int kDrawUnroll = GRAPE_TAB_DRAW_UNROLL;
 #ifndef GRAPE_TAB_MIN_BLOCKS
 #define GRAPE_TAB_MIN_BLOCKS 4
 #endif
-#ifndef GRAPE_TAB_STASH
-#define GRAPE_TAB_STASH 1        // keep a 32-B record in shared memory across its membership test
-#endif
+
 
 struct TabParams {
     const NodeRec* nodes;
@@ -165,12 +163,6 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
         for (int q = 0; q < kStatsWords; ++q) cnt[q] = 0;
     }
     __shared__ uint32_t stage[8 * kBlock];
-    // 32-B records (weighted, not compact): the record whose x goes through a membership
-    // test is kept here (per lane, transposed like the row stage), so an accepted x is
-    // emitted from shared memory instead of re-reading its record or guide entry
-    constexpr bool STASH = GRAPE_TAB_STASH && WEIGHTED && !COMPACT;
-    __shared__ uint32_t stash[STASH ? 8 * kBlock : 1];
-    bool stashed = false;
     RowWriter w;
     w.slot = stage + threadIdx.x;
     const uint32_t L = P.L;
@@ -386,11 +378,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
             }
             if (found || empty) {
                 if (found ? u <= P.t1_m1 : u <= P.tq_m1) {
-                    if (STASH && stashed) {   // x's record was kept in shared memory
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) sec[q] = stash[q * kBlock + threadIdx.x];
-                        emit = true;
-                    } else if constexpr (WEIGHTED) {
+                    if constexpr (WEIGHTED) {
                         acc = true;   // read the record again for x's data
                         scan = false;
                         st = gsrc ? ST_GUIDE : ST_REC;
@@ -447,13 +435,6 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                 if (STATS) ++cnt[C_MEMB];
                 st = ST_HASH;   // home bucket of x among t's floor(deg t / H) + 1 buckets
                 hb = divH(tstart) + tid + (uint32_t)(((uint64_t)fmix32(x) * (divH(tdeg) + 1)) >> 32);
-                if (STASH) {
-                    stashed = have_rec;
-                    if (have_rec) {
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) stash[q * kBlock + threadIdx.x] = sec[q];
-                    }
-                }
             } else if (!ok) {
                 draw = true;
                 ++a;

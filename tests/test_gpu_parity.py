@@ -322,7 +322,11 @@ def test_invalid_inputs_rejected(grape):
         grape.graph_from_csr(off, col, w)                  # weight 0
     d = tiny_graph(4, 10, 0.3, directed=True)
     with pytest.raises(grape.GrapeError):
-        grape.graph_from_csr(d.off, d.col, symmetric=True)   # asymmetric with SYMMETRIC
+        grape.graph_from_csr(d.off, d.col, symmetric=True)   # asymmetric with SYMMETRIC (caught by the table build)
+    with pytest.raises(grape.GrapeError):
+        grape.graph_from_csr(d.off, d.col, symmetric=True, tables=False)   # (by the validation pass)
+    with pytest.raises(grape.GrapeError):   # tables that do not fit: the v3 walker, checked after the attempt
+        grape.graph_from_csr(d.off, d.col, symmetric=True, layout={"table_budget_bytes": 1})
     dg = grape.graph_from_csr(off, col, symmetric=True)
     st = torch.arange(10, dtype=torch.int32, device="cuda")
     for p, q in [(0.0, 1.0), (1.0, -2.0), (float("nan"), 1.0), (2.0 ** 25, 1.0)]:
