@@ -342,6 +342,8 @@ def run_ours(args):
         dg.partition([local] * args.parts)
     info = dg.info
     W_total = g.n * wk["walks_per_node"]          # the config's walk list (iteration-major)
+    if args.max_walks:                            # profiling runs: the first walks of the list only
+        W_total = min(W_total, args.max_walks)
     L = wk["L"]
     lo, hi = rank_slice(W_total, W_total, rank, world, args.scaling)
     base = lo
@@ -349,7 +351,7 @@ def run_ours(args):
     if args.scaling == "strong":
         starts = starts_per_node(g.n, wk["walks_per_node"], device=dev)[lo:hi].contiguous()
     else:
-        starts = starts_per_node(g.n, wk["walks_per_node"], device=dev)
+        starts = starts_per_node(g.n, wk["walks_per_node"], device=dev)[:W].contiguous()
     out = torch.empty((W, L), dtype=torch.int32, device=dev)
     steps_ctr = torch.zeros(1, dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -587,6 +589,8 @@ def run_ours(args):
                                  "weak: every rank walks W wids on its own block [r W, (r+1) W)")})
         if args.scale_down:
             cfg["scale_down"] = args.scale_down
+        if args.max_walks:
+            cfg["max_walks"] = args.max_walks
         if args.dist_tables:
             cfg["tables"] = (f"distributed: rank r owns part r of the sampling tables ({world} parts, CUDA IPC), "
                              f"every rank walks over all parts")
@@ -771,6 +775,8 @@ def main():
                     help="N > 1: strong = the config's fixed walk list sharded by start node (north_star); "
                          "weak = the whole per-GPU workload on every rank")
     ap.add_argument("--scale-down", type=int, default=0, help="shrink the config's graph by 2^k (tests)")
+    ap.add_argument("--max-walks", type=int, default=0,
+                    help="walk only the first N walks of the config's list (ncu captures of the long configs)")
     ap.add_argument("--device", type=int, default=None,
                     help="CUDA device of every rank (default LOCAL_RANK); tests pin two ranks to cuda:0")
     ap.add_argument("--dist-backend", default=None, choices=["nccl", "gloo"],
