@@ -69,6 +69,9 @@ constexpr int kDrawUnroll = GRAPE_TAB_DRAW_UNROLL;
 #ifndef GRAPE_TAB_MIN_BLOCKS
 #define GRAPE_TAB_MIN_BLOCKS 4
 #endif
+#ifndef GRAPE_TAB_PREDRAW
+#define GRAPE_TAB_PREDRAW 0      // one attempt of pure-draw lanes in the shadow of the warp's loads
+#endif
 
 
 struct TabParams {
@@ -273,7 +276,142 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
         // unweighted membership test, in the kept registers (kept)
         bool have_rec = false;   // the sector in hand is x's record
         bool kept = false;
-        if (st == ST_REC) {
+        // one attempt of a drawing lane: Philox, the band of u, the decisions that need no
+        // read (§8(c) c12); more: another draw follows in this iteration (a register-decided
+        // return is then emitted on the spot)
+        auto draw_once = [&](const bool more, const bool sub) {
+            if (STATS) ++cnt[C_ATTEMPT];
+            Draw dr;
+            uint32_t o3 = 0;
+            if constexpr (FOLD) {   // all four words: o3 decides the return's excess mass
+                const uint4 o = philox_block_rk(P.rk, P.base + i, s, a);
+                dr.x64 = (uint64_t)o.y << 32 | o.x;
+                dr.u = o.z;
+                o3 = o.w;
+            } else {
+                dr = philox_draw_rk(P.rk, P.base + i, s, a);
+            }
+            u = dr.u;
+            bool known = tlo <= thi;
+            uint32_t bs = 0;                 // SUSS: the proposed candidate
+            if (SUSS && sub) {
+                if constexpr (WEIGHTED) {    // first candidate whose running weight exceeds r
+                    r = bounded32(dr.x64, wc);
+                    uint32_t lo = 0, hi = P.dT;
+                    while (lo < hi) {
+                        const uint32_t mid = (lo + hi) >> 1;
+                        if (P.scratch[(uint64_t)(2 * mid) * P.lanes + gl] <= r) lo = mid + 1;
+                        else hi = mid;
+                    }
+                    bs = lo;
+                    r = bs;                  // "x == t" <=> the candidate is t's
+                    known = true;
+                } else {                     // uniform candidate; its row index vs t's
+                    bs = bounded32(dr.x64, P.dT);
+                    r = suss_index(bs);
+                }
+            } else {
+                r = bounded32(dr.x64, vW);   // index (unweighted: vW = deg) or weight point
+            }
+            bool need_x = true, ret = false;
+            bool outlier = false;
+            if (FOLD && tid != kNone) {   // o3 * M < N * 2^32, N = w_vt X, M = W_v E + N
+                const uint64_t N = known ? (uint64_t)(thi - tlo) * P.fold_x : 0;   // w_vt = width of t's interval
+                const uint64_t M = (uint64_t)vW * P.fold_e + N;
+                const uint64_t p1 = (uint64_t)o3 * (M >> 32) + (((uint64_t)o3 * (uint32_t)M) >> 32);
+                outlier = p1 < N;
+            }
+            if (outlier) {
+                need_x = false;
+                ret = true;
+                if (STATS) ++cnt[C_ALU];
+            } else if (NODE2VEC && tid != kNone) {
+                const bool cp = u <= P.tp_m1, cq = u <= P.tq_m1, c1 = nt ? cq : u <= P.t1_m1;
+                if (cp == c1 && c1 == cq) {
+                    need_x = cp;
+                } else if (c1 == cq && known) {   // only "x == t" matters, and it is known
+                    const bool is_t = (SUSS && WEIGHTED && sub) ? bs == bt : r - tlo < thi - tlo;
+                    const bool ok = is_t ? cp : c1;
+                    need_x = ok && !is_t;
+                    ret = ok && is_t;
+                }
+                if (STATS) cnt[C_ALU] += !need_x;
+            }
+            acc = false;
+            scan = false;
+            gsrc = false;
+            draw = false;
+            if (ret) {          // return to t, no read
+                if (more && s + 1 < L) {   // emit now; t's row is not empty
+                    GRAPE_DCHECK(s < L && tid < P.n, "returned walk entry within the row");
+                    w.put(s, tid);
+                    ++steps;
+                    uint32_t q;
+                    q = vstart; vstart = tstart; tstart = q;
+                    q = vdeg; vdeg = tdeg; tdeg = q;
+                    q = vW; vW = tW; tW = q;
+                    q = vid; vid = tid; tid = q;
+                    q = tlo; tlo = slo; slo = q;
+                    q = thi; thi = shi; shi = q;
+                    const bool b_ = nt; nt = ntr; ntr = b_;
+                    ++s;
+                    a = 0;
+                    cb = 0;
+                    draw = true;
+                } else {        // emitted next iteration
+                    x = tid;
+                }
+                st = ST_BACK;
+            } else if (!need_x) {
+                ++a;            // rejected without reading the graph
+                st = ST_DRAW;
+                draw = true;
+            } else if (SUSS && WEIGHTED && sub) {   // x is in scratch: decide, then read its record
+                x = P.scratch[(uint64_t)(2 * bs + 1) * P.lanes + gl];
+                ri = suss_index(bs);
+                bool ok = true, hash = false;
+                if (NODE2VEC && tid != kNone) {
+                    const bool cp = u <= P.tp_m1, cq = u <= P.tq_m1, c1 = nt ? cq : u <= P.t1_m1;
+                    if (x == tid) ok = cp;
+                    else if (!NEED_MEMBER || c1 == cq) ok = c1;
+                    else hash = true;
+                }
+                if (hash) {
+                    if (STATS) ++cnt[C_MEMB];
+                    st = ST_HASH;
+                    hb = divH(tstart) + tid + (uint32_t)(((uint64_t)fmix32(x) * (divH(tdeg) + 1)) >> 32);
+                } else if (ok) {
+                    acc = true;
+                    st = ST_REC;
+                } else {
+                    ++a;
+                    st = ST_DRAW;
+                    draw = true;
+                }
+            } else if constexpr (WEIGHTED) {
+                if (vdeg == 1) {
+                    ri = 0;
+                    st = ST_REC;
+                } else {
+                    idx = bounded32(dr.x64, P.G * vdeg);   // guide bucket
+                    st = ST_GUIDE;
+                }
+            } else {
+                ri = r;
+                st = ST_REC;
+            }
+        };
+        const uint32_t st0 = st;   // the state this iteration's load served (the dispatch below)
+#if GRAPE_TAB_PREDRAW
+        // lanes that only draw this iteration make one attempt here, while the loads the
+        // other lanes of the warp just issued are in flight (they draw again below)
+        if constexpr (!SUSS) {
+            if (__any_sync(0xffffffffu, st0 == ST_DRAW)) {
+                if (st0 == ST_DRAW) draw_once(true, false);
+            }
+        }
+#endif
+        if (st0 == ST_REC) {
             have_rec = true;
             bool found = true;
             if constexpr (WEIGHTED && COMPACT) {   // 16-B {x, hi, rlo, rhi} at word j (0 or 4)
@@ -306,7 +444,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                 if (acc) emit = true;
                 else decide = true;
             }
-        } else if (st == ST_GUIDE) {
+        } else if (st0 == ST_GUIDE) {
             uint32_t e0, e1;
             bool split;
             if constexpr (FAT) {   // unsplit: a record copy; split: {i_lo, cw[i_lo], .., flags in word 5}
@@ -338,7 +476,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                 x = e1;
                 decide = true;
             }
-        } else if (SUSS && WEIGHTED && st == ST_CAND) {   // candidate cb's record: its node and weight
+        } else if (SUSS && WEIGHTED && st0 == ST_CAND) {   // candidate cb's record: its node and weight
             bool done = true;
             uint32_t wgt = 0;
             if constexpr (COMPACT) {
@@ -369,7 +507,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                 if (cb < P.dT) ri = suss_index(cb);
                 else draw = true;
             }
-        } else if (st == ST_HASH) {   // one bucket (8 slots) of t's set
+        } else if (st0 == ST_HASH) {   // one bucket (8 slots) of t's set
             bool found = false, empty = false;
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
@@ -394,7 +532,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                 const uint32_t base = divH(tstart) + tid;
                 hb = hb + 1 == base + divH(tdeg) + 1 ? base : hb + 1;
             }
-        } else if (st == ST_NODE) {   // node record: a start node, or (compact records) a taken arc's head
+        } else if (st0 == ST_NODE) {   // node record: a start node, or (compact records) a taken arc's head
             const bool h = (j & 4) != 0;
             vstart = h ? sec[4] : sec[0];
             vdeg = h ? sec[6] : sec[2];
@@ -403,7 +541,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
             cb = 0;
             if (vdeg == 0) fin = true;
             else draw = true;
-        } else if (st == ST_START) {
+        } else if (st0 == ST_START) {
             const uint32_t start = pick8(sec, j);
             w.begin(P.out + i * L);
             s = 0;
@@ -560,128 +698,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                 ri = suss_index(0);
                 st = ST_CAND;
             }
-            if (draw) {
-                if (STATS) ++cnt[C_ATTEMPT];
-                Draw dr;
-                uint32_t o3 = 0;
-                if constexpr (FOLD) {   // all four words: o3 decides the return's excess mass
-                    const uint4 o = philox_block_rk(P.rk, P.base + i, s, a);
-                    dr.x64 = (uint64_t)o.y << 32 | o.x;
-                    dr.u = o.z;
-                    o3 = o.w;
-                } else {
-                    dr = philox_draw_rk(P.rk, P.base + i, s, a);
-                }
-                u = dr.u;
-                bool known = tlo <= thi;
-                uint32_t bs = 0;                 // SUSS: the proposed candidate
-                if (SUSS && sub) {
-                    if constexpr (WEIGHTED) {    // first candidate whose running weight exceeds r
-                        r = bounded32(dr.x64, wc);
-                        uint32_t lo = 0, hi = P.dT;
-                        while (lo < hi) {
-                            const uint32_t mid = (lo + hi) >> 1;
-                            if (P.scratch[(uint64_t)(2 * mid) * P.lanes + gl] <= r) lo = mid + 1;
-                            else hi = mid;
-                        }
-                        bs = lo;
-                        r = bs;                  // "x == t" <=> the candidate is t's
-                        known = true;
-                    } else {                     // uniform candidate; its row index vs t's
-                        bs = bounded32(dr.x64, P.dT);
-                        r = suss_index(bs);
-                    }
-                } else {
-                    r = bounded32(dr.x64, vW);   // index (unweighted: vW = deg) or weight point
-                }
-                bool need_x = true, ret = false;
-                bool outlier = false;
-                if (FOLD && tid != kNone) {   // o3 * M < N * 2^32, N = w_vt X, M = W_v E + N
-                    const uint64_t N = known ? (uint64_t)(thi - tlo) * P.fold_x : 0;   // w_vt = width of t's interval
-                    const uint64_t M = (uint64_t)vW * P.fold_e + N;
-                    const uint64_t p1 = (uint64_t)o3 * (M >> 32) + (((uint64_t)o3 * (uint32_t)M) >> 32);
-                    outlier = p1 < N;
-                }
-                if (outlier) {
-                    need_x = false;
-                    ret = true;
-                    if (STATS) ++cnt[C_ALU];
-                } else if (NODE2VEC && tid != kNone) {
-                    const bool cp = u <= P.tp_m1, cq = u <= P.tq_m1, c1 = nt ? cq : u <= P.t1_m1;
-                    if (cp == c1 && c1 == cq) {
-                        need_x = cp;
-                    } else if (c1 == cq && known) {   // only "x == t" matters, and it is known
-                        const bool is_t = (SUSS && WEIGHTED && sub) ? bs == bt : r - tlo < thi - tlo;
-                        const bool ok = is_t ? cp : c1;
-                        need_x = ok && !is_t;
-                        ret = ok && is_t;
-                    }
-                    if (STATS) cnt[C_ALU] += !need_x;
-                }
-                acc = false;
-                scan = false;
-                gsrc = false;
-                draw = false;
-                if (ret) {          // return to t, no read
-                    if (k + 1 < GRAPE_TAB_DRAWS && s + 1 < L) {   // emit now; t's row is not empty
-                        GRAPE_DCHECK(s < L && tid < P.n, "returned walk entry within the row");
-                        w.put(s, tid);
-                        ++steps;
-                        uint32_t q;
-                        q = vstart; vstart = tstart; tstart = q;
-                        q = vdeg; vdeg = tdeg; tdeg = q;
-                        q = vW; vW = tW; tW = q;
-                        q = vid; vid = tid; tid = q;
-                        q = tlo; tlo = slo; slo = q;
-                        q = thi; thi = shi; shi = q;
-                        const bool b_ = nt; nt = ntr; ntr = b_;
-                        ++s;
-                        a = 0;
-                        cb = 0;
-                        draw = true;
-                    } else {        // emitted next iteration
-                        x = tid;
-                    }
-                    st = ST_BACK;
-                } else if (!need_x) {
-                    ++a;            // rejected without reading the graph
-                    st = ST_DRAW;
-                    draw = true;
-                } else if (SUSS && WEIGHTED && sub) {   // x is in scratch: decide, then read its record
-                    x = P.scratch[(uint64_t)(2 * bs + 1) * P.lanes + gl];
-                    ri = suss_index(bs);
-                    bool ok = true, hash = false;
-                    if (NODE2VEC && tid != kNone) {
-                        const bool cp = u <= P.tp_m1, cq = u <= P.tq_m1, c1 = nt ? cq : u <= P.t1_m1;
-                        if (x == tid) ok = cp;
-                        else if (!NEED_MEMBER || c1 == cq) ok = c1;
-                        else hash = true;
-                    }
-                    if (hash) {
-                        if (STATS) ++cnt[C_MEMB];
-                        st = ST_HASH;
-                        hb = divH(tstart) + tid + (uint32_t)(((uint64_t)fmix32(x) * (divH(tdeg) + 1)) >> 32);
-                    } else if (ok) {
-                        acc = true;
-                        st = ST_REC;
-                    } else {
-                        ++a;
-                        st = ST_DRAW;
-                        draw = true;
-                    }
-                } else if constexpr (WEIGHTED) {
-                    if (vdeg == 1) {
-                        ri = 0;
-                        st = ST_REC;
-                    } else {
-                        idx = bounded32(dr.x64, P.G * vdeg);   // guide bucket
-                        st = ST_GUIDE;
-                    }
-                } else {
-                    ri = r;
-                    st = ST_REC;
-                }
-            }
+            if (draw) draw_once(k + 1 < GRAPE_TAB_DRAWS, sub);
         }
         if (draw) st = ST_DRAW;   // still drawing: no load next iteration
     }

@@ -141,3 +141,15 @@ def test_binding_rejects_mismatched_output_buffers():
             grape._check_steps(bad, False, 0)
     with pytest.raises(ValueError, match="cuda:0"):
         grape._check_steps(torch.zeros(1, dtype=torch.int64), True, 0)
+
+
+def test_chunked_table_layout_host_logic(tmp_path):
+    """The chunk / owner arithmetic of the partitioned and distributed table layouts
+    (csrc/internal.h), compiled for the host and checked exhaustively over sizes and
+    owner counts (tests/pins/chunks_test.cpp)."""
+    exe = tmp_path / "chunks_test"
+    src = os.path.join(ROOT, "tests", "pins", "chunks_test.cpp")
+    subprocess.check_call(["g++", "-O1", "-std=c++17", "-I/usr/local/cuda/include", "-Iinclude", src, "-o", str(exe)],
+                          cwd=ROOT)
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 0 and "chunks_test: ok" in out.stdout, out.stdout + out.stderr
