@@ -69,9 +69,7 @@ constexpr int kDrawUnroll = GRAPE_TAB_DRAW_UNROLL;
 #ifndef GRAPE_TAB_MIN_BLOCKS
 #define GRAPE_TAB_MIN_BLOCKS 4
 #endif
-#ifndef GRAPE_TAB_PREDRAW
-#define GRAPE_TAB_PREDRAW 0      // one attempt of pure-draw lanes in the shadow of the warp's loads
-#endif
+
 
 
 struct TabParams {
@@ -402,15 +400,6 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
             }
         };
         const uint32_t st0 = st;   // the state this iteration's load served (the dispatch below)
-#if GRAPE_TAB_PREDRAW
-        // lanes that only draw this iteration make one attempt here, while the loads the
-        // other lanes of the warp just issued are in flight (they draw again below)
-        if constexpr (!SUSS) {
-            if (__any_sync(0xffffffffu, st0 == ST_DRAW)) {
-                if (st0 == ST_DRAW) draw_once(true, false);
-            }
-        }
-#endif
         if (st0 == ST_REC) {
             have_rec = true;
             bool found = true;
