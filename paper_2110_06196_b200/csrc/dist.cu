@@ -168,11 +168,15 @@ grape_status grape_graph_dist_create(uint32_t num_nodes, uint64_t num_arcs, cons
         const uint64_t len = hi - lo;
         g->part_len[t] = len;
         if (len == 0) continue;
+        // whole 2 MB pages: a CUDA IPC mapping of an allocation with a ragged last page was
+        // measured 150x slower for random reads from the importing process (the last rank's
+        // part, whose length is the table's remainder; tools/dist_probe.py)
+        const uint64_t alloc = (len + (2ull << 20) - 1) & ~((2ull << 20) - 1);
         void* p = nullptr;
-        cudaError_t e = cudaMalloc(&p, len);
+        cudaError_t e = cudaMalloc(&p, alloc);
         if (e != cudaSuccess) return fail(cuda_fail(e, "cudaMalloc of this rank's table part"));
         *part_slot(g, t, part) = p;
-        e = cudaMemset(p, t == 2 ? 0xFF : 0, len);   // empty hash slots = 0xFFFFFFFF
+        e = cudaMemset(p, t == 2 ? 0xFF : 0, alloc);   // empty hash slots = 0xFFFFFFFF
         if (e != cudaSuccess) return fail(cuda_fail(e, "memset of a table part"));
     }
     cudaError_t e = cudaDeviceSynchronize();

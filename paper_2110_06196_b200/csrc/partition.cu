@@ -30,9 +30,9 @@ cudaError_t split(const grape_graph* g, const void* src, uint64_t bytes, uint32_
         uint64_t lo, hi;
         owner_range(bytes, k, j, parts, &lo, &hi);
         if (hi == lo) continue;   // (fewer chunks than owners) never addressed
-        {
+        {   // whole 2 MB pages (see dist.cu: ragged last pages of shared allocations were slow)
             DeviceGuard on(devices[j]);
-            e = cudaMalloc(&out.mem[j], hi - lo);
+            e = cudaMalloc(&out.mem[j], ((hi - lo) + (2ull << 20) - 1) & ~((2ull << 20) - 1));
         }
         if (e == cudaSuccess) e = cudaMemcpyPeer(out.mem[j], devices[j], (const char*)src + lo, g->device, hi - lo);
     }

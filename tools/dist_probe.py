@@ -22,7 +22,8 @@ def worker(rank, world, port, dist_tables, q):
     from graphgen import config_graph, starts_per_node
     g = config_graph(2, device="cuda")
     if dist_tables:
-        dg = grape.graph_from_csr_dist(g.off, g.col, g.w, device=0, symmetric=True, table_budget_bytes=int(12e9))
+        dg = grape.graph_from_csr_dist(g.off, g.col, g.w, device=0, symmetric=True,
+                                       table_budget_bytes=int(24e9 / world))
     else:
         dg = grape.graph_from_csr(g.off, g.col, g.w, device=0, symmetric=True)
     g = g.to("cpu")
@@ -59,14 +60,16 @@ def worker(rank, world, port, dist_tables, q):
 
 
 if __name__ == "__main__":
-    for dist_tables in (False, True):
+    world = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+    modes = (True,) if len(sys.argv) > 2 else (False, True)
+    for dist_tables in modes:
         ctx = mp.get_context("spawn")
         q = ctx.Queue()
         s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
-        ps = [ctx.Process(target=worker, args=(r, 2, port, dist_tables, q)) for r in range(2)]
+        ps = [ctx.Process(target=worker, args=(r, world, port, dist_tables, q)) for r in range(world)]
         for p in ps:
             p.start()
-        out = sorted(q.get(timeout=900) for _ in range(2))
+        out = sorted(q.get(timeout=900) for _ in range(world))
         for p in ps:
             p.join()
         print("dist_tables" if dist_tables else "replicated", out, flush=True)
