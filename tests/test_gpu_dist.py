@@ -80,6 +80,27 @@ def _worker(rank, world, port, case, q):
             exp = grape.walks_first_order(ref, st, L, seed=42, walk_id_base=lo)
         torch.cuda.synchronize()
         same = bool(torch.equal(mine, exp))
+        # each rank alone (the other waits at a barrier): the distributed tables must not be
+        # pathologically slower than the contiguous ones (a ragged IPC allocation once made
+        # them 150x slower for every rank but the last)
+        def timed(graph):
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            ev[0].record()
+            for _ in range(3):
+                if mode == "node2vec":
+                    grape.walks_node2vec(graph, st, L, p, qq, seed=42, walk_id_base=lo, out=mine)
+                else:
+                    grape.walks_first_order(graph, st, L, seed=42, walk_id_base=lo, out=mine)
+            ev[1].record()
+            torch.cuda.synchronize()
+            return ev[0].elapsed_time(ev[1]) / 3
+        t_ref = t_dist = 0.0
+        for r_ in range(world):
+            dist.barrier()
+            if r_ == rank:
+                timed(dg)
+                t_ref, t_dist = timed(ref), timed(dg)
+            dist.barrier()
         rows = mine.cpu().numpy().view(np.uint32)
         # a sample against the oracle
         from oracle.oracle import Oracle
@@ -90,7 +111,8 @@ def _worker(rank, world, port, case, q):
             e, _ = o.walks(np.array([lo + i], dtype=np.uint32), L, mode=mode, p=p, q=qq, seed=42, base=int(lo + i))
             if not np.array_equal(rows[i], e[0]):
                 bad.append(int(lo + i))
-        q.put((rank, refused, same, bad, info["parts"], info["table_bytes"], total, budget, int(steps.item())))
+        q.put((rank, refused, same, bad, info["parts"], info["table_bytes"], total, budget, int(steps.item()),
+               t_ref, t_dist))
         dg.free()
         ref.free()
     finally:
@@ -110,7 +132,8 @@ def test_two_process_distributed_tables(case):
     for pr in procs:
         pr.join(timeout=120)
         assert pr.exitcode == 0
-    for rank, refused, same, bad, parts, part_bytes, total, budget, steps in res:
+    for rank, refused, same, bad, parts, part_bytes, total, budget, steps, t_ref, t_dist in res:
+        assert t_dist < 3 * t_ref + 2.0, f"rank {rank}: {t_dist:.2f} ms over distributed tables vs {t_ref:.2f} ms"
         assert parts == 2
         assert same, f"rank {rank}: walks over the distributed tables differ from the contiguous tables"
         assert not bad, f"rank {rank}: walks differ from the oracle at wids {bad[:5]}"
