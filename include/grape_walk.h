@@ -113,6 +113,7 @@ typedef struct {
     uint32_t hash_h;          /* tables: arcs per edge-hash bucket (4 or 6) */
     uint32_t notri;           /* tables: records carry the no-common-neighbour flags */
     uint32_t parts;           /* 1, or the number of parts after grape_graph_partition */
+    uint32_t wide;            /* 1: 34-bit arc offsets (m >= 2^32 - 64; the default walk rules only) */
 } grape_graph_info;
 
 /*

@@ -51,6 +51,7 @@ class GraphInfo(ctypes.Structure):
         ("hash_h", ctypes.c_uint32),
         ("notri", ctypes.c_uint32),
         ("parts", ctypes.c_uint32),
+        ("wide", ctypes.c_uint32),
     ]
 
 

@@ -272,6 +272,10 @@ grape_status walks_common(const grape_graph* g, const uint32_t* starts, uint64_t
         set_error("a distributed graph walks after grape_graph_dist_finish");
         return GRAPE_EINVAL;
     }
+    if (g->wide && (dT != 0 || sampler != 0)) {
+        set_error("a graph with 2^32 - 64 or more arcs serves the default walk rules only");
+        return GRAPE_EINVAL;
+    }
     int cur = -1;
     if (cudaGetDevice(&cur) != cudaSuccess) { cudaGetLastError(); cur = -1; }
     if (cur != g->device) {
@@ -421,6 +425,7 @@ grape_status grape_graph_get_info(const grape_graph* g, grape_graph_info* info)
     info->hash_h = g->hash_h;
     info->notri = g->notri ? 1u : 0u;
     info->parts = g->parts;
+    info->wide = g->wide ? 1u : 0u;
     return GRAPE_OK;
 }
 
@@ -626,6 +631,10 @@ grape_status grape_walks_stats_ex(const grape_graph* g, const uint32_t* starts, 
     }
     if (g->dist && !g->tables) {
         set_error("a distributed graph walks after grape_graph_dist_finish");
+        return GRAPE_EINVAL;
+    }
+    if (g->wide && (dT != 0 || sampler != 0)) {
+        set_error("a graph with 2^32 - 64 or more arcs serves the default walk rules only");
         return GRAPE_EINVAL;
     }
     if (sampler != 0 && (sampler != 2 || !g->tables || dT != 0 || !node2vec ||

@@ -157,6 +157,7 @@ grape_status grape_graph_dist_create(uint32_t num_nodes, uint64_t num_arcs, cons
                       (unsigned long long)o.table_budget_bytes);
         return fail(GRAPE_ENOMEM);
     }
+    g->wide = num_arcs >= (1ull << 32) - 64;
     g->dist = true;
     g->dist_part = part;
     g->parts = parts;

@@ -30,12 +30,14 @@
 //          bucketised linear probing from bucket floor(fmix32(x) nb / 2^32);
 //          empty = 0xFFFFFFFF (never a node id).  Load factor <= 1/2, so a
 //          lookup reads one sector unless its home bucket is full.
-// Index ranges: m < 2^32 - 64 (u32 arc offsets in node records and records), m/4 + n < 2^32
-// (u32 edge-hash bucket indices), max degree < 2^28 (flag bits, guide bits 30-31,
-// G deg < 2^32), row sums < 2^32 (u32 prefix).  When the tables are
+// Index ranges: m < 2^34 - 64 (row starts of 32 bits, or 34 bits in "wide" graphs: the high
+// bits in bits 26-27 of a record's degree word), m/4 + n < 2^32 (u32 edge-hash bucket
+// indices), max degree < 2^28 (2^26 when wide; flag bits, guide bits 30-31, G deg < 2^32),
+// row sums < 2^32 (u32 prefix).  When the tables are
 // built, col / cw / fences are released (graph.cu): nothing reads them after.  Outside them the tables are not built and
 // the v3 walker (fenced searches) runs.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include "internal.h"
 #include "build_common.cuh"
@@ -88,11 +90,13 @@ __device__ inline uint64_t upper_bound_u32(const uint32_t* __restrict__ cw, uint
 // are read from that canonical arc for both directions.  need_rev: every arc must
 // have its reverse (GRAPE_SYMMETRIC, checked here instead of a separate pass;
 // bit 1 of *asym when one has none).
+// Full records keep the head's row start xa (+ the arc-offset test bias): bits 0-31 in
+// their own word, bits 32-33 in bits 26-27 of the degree word (tables past 2^32 arcs).
 template <bool WEIGHTED, bool COMPACT>
 __global__ void build_records(const uint64_t* __restrict__ off, const uint32_t* __restrict__ col,
                               const uint32_t* __restrict__ cw, uint32_t n, uint64_t e_lo, uint64_t e_hi,
                               const TabRef rec, unsigned* __restrict__ asym, const TabRef notri, bool sym_half,
-                              bool need_rev)
+                              bool need_rev, uint64_t bias)
 {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const bool flags = notri.base[0] != nullptr;
@@ -112,7 +116,8 @@ __global__ void build_records(const uint64_t* __restrict__ off, const uint32_t* 
             fl = (*notri.at(e) ? 1u : 0u) | (found && *notri.at(j) ? 2u : 0u);
         }
         const uint32_t xf = COMPACT ? (x | (fl & 1) << 31 | (fl >> 1) << 30) : x;   // compact: bits 31 (self), 30 (rev)
-        const uint32_t df = COMPACT ? 0u : ((fl & 1) << 29 | (fl >> 1) << 28);   // full: bits 29, 28 of deg
+        const uint64_t xs = xa + bias;   // the head's row start as the walker sees it
+        const uint32_t df = COMPACT ? 0u : ((fl & 1) << 29 | (fl >> 1) << 28 | (uint32_t)((xs >> 32) & 3u) << 26);
         if (WEIGHTED) {
             const uint32_t own_hi = cw[e];
             const uint32_t own_lo = e > lo ? cw[e - 1] : 0u;
@@ -128,14 +133,14 @@ __global__ void build_records(const uint64_t* __restrict__ off, const uint32_t* 
                 const uint32_t xW = xb > xa ? cw[xb - 1] : 0u;
                 uint4* r = reinterpret_cast<uint4*>(rec.at(32 * e));   // one sector: never split by a part
                 r[0] = make_uint4(x, own_hi, rlo, rhi);
-                r[1] = make_uint4((uint32_t)xa, (uint32_t)(xb - xa) | df, xW, own_lo);
+                r[1] = make_uint4((uint32_t)xs, (uint32_t)(xb - xa) | df, xW, own_lo);
             }
         } else {
             const uint32_t rev = found ? (uint32_t)(j - xa) : kNone;
             if (COMPACT)
                 *reinterpret_cast<uint2*>(rec.at(8 * e)) = make_uint2(xf, rev);
             else
-                *reinterpret_cast<uint4*>(rec.at(16 * e)) = make_uint4(x, rev, (uint32_t)xa, (uint32_t)(xb - xa) | df);
+                *reinterpret_cast<uint4*>(rec.at(16 * e)) = make_uint4(x, rev, (uint32_t)xs, (uint32_t)(xb - xa) | df);
         }
     }
     if (WEIGHTED && bad) atomicOr(asym, 1u);
@@ -342,6 +347,12 @@ __global__ void build_notri(const uint64_t* __restrict__ off, const uint32_t* __
 
 uint64_t padded(uint64_t bytes) { return ((bytes + 31) / 32) * 32 + 32; }
 
+__global__ void bias_node_starts(NodeRec* __restrict__ nodes, uint32_t n, uint64_t bias)
+{
+    const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < n) nodes[v].start += bias;
+}
+
 TabRef flat(void* p, uint64_t bytes)
 {
     TabRef t{};
@@ -382,8 +393,11 @@ bool tables_in_range(const grape_graph* g)
     // arc offsets (node records, the records' copy of off[x]) are u32 in the walker; edge-hash
     // bucket indices floor(off / H) + v are u32; degrees leave 4 flag bits in their word;
     // the guide's per-row bucket index G deg is u32; row sums are u32 prefix values
-    return !(m >= (1ull << 32) - 64 || (m >> 2) + n + 2 >= (1ull << 32) || g->max_degree >= (1u << 28) ||
-             g->cw_bytes == 8);
+    // (34-bit offsets, "wide", past 2^32 - 64 arcs: bits 32-33 of a row start ride in bits 26-27
+    // of a record's degree word, so degrees stay below 2^26 there)
+    const bool wide = m >= (1ull << 32) - 64;
+    return !(m >= (1ull << 34) - 64 || (m >> 2) + n + 2 >= (1ull << 32) ||
+             g->max_degree >= (wide ? (1u << 26) : (1u << 28)) || g->cw_bytes == 8);
 }
 
 // Layout, in order of preference (fewest reads per step first): records with the
@@ -477,16 +491,16 @@ cudaError_t run_table_stage(const grape_graph* g, const TableJob& j, int stage, 
         const int grid = build::item_grid(j.e_hi - j.e_lo, sms);
         if (weighted && g->compact)
             build_records<true, true><<<grid, kThreads>>>(g->off, g->col, cw, g->n, j.e_lo, j.e_hi, j.rec, asym, j.notri, sym_half,
-                                                          need_rev);
+                                                          need_rev, g->arc_bias);
         else if (weighted)
             build_records<true, false><<<grid, kThreads>>>(g->off, g->col, cw, g->n, j.e_lo, j.e_hi, j.rec, asym, j.notri, sym_half,
-                                                          need_rev);
+                                                          need_rev, g->arc_bias);
         else if (g->compact)
             build_records<false, true><<<grid, kThreads>>>(g->off, g->col, nullptr, g->n, j.e_lo, j.e_hi, j.rec, asym,
-                                                           j.notri, sym_half, need_rev);
+                                                           j.notri, sym_half, need_rev, g->arc_bias);
         else
             build_records<false, false><<<grid, kThreads>>>(g->off, g->col, nullptr, g->n, j.e_lo, j.e_hi, j.rec, asym,
-                                                            j.notri, sym_half, need_rev);
+                                                            j.notri, sym_half, need_rev, g->arc_bias);
         break;
     }
     case 3:
@@ -527,6 +541,17 @@ grape_status build_tables(grape_graph* g, const grape_table_options& o)
     const int ch = choose_layout(g, o, budget);
     if (ch < 0) return GRAPE_ENOMEM;
     if (ch == 0) return GRAPE_OK;   // does not fit: v3 walker
+    g->wide = m >= (1ull << 32) - 64;
+    // Test hook: GRAPE_TEST_ARC_BIAS=b (rounded down to a multiple of 12, so divisible by
+    // both edge-hash H) offsets every row start the walker sees by b, so a small graph
+    // exercises the wide walker's 34-bit offset arithmetic end to end (tests/test_gpu_wide.py)
+    if (const char* env = getenv("GRAPE_TEST_ARC_BIAS")) {
+        const uint64_t b = strtoull(env, nullptr, 0) / 12 * 12;
+        if (b != 0 && b + m < (1ull << 34) - 64 && g->max_degree < (1u << 26)) {
+            g->arc_bias = b;
+            g->wide = true;
+        }
+    }
     if ((e = cudaMalloc(&g->rec, g->rec_alloc)) != cudaSuccess) return fail(e, "cudaMalloc arc records");
     if (weighted && (e = cudaMalloc((void**)&g->guide, g->guide_alloc)) != cudaSuccess)
         return fail(e, "cudaMalloc guide");
@@ -553,6 +578,8 @@ grape_status build_tables(grape_graph* g, const grape_table_options& o)
     for (int stage = 0; stage < 4 && e == cudaSuccess; ++stage) e = run_table_stage(g, j, stage, d_asym);
     if (e != cudaSuccess) return fail(e, "table kernels");
     g->notri = d_notri != nullptr;
+    if (g->arc_bias && n) bias_node_starts<<<(unsigned)((n + 255) / 256), 256>>>(g->nodes, n, g->arc_bias);
+    if ((e = cudaGetLastError()) != cudaSuccess) return fail(e, "node-record bias");
     unsigned asym = 0;
     if ((e = cudaMemcpy(&asym, d_asym, 4, cudaMemcpyDeviceToHost)) != cudaSuccess) return fail(e, "table build");
     if (asym & 2u) {   // GRAPE_SYMMETRIC asserted, checked by the record kernel

@@ -136,6 +136,13 @@ struct grape_graph {
     uint32_t hash_h;         // edge-hash buckets: floor(deg / H) + 1 per row (H = 4 or 6)
     bool compact;            // records without the head's node record (16 B weighted / 8 B)
     bool notri;              // records carry the no-common-neighbour flags (graph_tables.cu)
+    // 34-bit arc offsets (m >= 2^32 - 64; graph_tables.cu tables_in_range): the walker keeps
+    // row starts in 64 bits, records carry bits 32-33 of the head's row start in bits 26-27
+    // of the degree word (degrees < 2^26).  arc_bias: test hook (GRAPE_TEST_ARC_BIAS) —
+    // every row start in the node records and records is offset by it and the walker's
+    // table bases are moved back, so offsets past 2^32 run on a small graph
+    bool wide = false;
+    uint64_t arc_bias = 0;
     uint32_t* ehash;      // per-row bucketised sets of N(v): floor(deg/H)+1 buckets of 8 u32 slots from bucket floor(off[v]/H)+v
     uint64_t table_bytes;
     uint64_t rec_alloc = 0, guide_alloc = 0, hash_alloc = 0;   // table allocation bytes

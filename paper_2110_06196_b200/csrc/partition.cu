@@ -58,7 +58,7 @@ extern "C" grape_status grape_graph_partition(grape_graph* g, uint32_t parts, co
         set_error("grape_graph_partition: need a graph, 2 <= parts <= 8 and a device list");
         return GRAPE_EINVAL;
     }
-    if (!g->tables || g->parts != 1) {
+    if (!g->tables || g->parts != 1 || g->arc_bias != 0) {
         set_error("grape_graph_partition: the graph has no sampling tables, or is already partitioned");
         return GRAPE_EINVAL;
     }

@@ -152,9 +152,15 @@ enum : int { C_LOADS = 0, C_NODE, C_XNODE, C_CWPROBE, C_COLPROBE, C_REC, C_ATTEM
              C_GUIDE, C_HASH, C_ALU, C_ITER, C_ITER_DRAW, C_ITER_BACK };
 
 // WEIGHTED: 32-B records + guide; else 16-B records indexed by the draw.
-template <bool WEIGHTED, bool FAT, bool COMPACT, bool NODE2VEC, bool NEED_MEMBER, bool STATS, int MODE>
+// WIDE: arc offsets of 34 bits (graphs of 2^32 - 64 .. 2^34 arcs, or the arc-offset bias
+// test hook): row starts are u64 in registers, their bits 32-33 come from bits 26-27 of a
+// full record's degree word or from the node record's high word.
+template <bool WEIGHTED, bool FAT, bool COMPACT, bool NODE2VEC, bool NEED_MEMBER, bool STATS, int MODE,
+          bool WIDE = false>
 __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(const __grid_constant__ TabParams P)
 {
+    using off_t_ = typename std::conditional<WIDE, uint64_t, uint32_t>::type;   // a row start
+    constexpr uint32_t kDegMask = WIDE ? 0x03FFFFFFu : 0x0FFFFFFFu;                  // degree bits of a record
     constexpr bool SUSS = MODE == 1;   // approximated walks (grape_walks_approx)
     constexpr bool FOLD = MODE == 2;   // outlier-folded rejection (grape_walks_node2vec_folded)
     constexpr bool PARTS = MODE == 3;  // the default rule over partitioned tables (grape_graph_partition)
@@ -171,6 +177,11 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
     uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t st = i < P.num_walks ? ST_START : ST_DONE;
     auto divH = [&](uint32_t v) { return __umulhi(v, P.h_mul) >> P.h_shift; };   // floor(v / H)
+    auto divHo = [&](off_t_ t) -> uint32_t {   // floor(row start / H): an edge-hash bucket index
+        if constexpr (WIDE) return (uint32_t)(P.h_shift ? __umul64hi(t, 0xAAAAAAAAAAAAAAABull) >> 2 : t >> 2);
+        else return divH(t);
+    };
+
     uint32_t idx = 0;   // what the next load reads: NODE node id, GUIDE bucket (REC: ri, HASH: hb)
     uint32_t hb = 0;    // edge-hash bucket (absolute index)
     bool gsrc = false;  // fat guide: the proposal's record is the guide entry idx
@@ -181,8 +192,16 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
     unsigned long long steps = 0;
 
     uint32_t s = 0, a = 0;
-    uint32_t vid = 0, vstart = 0, vdeg = 0, vW = 0;        // current node v
-    uint32_t tid = kNone, tstart = 0, tdeg = 0, tW = 0;    // previous node t (kNone: first step)
+    uint32_t vid = 0, vdeg = 0, vW = 0;        // current node v
+    uint32_t tid = kNone, tdeg = 0, tW = 0;    // previous node t (kNone: first step)
+    off_t_ vstart = 0, tstart = 0;             // their row starts
+    auto swap_vt = [&]() {   // v and t trade places (a return)
+        const off_t_ z = vstart; vstart = tstart; tstart = z;
+        uint32_t q;
+        q = vdeg; vdeg = tdeg; tdeg = q;
+        q = vW; vW = tW; tW = q;
+        q = vid; vid = tid; tid = q;
+    };
     uint32_t tlo = 0, thi = 0;    // proposal interval of t in v's row (r units; empty if no arc v -> t)
     uint32_t slo = 0, shi = 0;    // proposal interval of v in t's row (for a return v -> t)
     uint32_t u = 0, r = 0;        // pending attempt: acceptance draw, bounded proposal draw
@@ -190,7 +209,8 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
     bool scan = false;            // weighted: compare r with the record's hi, advance if past it
     bool acc = false;             // the attempt is accepted; the record is read for x's data
     uint32_t x = 0;               // proposal
-    uint32_t hrev = 0, hxs = 0, hxd = 0;   // unweighted: x's record, kept across its membership test
+    uint32_t hrev = 0, hxd = 0;   // unweighted: x's record, kept across its membership test
+    off_t_ hxs = 0;
     // SUSS (approximated walks, §8(f) f1): at a node with deg > dT the step runs on dT
     // candidates, one uniform pick per bucket [floor(b deg/dT), floor((b+1) deg/dT))
     uint32_t cb = 0;              // weighted: candidates read so far this step (dT: sub-sample in scratch)
@@ -245,7 +265,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                     if (gd) GRAPE_DCHECK(idx < P.G * vdeg, "guide bucket within the row");
                     if (nd) GRAPE_DCHECK(idx < P.n, "node record of a node");
                     if (st == ST_HASH)
-                        GRAPE_DCHECK(hb >= divH(tstart) + tid && hb < divH(tstart) + tid + divH(tdeg) + 1,
+                        GRAPE_DCHECK(hb >= divHo(tstart) + tid && hb < divHo(tstart) + tid + divH(tdeg) + 1,
                                      "hash bucket within t's buckets");
                 }
             }
@@ -344,11 +364,8 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                     GRAPE_DCHECK(s < L && tid < P.n, "returned walk entry within the row");
                     w.put(s, tid);
                     ++steps;
+                    swap_vt();
                     uint32_t q;
-                    q = vstart; vstart = tstart; tstart = q;
-                    q = vdeg; vdeg = tdeg; tdeg = q;
-                    q = vW; vW = tW; tW = q;
-                    q = vid; vid = tid; tid = q;
                     q = tlo; tlo = slo; slo = q;
                     q = thi; thi = shi; shi = q;
                     const bool b_ = nt; nt = ntr; ntr = b_;
@@ -377,7 +394,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                 if (hash) {
                     if (STATS) ++cnt[C_MEMB];
                     st = ST_HASH;
-                    hb = divH(tstart) + tid + (uint32_t)(((uint64_t)fmix32(x) * (divH(tdeg) + 1)) >> 32);
+                    hb = divHo(tstart) + tid + (uint32_t)(((uint64_t)fmix32(x) * (divH(tdeg) + 1)) >> 32);
                 } else if (ok) {
                     acc = true;
                     st = ST_REC;
@@ -518,12 +535,13 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                     ++a;
                 }
             } else {   // full bucket without x: the next one, cyclically within t's buckets
-                const uint32_t base = divH(tstart) + tid;
+                const uint32_t base = divHo(tstart) + tid;
                 hb = hb + 1 == base + divH(tdeg) + 1 ? base : hb + 1;
             }
         } else if (st0 == ST_NODE) {   // node record: a start node, or (compact records) a taken arc's head
             const bool h = (j & 4) != 0;
             vstart = h ? sec[4] : sec[0];
+            if constexpr (WIDE) vstart |= (off_t_)(h ? sec[5] : sec[1]) << 32;   // NodeRec.start is u64
             vdeg = h ? sec[6] : sec[2];
             vW = h ? sec[7] : sec[3];
             a = 0;
@@ -561,7 +579,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
             if (hash) {
                 if (STATS) ++cnt[C_MEMB];
                 st = ST_HASH;   // home bucket of x among t's floor(deg t / H) + 1 buckets
-                hb = divH(tstart) + tid + (uint32_t)(((uint64_t)fmix32(x) * (divH(tdeg) + 1)) >> 32);
+                hb = divHo(tstart) + tid + (uint32_t)(((uint64_t)fmix32(x) * (divH(tdeg) + 1)) >> 32);
             } else if (!ok) {
                 draw = true;
                 ++a;
@@ -583,10 +601,12 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
             ++steps;
             bool need_node = false;
             if (emit) {   // the record of the taken arc: T, S, flags and (full records) x's node record
-                uint32_t fnlo, fnhi, fnslo, fnshi, fxs = 0, fxd = 0, fxw = 0, ffl;
+                uint32_t fnlo, fnhi, fnslo, fnshi, fxd = 0, fxw = 0, ffl;
+                off_t_ fxs = 0;
                 if constexpr (WEIGHTED && !COMPACT) {   // 32-B record at word 0 (also a fat guide entry)
                     fnlo = sec[2]; fnhi = sec[3]; fnslo = sec[7]; fnshi = sec[1];
-                    fxs = sec[4]; fxd = sec[5] & 0x0FFFFFFFu; fxw = sec[6];
+                    fxs = sec[4]; fxd = sec[5] & kDegMask; fxw = sec[6];
+                    if constexpr (WIDE) fxs |= (off_t_)((sec[5] >> 26) & 3u) << 32;
                     ffl = (sec[5] >> 28) & 3u;
                 } else if constexpr (WEIGHTED) {        // 16-B {x, hi, rlo, rhi} at word j
                     const bool h = (j & 4) != 0;
@@ -604,8 +624,9 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                     } else {
                         rev = hrev;
                         fxs = hxs;
+                        if constexpr (WIDE) fxs |= (off_t_)((hxd >> 26) & 3u) << 32;
                         ffl = (hxd >> 28) & 3u;
-                        fxd = hxd & 0x0FFFFFFFu;
+                        fxd = hxd & kDegMask;
                         fxw = fxd;
                     }
                     (void)kept;
@@ -620,21 +641,14 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                     if constexpr (COMPACT) need_node = true;   // x's node record: next iteration
                     else { vstart = fxs; vdeg = fxd; vW = fxw; }
                 } else {   // compact record of a return: t's node record is in registers
-                    uint32_t q;
-                    q = vstart; vstart = tstart; tstart = q;
-                    q = vdeg; vdeg = tdeg; tdeg = q;
-                    q = vW; vW = tW; tW = q;
-                    q = vid; vid = tid; tid = q;
+                    swap_vt();
                 }
                 tlo = fnlo; thi = fnhi; slo = fnslo; shi = fnshi;
                 nt = (ffl >> 1) != 0; ntr = (ffl & 1) != 0;
             } else {   // x = t: v and t swap, and so do T and S
                 const bool b_ = nt; nt = ntr; ntr = b_;
+                swap_vt();
                 uint32_t q;
-                q = vstart; vstart = tstart; tstart = q;
-                q = vdeg; vdeg = tdeg; tdeg = q;
-                q = vW; vW = tW; tW = q;
-                q = vid; vid = tid; tid = q;
                 q = tlo; tlo = slo; slo = q;
                 q = thi; thi = shi; shi = q;
             }
@@ -704,7 +718,8 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
     }
 }
 
-template <bool WEIGHTED, bool FAT, bool COMPACT, bool NODE2VEC, bool NEED_MEMBER, bool STATS, int MODE>
+template <bool WEIGHTED, bool FAT, bool COMPACT, bool NODE2VEC, bool NEED_MEMBER, bool STATS, int MODE,
+          bool WIDE = false>
 cudaError_t launch_k(const grape_graph* g, const WalkArgs& a, const Thresholds& T, cudaStream_t stream)
 {
     TabParams P{};
@@ -714,6 +729,12 @@ cudaError_t launch_k(const grape_graph* g, const WalkArgs& a, const Thresholds& 
     P.guide = g->guide;
     P.ehash = g->ehash;
     P.G = g->guide_factor;
+    if (g->arc_bias) {   // test hook (graph_tables.cu): row starts are biased; the bases move back
+        const uint64_t b = g->arc_bias;
+        P.rec = (const char*)g->rec - b * g->rec_bytes;
+        P.guide = (const uint32_t*)((const char*)g->guide - b * g->guide_factor * g->guide_bytes);
+        P.ehash = (const uint32_t*)((const char*)g->ehash - (b / g->hash_h) * 32);
+    }
     if (g->hash_h == 6) { P.h_mul = 0xAAAAAAABu; P.h_shift = 2; }   // floor(v/6) = umulhi(v, ceil(2^34/6)) >> 2
     else { P.h_mul = 0x40000000u; P.h_shift = 0; }                  // floor(v/4)
     P.wsym = g->wsym;
@@ -753,7 +774,8 @@ cudaError_t launch_k(const grape_graph* g, const WalkArgs& a, const Thresholds& 
 #endif
     // blocks per SM x SMs of the graph's device (cached per kernel and device)
     const int resident = resident_blocks(
-        (const void*)walk_tab_kernel<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, STATS, MODE>, kBlock, 0, g->device);
+        (const void*)walk_tab_kernel<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, STATS, MODE, WIDE>, kBlock, 0,
+        g->device);
     uint64_t blocks = (a.num_walks + kBlock - 1) / kBlock;
     if (blocks > (uint64_t)resident) blocks = resident;
     P.lanes = (uint32_t)(blocks * kBlock);
@@ -774,7 +796,8 @@ cudaError_t launch_k(const grape_graph* g, const WalkArgs& a, const Thresholds& 
     if (e == cudaSuccess && SUSS && WEIGHTED)   // per-lane candidate scratch, stream-ordered
         e = cudaMallocAsync((void**)&P.scratch, (uint64_t)2 * a.dT * P.lanes * 4, stream);
     if (e == cudaSuccess) {
-        walk_tab_kernel<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, STATS, MODE><<<(unsigned)blocks, kBlock, 0, stream>>>(P);
+        auto kern = walk_tab_kernel<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, STATS, MODE, WIDE>;
+        kern<<<(unsigned)blocks, kBlock, 0, stream>>>(P);
         e = cudaGetLastError();
     }
     if (SUSS && WEIGHTED && P.scratch) cudaFreeAsync(P.scratch, stream);
@@ -794,6 +817,14 @@ cudaError_t launch_s(const grape_graph* g, const WalkArgs& a, const Thresholds& 
     if (NODE2VEC && a.sampler == 2 && T.Tp > (T.T1 > T.Tq ? T.T1 : T.Tq)) {
         if (a.stats != nullptr) return launch_k<WEIGHTED, FAT, COMPACT, NODE2VEC, true, true, 2>(g, a, T, stream);
         return launch_k<WEIGHTED, FAT, COMPACT, NODE2VEC, true, false, 2>(g, a, T, stream);
+    }
+    if (g->wide) {   // 34-bit arc offsets: the default rule, contiguous or partitioned tables (capi.cu)
+        if (g->parts > 1) {
+            if (a.stats != nullptr) return launch_k<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, true, 3, true>(g, a, T, stream);
+            return launch_k<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, false, 3, true>(g, a, T, stream);
+        }
+        if (a.stats != nullptr) return launch_k<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, true, 0, true>(g, a, T, stream);
+        return launch_k<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, false, 0, true>(g, a, T, stream);
     }
     if (g->parts > 1) {   // partitioned tables: the default rule only (capi.cu rejects the other modes)
         if (a.stats != nullptr) return launch_k<WEIGHTED, FAT, COMPACT, NODE2VEC, NEED_MEMBER, true, 3>(g, a, T, stream);
