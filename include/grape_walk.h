@@ -135,7 +135,7 @@ typedef struct {
  * The handle stores off (u64[n+1]), the node records and, by default, the
  * sampling tables (built from col and the row-local inclusive
  * prefix sums of the weights, then those are released); graphs built with
- * GRAPE_NO_TABLES, or outside the tables' index ranges (m >= 2^32 - 64, a degree
+ * GRAPE_NO_TABLES, or outside the tables' index ranges (m >= 2^34 - 64, a degree
  * >= 2^28, a row sum >= 2^32), keep col (u32[m]), the prefix sums (u32[m] when
  * every row sum fits in 32 bits, else u64[m]) and their fence levels instead.
  * grape_graph_from_csr = grape_graph_from_csr_opts with automatic layout.

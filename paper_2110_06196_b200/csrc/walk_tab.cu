@@ -192,16 +192,20 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
     unsigned long long steps = 0;
 
     uint32_t s = 0, a = 0;
-    uint32_t vid = 0, vdeg = 0, vW = 0;        // current node v
-    uint32_t tid = kNone, tdeg = 0, tW = 0;    // previous node t (kNone: first step)
-    off_t_ vstart = 0, tstart = 0;             // their row starts
-    auto swap_vt = [&]() {   // v and t trade places (a return)
-        const off_t_ z = vstart; vstart = tstart; tstart = z;
-        uint32_t q;
-        q = vdeg; vdeg = tdeg; tdeg = q;
-        q = vW; vW = tW; tW = q;
-        q = vid; vid = tid; tid = q;
-    };
+    uint32_t vid = 0;                           // current node v
+    off_t_ vstart = 0;                          // (its row start)
+    uint32_t vdeg = 0, vW = 0;
+    uint32_t tid = kNone;                       // previous node t (kNone: first step)
+    off_t_ tstart = 0;
+    uint32_t tdeg = 0, tW = 0;
+#define GRAPE_SWAP_VT()                                        \
+    do {                                                       \
+        const off_t_ z_ = vstart; vstart = tstart; tstart = z_; \
+        uint32_t q_;                                           \
+        q_ = vdeg; vdeg = tdeg; tdeg = q_;                     \
+        q_ = vW; vW = tW; tW = q_;                             \
+        q_ = vid; vid = tid; tid = q_;                         \
+    } while (0)
     uint32_t tlo = 0, thi = 0;    // proposal interval of t in v's row (r units; empty if no arc v -> t)
     uint32_t slo = 0, shi = 0;    // proposal interval of v in t's row (for a return v -> t)
     uint32_t u = 0, r = 0;        // pending attempt: acceptance draw, bounded proposal draw
@@ -209,8 +213,9 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
     bool scan = false;            // weighted: compare r with the record's hi, advance if past it
     bool acc = false;             // the attempt is accepted; the record is read for x's data
     uint32_t x = 0;               // proposal
-    uint32_t hrev = 0, hxd = 0;   // unweighted: x's record, kept across its membership test
+    uint32_t hrev = 0;   // unweighted: x's record, kept across its membership test
     off_t_ hxs = 0;
+    uint32_t hxd = 0;
     // SUSS (approximated walks, §8(f) f1): at a node with deg > dT the step runs on dT
     // candidates, one uniform pick per bucket [floor(b deg/dT), floor((b+1) deg/dT))
     uint32_t cb = 0;              // weighted: candidates read so far this step (dT: sub-sample in scratch)
@@ -364,7 +369,7 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                     GRAPE_DCHECK(s < L && tid < P.n, "returned walk entry within the row");
                     w.put(s, tid);
                     ++steps;
-                    swap_vt();
+                    GRAPE_SWAP_VT();
                     uint32_t q;
                     q = tlo; tlo = slo; slo = q;
                     q = thi; thi = shi; shi = q;
@@ -641,13 +646,13 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
                     if constexpr (COMPACT) need_node = true;   // x's node record: next iteration
                     else { vstart = fxs; vdeg = fxd; vW = fxw; }
                 } else {   // compact record of a return: t's node record is in registers
-                    swap_vt();
+                    GRAPE_SWAP_VT();
                 }
                 tlo = fnlo; thi = fnhi; slo = fnslo; shi = fnshi;
                 nt = (ffl >> 1) != 0; ntr = (ffl & 1) != 0;
             } else {   // x = t: v and t swap, and so do T and S
                 const bool b_ = nt; nt = ntr; ntr = b_;
-                swap_vt();
+                GRAPE_SWAP_VT();
                 uint32_t q;
                 q = tlo; tlo = slo; slo = q;
                 q = thi; thi = shi; shi = q;
@@ -717,6 +722,8 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
         }
     }
 }
+
+#undef GRAPE_SWAP_VT
 
 template <bool WEIGHTED, bool FAT, bool COMPACT, bool NODE2VEC, bool NEED_MEMBER, bool STATS, int MODE,
           bool WIDE = false>
