@@ -24,6 +24,11 @@ CONFIGS = {
     6: dict(name="x6_chunglu_55M_2.2Garcs_n2v_p2_q0.5", graph=dict(kind="chung_lu", n=55_000_000, m=1_110_000_000,
                                                                   weights=1000),
             mode="node2vec", p=2.0, q=0.5, walks_per_node=1, L=100, seed=42),
+    # beyond BASELINE: past 2^32 arcs (the wide walker): unweighted Chung-Lu with
+    # 100M nodes and 2.4e9 edge draws -> ~4.7e9 arcs; bench.py --config 7 --max-walks 20000000
+    7: dict(name="x7_chunglu_100M_4.7Garcs_n2v_p2_q0.5", graph=dict(kind="chung_lu", n=100_000_000,
+                                                                   m=2_400_000_000, weights=None),
+            mode="node2vec", p=2.0, q=0.5, walks_per_node=1, L=100, seed=42),
 }
 
 
