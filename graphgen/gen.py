@@ -102,24 +102,62 @@ def _csr_from_sorted_keys(n: int, key: torch.Tensor) -> tuple[torch.Tensor, torc
     return off, col
 
 
-def _csr_symmetric(n: int, ckey: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+# torch's CUB-backed sort / unique refuse more than 2^31 - 1 elements: above this,
+# work by key-value ranges (bucket b holds the keys in [b K / B, (b+1) K / B)), each
+# bucket sorted on its own; the concatenation is the same sorted array.
+_BIG = (1 << 31) - (1 << 20)
+
+
+def _by_ranges(x: torch.Tensor, kmax: int, fn, buckets: int = 32) -> torch.Tensor:
+    out = []
+    for j in range(buckets):
+        lo, hi = kmax * j // buckets, kmax * (j + 1) // buckets
+        sel = x[(x >= lo) & (x < hi)]
+        if sel.numel():
+            out.append(fn(sel))
+        del sel
+    return torch.cat(out) if out else x[:0]
+
+
+def _sorted_unique(key: torch.Tensor, kmax: int) -> torch.Tensor:
+    if key.numel() <= _BIG:
+        return torch.unique(key, sorted=True)
+    return _by_ranges(key, kmax, lambda s: torch.unique(s, sorted=True))
+
+
+def _sorted(key: torch.Tensor, kmax: int) -> torch.Tensor:
+    if key.numel() <= _BIG:
+        return torch.sort(key).values
+    return _by_ranges(key, kmax, lambda s: torch.sort(s).values)
+
+
+def _bincount_rows(key: torch.Tensor, n: int, chunk: int = 1 << 28) -> torch.Tensor:
+    cnt = torch.zeros(n, dtype=torch.int64, device=key.device)
+    for lo in range(0, key.numel(), chunk):
+        cnt += torch.bincount(torch.div(key[lo:lo + chunk], n, rounding_mode="floor"), minlength=n)
+    return cnt
+
+
+def _csr_symmetric(n: int, ckey: torch.Tensor, chunk: int = 1 << 28) -> tuple[torch.Tensor, torch.Tensor]:
     """Symmetric CSR from sorted unique canonical keys a * n + b (a < b): every edge
     gives arcs a->b and b->a.  The reversed keys are sorted once and merged by rank
-    (searchsorted), so no sort ever holds all 2m arcs."""
-    a = torch.div(ckey, n, rounding_mode="floor")
-    b = ckey - a * n
-    rkey = torch.sort(b * n + a).values
-    del a, b
+    (searchsorted), so no sort ever holds all 2m arcs (and the merge runs in chunks)."""
     m1 = ckey.numel()
+    rkey = torch.empty_like(ckey)
+    for lo in range(0, m1, chunk):
+        ck = ckey[lo:lo + chunk]
+        a = torch.div(ck, n, rounding_mode="floor")
+        rkey[lo:lo + chunk] = (ck - a * n) * n + a
+        del a
+    rkey = _sorted(rkey, n * n)
     col = torch.empty(2 * m1, dtype=torch.int32, device=ckey.device)
-    idx = torch.arange(m1, device=ckey.device)
-    pos = idx + torch.searchsorted(rkey, ckey)
-    col[pos] = (ckey % n).to(torch.int32)
-    pos = idx + torch.searchsorted(ckey, rkey)
-    col[pos] = (rkey % n).to(torch.int32)
-    del pos, idx
-    cnt = torch.bincount(torch.div(ckey, n, rounding_mode="floor"), minlength=n)
-    cnt += torch.bincount(torch.div(rkey, n, rounding_mode="floor"), minlength=n)
+    for src, other in ((ckey, rkey), (rkey, ckey)):
+        for lo in range(0, m1, chunk):
+            s = src[lo:lo + chunk]
+            pos = torch.arange(lo, lo + s.numel(), device=ckey.device) + torch.searchsorted(other, s)
+            col[pos] = (s % n).to(torch.int32)
+            del pos
+    cnt = _bincount_rows(ckey, n, chunk) + _bincount_rows(rkey, n, chunk)
     off = torch.zeros(n + 1, dtype=torch.int64, device=ckey.device)
     off[1:] = torch.cumsum(cnt, 0)
     return off, col
@@ -191,8 +229,9 @@ def chung_lu(n: int, m_target: int, *, seed: int, weights: int | None = None,
         keep = a != b
         a, b = a[keep], b[keep]
         keys.append(torch.minimum(a, b) * n + torch.maximum(a, b))
-    key = torch.unique(torch.cat(keys), sorted=True)
+    key = torch.cat(keys)
     del keys
+    key = _sorted_unique(key, n * n)
     off, col = _csr_symmetric(n, key)
     del key
     w = None

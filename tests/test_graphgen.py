@@ -80,3 +80,13 @@ def test_starts_iteration_major():
 def test_tiny_graph_directed_has_sinks():
     g = tiny_graph(1, 30, 0.03, directed=True)
     assert np.any(np.diff(g.off.numpy()) == 0)
+
+
+def test_large_graph_paths_give_the_same_graph(monkeypatch):
+    """Past 2^31 keys the generator sorts / deduplicates by key ranges (torch's CUB
+    sort refuses more); forcing that path on a small graph gives the identical CSR."""
+    import graphgen.gen as G
+    ref = G.chung_lu(3000, 40000, seed=5, weights=7)
+    monkeypatch.setattr(G, "_BIG", 500)
+    big = G.chung_lu(3000, 40000, seed=5, weights=7)
+    assert torch.equal(ref.off, big.off) and torch.equal(ref.col, big.col) and torch.equal(ref.w, big.w)
