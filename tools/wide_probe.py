@@ -18,7 +18,8 @@ g = config_graph(7, device="cuda")
 print(f"generated n={g.n} m={g.m} ({g.m / 2**32:.3f} x 2^32) in {time.time() - t0:.0f} s", flush=True)
 torch.cuda.empty_cache()
 t0 = time.time()
-dg = grape.graph_from_csr(g.off, g.col, g.w, device=0, symmetric=True)
+# (past the automatic layout's 68 GB gather-reach cap: give the tables 100 GB)
+dg = grape.graph_from_csr(g.off, g.col, g.w, device=0, symmetric=True, layout={"table_budget_bytes": int(100e9)})
 torch.cuda.synchronize()
 print(f"built in {time.time() - t0:.1f} s: {dg.info}", flush=True)
 assert dg.info["tables"] == 1 and dg.info["wide"] == 1
