@@ -225,7 +225,8 @@ def test_specialisation_identities(grape):
 
 
 FULL = [(2, "node2vec"), (3, "node2vec"), (4, "node2vec"), (5, "node2vec"), (5, "first_order"),
-        (6, "node2vec")]   # 6: beyond BASELINE, 2.2e9 arcs (> 2^31: the lifted index range)
+        (6, "node2vec"),   # 6: beyond BASELINE, 2.2e9 arcs (> 2^31: the lifted index range)
+        (7, "node2vec")]   # 7: beyond BASELINE, 4.8e9 arcs (> 2^32: the wide walker), first 2e7 walks
 
 
 @pytest.mark.parametrize("k,mode", FULL, ids=[f"cfg{k}-{m}" for k, m in FULL])
@@ -240,10 +241,11 @@ def test_full_size_config_sampled(grape, k, mode):
     wk = config_walks(k)
     g = config_graph(k, device="cuda")
     torch.cuda.empty_cache()
-    if k == 6:   # past the automatic layout's 68 GB gather-reach cap: give the tables 100 GB
+    if k in (6, 7):   # past the automatic layout's 68 GB gather-reach cap: give the tables 100 GB
         dg = grape.graph_from_csr(g.off, g.col, g.w, device=0, symmetric=g.symmetric,
                                   layout={"table_budget_bytes": int(100e9)})
         assert g.m > 2 ** 31 and dg.info["tables"] == 1   # the table walker, past the old 2^31-arc range
+        assert dg.info["wide"] == int(k == 7) and (k == 6 or g.m > 2 ** 32)
     else:
         dg = _dev_graph(grape, g)
     deg = (g.off[1:] - g.off[:-1])
@@ -258,6 +260,8 @@ def test_full_size_config_sampled(grape, k, mode):
     del g
     torch.cuda.empty_cache()
     starts = starts_per_node(gc.n, wk["walks_per_node"], device="cuda")
+    if k == 7:   # the first 2e7 walks of the list (an 8 GB walk matrix next to 67 GB of tables)
+        starts = starts[:20_000_000].contiguous()
     steps = torch.zeros(1, dtype=torch.int64, device="cuda")
     if mode == "node2vec":
         out = grape.walks_node2vec(dg, starts, wk["L"], wk["p"], wk["q"], seed=wk["seed"], steps=steps)
@@ -276,6 +280,9 @@ def test_full_size_config_sampled(grape, k, mode):
     del pad
     assert realised == int(steps.item())
     rng = np.random.default_rng(k)
+    if W < gc.n * wk["walks_per_node"]:   # (k = 7) a prefix of the walk list: the hubs / sinks inside it
+        hubs, sinks = hubs[hubs < W], sinks[sinks < W]
+        n_sinks = min(n_sinks, len(sinks))
     # every walk whose start is a hub or a sink: wid = it * n + node for every iteration it
     special = np.concatenate([hubs, sinks]).astype(np.int64)
     its = np.arange(wk["walks_per_node"], dtype=np.int64) * gc.n
