@@ -12,7 +12,12 @@ LIB       := $(PKG)/libgrape_walk.so
 LIBCHK    := $(PKG)/libgrape_walk_checked.so
 OBJSCHK   := $(patsubst $(PKG)/csrc/%.cu,build_checked/%.o,$(SRCS))
 
-all: $(LIB) $(LIBCHK) oracle/liboracle.so
+all: $(LIB) $(LIBCHK) oracle/liboracle.so tools/libgrape_dram_probe.so
+
+# measurement aid for bench.py (DRAM bytes of one launch from the GPU counters; CUPTI), not the product
+tools/libgrape_dram_probe.so: tools/dram_probe.cpp
+	g++ -O2 -std=c++17 -shared -fPIC $< -I/usr/local/cuda/include -L/usr/local/cuda/lib64 \
+	    -Wl,-rpath,/usr/local/cuda/lib64 -lcupti -lnvperf_host -lcuda -o $@
 
 # bounds-checked build (GRAPE_CHECKED: every table access, row write and derived index
 # checked in the kernels; tests/test_gpu_checked.py) — same sources, same ABI
@@ -36,6 +41,6 @@ oracle/liboracle.so: oracle/grape_oracle.c
 	gcc -O2 -std=gnu99 -fPIC -shared -ffp-contract=off -fno-fast-math -Wall -o $@ $< -lm
 
 clean:
-	rm -rf build build_checked $(LIB) $(LIBCHK) oracle/liboracle.so
+	rm -rf build build_checked $(LIB) $(LIBCHK) oracle/liboracle.so tools/libgrape_dram_probe.so
 
 .PHONY: all clean checked

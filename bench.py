@@ -245,6 +245,32 @@ def _cpu_model() -> str:
     return platform.processor() or "unknown"
 
 
+def _dram_probe(launch, dev):
+    """DRAM bytes (read + write) of the kernels `launch` runs, from the GPU counters
+    (tools/libgrape_dram_probe.so, CUPTI range profiler; untimed).  None if unavailable."""
+    path = os.path.join(ROOT, "tools", "libgrape_dram_probe.so")
+    if not os.path.exists(path):
+        return None
+    try:
+        import ctypes
+        lib = ctypes.CDLL(path)
+        lib.grape_dram_probe_error.restype = ctypes.c_char_p
+        torch.cuda.synchronize(dev)
+        if lib.grape_dram_probe_begin() != 0:
+            print("dram probe:", lib.grape_dram_probe_error().decode(), file=sys.stderr)
+            return None
+        launch()
+        torch.cuda.synchronize(dev)
+        rd, wr, ns = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        if lib.grape_dram_probe_end(ctypes.byref(rd), ctypes.byref(wr), ctypes.byref(ns)) != 0:
+            print("dram probe:", lib.grape_dram_probe_error().decode(), file=sys.stderr)
+            return None
+        return rd.value + wr.value if rd.value + wr.value > 0 else None
+    except Exception as ex:   # measurement aid only: never fail the bench over it
+        print("dram probe:", ex, file=sys.stderr)
+        return None
+
+
 def _needs_flush(g, W, L):
     """Workloads whose CSR and output fit twice in L2 get an L2 flush between timed steps
     (decided from the CSR, so both arms state the same config)."""
@@ -501,6 +527,13 @@ def run_ours(args):
         t_launch = avg_launch_ms / 1e3
         peak, peak_src = _peaks()
         traffic = args.traffic_per_launch
+        traffic_src = "--traffic-per-launch" if traffic is not None else None
+        if traffic is None and not args.no_probe:
+            # DRAM bytes of one more (untimed) launch of the same call, read from the GPU's
+            # counters in this run (tools/dram_probe.cpp, CUPTI range profiler)
+            traffic = _dram_probe(lambda: one(None), dev)
+            if traffic is not None:
+                traffic_src = "measured in this run: CUPTI range profiler over one untimed launch (tools/dram_probe.cpp)"
         tfile = os.path.join(ROOT, "profiles", f"traffic_cfg{k}.json")
         kname = "walk_tab_kernel" if info.get("tables") else "walk_sm_kernel"
         if traffic is None and os.path.exists(tfile):
@@ -509,6 +542,7 @@ def run_ours(args):
             if (kname in tj.get("kernel", "") and tj.get("mode", wk["mode"]) == wk["mode"]
                     and tj.get("sampler", "rejection") == args.sampler and tj.get("dT", 0) == dT):
                 traffic = tj["dram_bytes_per_launch"]
+                traffic_src = f"profiles/traffic_cfg{k}.json (an earlier ncu capture of the same kernel)"
         # random-sector ceiling at this graph's randomly read footprint (measured,
         # profiles/gather_footprint.json; linear interpolation in footprint)
         ceil, ceil_src = None, None
@@ -528,7 +562,7 @@ def run_ours(args):
             ceil_src = f"profiles/gather_footprint.json at {fp:.1f} GB"
         achieved = alg_bytes / t_launch / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic,
+                "traffic": traffic, "traffic_source": traffic_src,
                 "kernel": ("walk_tab_kernel" if info.get("tables") else "walk_sm_kernel") +
                           (" (grape_walks_node2vec)" if node2vec else " (grape_walks_first_order)"),
                 "peak_source": peak_src, "avg_launch_ms": avg_launch_ms,
@@ -780,6 +814,8 @@ def main():
     ap.add_argument("--layout", default="", help="force table layout fields, e.g. "
                     "record_bytes=16,guide_bytes=8,guide_factor=1,hash_h=6 (grape_table_options)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle baseline (profiling runs)")
+    ap.add_argument("--no-probe", action="store_true",
+                    help="do not read the walk kernel's DRAM bytes from the GPU counters (CUPTI)")
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="N > 1: strong = the config's fixed walk list sharded by start node (north_star); "
                          "weak = the whole per-GPU workload on every rank")
