@@ -6,11 +6,11 @@
 //
 //   grape_dram_probe_begin()  -> 0 on success (profiling the current CUDA context)
 //   ... launch the kernel(s) ...
-//   grape_dram_probe_end(&read, &write, &ns) -> 0 on success; per-kernel ranges (auto
-//       range, kernel replay) summed: dram__bytes_read.sum, dram__bytes_write.sum,
-//       gpu__time_duration.sum
+//   grape_dram_probe_end(&read, &write, &ns) -> 0 on success: dram__bytes_read.sum and
+//       dram__bytes_write.sum of one user range around the launches (single pass; ns: 0)
 //   grape_dram_probe_error() -> the last failure as text
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -29,8 +29,8 @@ CUpti_Profiler_Host_Object* g_host = nullptr;
 std::vector<uint8_t> g_config, g_counter;
 CUcontext g_ctx = nullptr;
 bool g_inited = false;
-const char* kMetrics[] = {"dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"};
-constexpr size_t kNumMetrics = 3;
+const char* kMetrics[] = {"dram__bytes_read.sum", "dram__bytes_write.sum"};
+constexpr size_t kNumMetrics = 2;
 constexpr size_t kMaxRanges = 64;
 
 bool fail(const char* what, CUptiResult r)
@@ -70,6 +70,21 @@ void cleanup()
 extern "C" {
 
 const char* grape_dram_probe_error(void) { return g_err.c_str(); }
+
+// Initialise CUPTI's profiler early (before the process launches kernels); begin() does it
+// otherwise.
+int grape_dram_probe_init(void)
+{
+    if (g_inited) return 0;
+    CUpti_Profiler_Initialize_Params p{CUpti_Profiler_Initialize_Params_STRUCT_SIZE};
+    CUptiResult r = cuptiProfilerInitialize(&p);
+    if (r != CUPTI_SUCCESS) {
+        fail("cuptiProfilerInitialize", r);
+        return 1;
+    }
+    g_inited = true;
+    return 0;
+}
 
 static int begin_impl(void);
 
@@ -152,8 +167,8 @@ static int begin_impl(void)
     sc.configSize = g_config.size();
     sc.pCounterDataImage = g_counter.data();
     sc.counterDataImageSize = g_counter.size();
-    sc.range = CUPTI_AutoRange;
-    sc.replayMode = CUPTI_KernelReplay;
+    sc.range = CUPTI_UserRange;        // one range around everything launched until end()
+    sc.replayMode = CUPTI_UserReplay;  // (the two DRAM counters need a single pass)
     sc.maxRangesPerPass = kMaxRanges;
     sc.numNestingLevels = 1;
     sc.minNestingLevel = 1;
@@ -163,6 +178,10 @@ static int begin_impl(void)
     CUpti_RangeProfiler_Start_Params st{CUpti_RangeProfiler_Start_Params_STRUCT_SIZE};
     st.pRangeProfilerObject = g_obj;
     TRY(cuptiRangeProfilerStart(&st), "cuptiRangeProfilerStart");
+    CUpti_RangeProfiler_PushRange_Params pr{CUpti_RangeProfiler_PushRange_Params_STRUCT_SIZE};
+    pr.pRangeProfilerObject = g_obj;
+    pr.pRangeName = "probe";
+    TRY(cuptiRangeProfilerPushRange(&pr), "cuptiRangeProfilerPushRange");
     return 0;
 }
 
@@ -174,19 +193,29 @@ int grape_dram_probe_end(double* read_bytes, double* write_bytes, double* ns)
     }
     int rc = 0;
     auto run = [&]() -> int {
+        CUpti_RangeProfiler_PopRange_Params pp{CUpti_RangeProfiler_PopRange_Params_STRUCT_SIZE};
+        pp.pRangeProfilerObject = g_obj;
+        TRY(cuptiRangeProfilerPopRange(&pp), "cuptiRangeProfilerPopRange");
         CUpti_RangeProfiler_Stop_Params sp{CUpti_RangeProfiler_Stop_Params_STRUCT_SIZE};
         sp.pRangeProfilerObject = g_obj;
         TRY(cuptiRangeProfilerStop(&sp), "cuptiRangeProfilerStop");
+        if (!sp.isAllPassSubmitted) {
+            g_err = "the DRAM counters needed more than one pass";
+            return 1;
+        }
         CUpti_RangeProfiler_DecodeData_Params dd{CUpti_RangeProfiler_DecodeData_Params_STRUCT_SIZE};
         dd.pRangeProfilerObject = g_obj;
         TRY(cuptiRangeProfilerDecodeData(&dd), "cuptiRangeProfilerDecodeData");
+        if (getenv("GRAPE_DRAM_PROBE_DEBUG"))
+            fprintf(stderr, "dram probe: all passes submitted %d, ranges dropped %zu\n", (int)sp.isAllPassSubmitted,
+                    dd.numOfRangeDropped);
         CUpti_RangeProfiler_GetCounterDataInfo_Params gi{CUpti_RangeProfiler_GetCounterDataInfo_Params_STRUCT_SIZE};
         gi.pCounterDataImage = g_counter.data();
         gi.counterDataImageSize = g_counter.size();
         TRY(cuptiRangeProfilerGetCounterDataInfo(&gi), "cuptiRangeProfilerGetCounterDataInfo");
-        double sum[kNumMetrics] = {0, 0, 0};
+        double sum[kNumMetrics] = {0, 0};
         for (size_t r = 0; r < gi.numTotalRanges; ++r) {
-            double v[kNumMetrics] = {0, 0, 0};
+            double v[kNumMetrics] = {0, 0};
             CUpti_Profiler_Host_EvaluateToGpuValues_Params ev{CUpti_Profiler_Host_EvaluateToGpuValues_Params_STRUCT_SIZE};
             ev.pHostObject = g_host;
             ev.pCounterDataImage = g_counter.data();
@@ -200,7 +229,7 @@ int grape_dram_probe_end(double* read_bytes, double* write_bytes, double* ns)
         }
         *read_bytes = sum[0];
         *write_bytes = sum[1];
-        *ns = sum[2];
+        *ns = 0;   // (durations are CUDA-event measurements in bench.py)
         if (gi.numTotalRanges == 0) {
             g_err = "no kernel ranges were recorded";
             return 1;
