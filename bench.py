@@ -599,9 +599,13 @@ def run_ours(args):
         t_launch = avg_launch_ms / 1e3
         peak, peak_src = _peaks()
         tfile = os.path.join(ROOT, "profiles", f"traffic_cfg{k}_cdf.json")
-        traffic = json.load(open(tfile))["dram_bytes_per_launch"] if os.path.exists(tfile) else None
+        traffic = None if args.no_probe else _dram_probe(lambda: one(None), dev)
+        traffic_src = "measured in this run: CUPTI range profiler over one untimed launch (tools/dram_probe.cpp)"
+        if traffic is None and os.path.exists(tfile):
+            traffic = json.load(open(tfile))["dram_bytes_per_launch"]
+            traffic_src = f"profiles/traffic_cfg{k}_cdf.json (an earlier ncu capture of the same kernel)"
         roof = {"bound": "hbm", "achieved": alg_bytes / t_launch / 1e9, "peak": peak, "unit": "GB/s",
-                "frac": alg_bytes / t_launch / 1e9 / peak, "traffic": traffic,
+                "frac": alg_bytes / t_launch / 1e9 / peak, "traffic": traffic, "traffic_source": traffic_src,
                 "dram_gbs": (traffic / t_launch / 1e9) if traffic else None,
                 "dram_frac": (traffic / t_launch / 1e9 / peak) if traffic else None,
                 "kernel": "walk_cdf_kernel (grape_walks_node2vec_cdf)", "peak_source": peak_src,
