@@ -743,6 +743,7 @@ def run_skipgram(args):
     slots_all = _allreduce(float(valid * args.steps), dist.ReduceOp.SUM, world)
     peak, peak_src = _peaks()
     bytes_pair = S * (2 + K) * 4 + B * L * 4   # outputs written once + the walk matrix read once
+    pair_traffic = None if (args.no_probe or rank != 0) else _dram_probe(pairs, dev)   # one more, untimed
     cpu = None
     if rank == 0 and not args.no_cpu and world == 1:
         from oracle.oracle import Oracle
@@ -780,7 +781,9 @@ def run_skipgram(args):
                                 "negatives_per_s": valid * K * args.steps / t_pair},
                 "roofline": {"bound": "hbm", "kernel": "skipgram_kernel (grape_skipgram_pairs)",
                              "achieved": bytes_pair * args.steps / t_pair / 1e9, "peak": peak, "unit": "GB/s",
-                             "frac": bytes_pair * args.steps / t_pair / 1e9 / peak, "traffic": None,
+                             "frac": bytes_pair * args.steps / t_pair / 1e9 / peak, "traffic": pair_traffic,
+                             "traffic_source": ("measured in this run: CUPTI range profiler over one untimed "
+                                                "pair-kernel launch" if pair_traffic else None),
                              "peak_source": peak_src, "algorithmic_bytes_per_launch": bytes_pair},
                 "cpu_baseline": cpu, "e2e": None, "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
