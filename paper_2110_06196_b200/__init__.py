@@ -220,25 +220,36 @@ def graph_from_csr_dist(row_offsets, col_indices, weights=None, *, device: int, 
     g._h = h
     g.device = device
     g._group = group
+
+    def agreed(status: int, payload, what: str):
+        """All-gather (status, payload) — the stage barrier — and raise on every rank if any
+        rank failed, so no rank is left waiting in a collective the others never reach."""
+        got = [None] * world
+        dist.all_gather_object(got, (int(status), payload), group=group)
+        if any(s != GRAPE_OK for s, _ in got):
+            bad = next(r for r, (s, _) in enumerate(got) if s != GRAPE_OK)
+            detail = _lib.grape_last_error().decode(errors="replace") if status != GRAPE_OK else ""
+            _lib.grape_graph_free(h)
+            g._h = None
+            raise GrapeError(got[bad][0], f"{what} failed on rank {bad}" + (f": {detail}" if detail else ""))
+        return [p for _, p in got]
+
     ex = _capi.PartExport()
-    _capi.check(_lib, _lib.grape_graph_dist_export(h, ctypes.byref(ex)), "grape_graph_dist_export")
-    allx = [None] * world
-    dist.all_gather_object(allx, bytes(ex), group=group)
+    st = _lib.grape_graph_dist_export(h, ctypes.byref(ex))
+    allx = agreed(st, bytes(ex), "grape_graph_dist_export")
     arr = (_capi.PartExport * world)()
     for x in allx:
         e = _capi.PartExport.from_buffer_copy(x)
         arr[e.part] = e
-    _capi.check(_lib, _lib.grape_graph_dist_import(h, arr), "grape_graph_dist_import")
-    dist.barrier(group=group)   # every rank has opened every part
+    agreed(_lib.grape_graph_dist_import(h, arr), None, "grape_graph_dist_import")   # every rank opened every part
     fl = ctypes.c_uint32(0)
     flags_all = 0
     for stage in range(4):
-        _capi.check(_lib, _lib.grape_graph_dist_build(h, stage, ctypes.byref(fl)), "grape_graph_dist_build")
-        flv = [None] * world
-        dist.all_gather_object(flv, int(fl.value), group=group)   # (also the stage barrier)
-        for v in flv:
+        st = _lib.grape_graph_dist_build(h, stage, ctypes.byref(fl))
+        for v in agreed(st, int(fl.value), f"grape_graph_dist_build stage {stage}"):
             flags_all |= v
-    _capi.check(_lib, _lib.grape_graph_dist_finish(h, flags_all), "grape_graph_dist_finish")
+    st = _lib.grape_graph_dist_finish(h, flags_all)
+    agreed(st, None, "grape_graph_dist_finish")
     info = _capi.GraphInfo()
     _capi.check(_lib, _lib.grape_graph_get_info(h, ctypes.byref(info)), "grape_graph_get_info")
     g.info = {f: getattr(info, f) for f, _ in _capi.GraphInfo._fields_}
