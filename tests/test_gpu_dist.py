@@ -141,3 +141,38 @@ def test_two_process_distributed_tables(case):
         if case[0] != "tiny":
             assert refused, "the single-process build should not fit the per-rank budget"
             assert part_bytes < total
+
+
+def _mismatch_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        import paper_2110_06196_b200 as grape
+        from graphgen import tiny_graph
+        # rank 1 passes a different graph: the import sees other sizes on rank 1, and every
+        # rank raises together instead of leaving rank 0 waiting in a collective
+        g = tiny_graph(900 + rank, 400, 0.05, weighted=True)
+        try:
+            grape.graph_from_csr_dist(g.off, g.col, g.w, device=0, symmetric=True, table_budget_bytes=1 << 30)
+            q.put((rank, "built"))
+        except grape.GrapeError as ex:
+            q.put((rank, f"error {ex.status}"))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_distributed_build_fails_together_on_mismatched_ranks():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_mismatch_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = sorted([q.get(timeout=300) for _ in range(2)])
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert all(r[1].startswith("error") for r in res), res
