@@ -111,8 +111,25 @@ def _worker(rank, world, port, case, q):
             e, _ = o.walks(np.array([lo + i], dtype=np.uint32), L, mode=mode, p=p, q=qq, seed=42, base=int(lo + i))
             if not np.array_equal(rows[i], e[0]):
                 bad.append(int(lo + i))
+        # the other entry points over the distributed tables: host buffers, L = 1, no walks,
+        # the counting build and the streamed SkipGram consumer
+        extra_ok = True
+        if mode == "node2vec":
+            host = grape.walks_node2vec(dg, st.cpu(), L, p, qq, seed=42, walk_id_base=lo)
+            extra_ok &= bool(torch.equal(host, exp.cpu()))
+            one = grape.walks_node2vec(dg, st, 1, p, qq, seed=42, walk_id_base=lo)
+            extra_ok &= bool(torch.equal(one[:, 0], st))
+            empty = grape.walks_node2vec(dg, st[:0], L, p, qq, seed=42)
+            extra_ok &= empty.shape == (0, L)
+            cnt_out, stats = grape.walks_stats(dg, st, L, node2vec=True, p=p, q=qq, seed=42, walk_id_base=lo)
+            extra_ok &= bool(torch.equal(cnt_out, exp)) and stats["steps"] == int(steps.item())
+            c1, x1, n1 = grape.skipgram_pairs(ref, exp[:300].contiguous(), 2, 3, seed=5, walk_id_base=lo)
+            c2, x2, n2 = grape.walks_skipgram(dg, st[:300].contiguous(), L, 2, 3, node2vec=True, p=p, q=qq, seed=42,
+                                              pair_seed=5, walk_id_base=lo)
+            torch.cuda.synchronize()
+            extra_ok &= bool(torch.equal(c1, c2) and torch.equal(n1, n2))
         q.put((rank, refused, same, bad, info["parts"], info["table_bytes"], total, budget, int(steps.item()),
-               t_ref, t_dist))
+               t_ref, t_dist, extra_ok))
         dg.free()
         ref.free()
     finally:
@@ -132,7 +149,8 @@ def test_two_process_distributed_tables(case):
     for pr in procs:
         pr.join(timeout=120)
         assert pr.exitcode == 0
-    for rank, refused, same, bad, parts, part_bytes, total, budget, steps, t_ref, t_dist in res:
+    for rank, refused, same, bad, parts, part_bytes, total, budget, steps, t_ref, t_dist, extra_ok in res:
+        assert extra_ok, f"rank {rank}: host buffers / L = 1 / empty / counting build / streamed SkipGram differ"
         assert t_dist < 3 * t_ref + 2.0, f"rank {rank}: {t_dist:.2f} ms over distributed tables vs {t_ref:.2f} ms"
         assert parts == 2
         assert same, f"rank {rank}: walks over the distributed tables differ from the contiguous tables"
