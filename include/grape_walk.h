@@ -268,14 +268,16 @@ grape_status grape_walks_node2vec_folded(const grape_graph* g, const uint32_t* s
                                          cudaStream_t stream);
 
 /*
- * grape_graph_partition — the §8(f) f4 table layout (DESIGN.md §10): split every
- * sampling table of a built graph into `parts` power-of-two byte ranges, part j
- * placed on device devices[j] (peer access from the graph's device is enabled;
+ * grape_graph_partition — the §8(f) f4 table layout (DESIGN.md §10b): split every
+ * sampling table of a built graph into chunks of 2^k bytes (at most 64 per table),
+ * owner j of `parts` holding a contiguous range of chunks (owners differ by at most one
+ * chunk) on device devices[j] (peer access from the graph's device is enabled;
  * devices may repeat, e.g. all equal to the graph's device).  Walks then read each
  * table entry from its part (over NVLink for a peer's part) and stay bit-identical
  * to the unpartitioned graph.  Only the default rules run on a partitioned graph
- * (grape_walks_first_order / _node2vec / _stats, grape_skipgram_pairs); the
- * approximated, CDF and folded modes return EINVAL.  Synchronous.
+ * (grape_walks_first_order / _node2vec / _stats, grape_skipgram_pairs,
+ * grape_walks_skipgram); the approximated, CDF and folded modes return EINVAL.
+ * Synchronous.
  *   parts     2 .. 8;   devices  host int[parts]
  * Errors: EINVAL on a NULL graph / device list, parts out of range, a graph without
  * tables or already partitioned, a device that does not exist or that the graph's
@@ -287,10 +289,11 @@ grape_status grape_graph_partition(grape_graph* g, uint32_t parts, const int* de
 
 /*
  * Distributed table build — the §8(f) f4 row for graphs whose sampling tables
- * exceed one GPU (DESIGN.md §10; the paper's ClueWeb09 / sk-2005 scale, P:80,
+ * exceed one GPU (DESIGN.md §10b; the paper's ClueWeb09 / sk-2005 scale, P:80,
  * P:288).  One process per GPU ("rank" j of `parts`), each holding the whole CSR
  * (8 bytes per arc) and owning part j of every table (records, guide, edge hash:
- * power-of-two byte ranges, as grape_graph_partition lays them out).  The ranks
+ * owner j's contiguous range of 2^k-byte chunks, as grape_graph_partition lays them
+ * out; each owner's range allocated in whole 2 MB pages).  The ranks
  * exchange CUDA IPC handles of their parts and build in four stages; every rank
  * then walks over all parts (peer parts over NVLink, or the same GPU's memory
  * when ranks share a device), bit-identical to the single-GPU tables.  The ABI
