@@ -24,20 +24,6 @@ namespace grape {
 namespace {
 
 constexpr uint32_t kPadSg = 0xFFFFFFFFu;
-#ifndef GRAPE_SG_STREAM_STORES
-#define GRAPE_SG_STREAM_STORES 1
-#endif
-
-// The outputs are written once and never read here: streaming stores (evict-first) keep
-// them from pushing the node guide and off[] (read by every negative) out of L2.
-__device__ __forceinline__ void sg_store(uint32_t* p, uint32_t v)
-{
-#if GRAPE_SG_STREAM_STORES
-    __stcs(p, v);
-#else
-    *p = v;
-#endif
-}
 
 __device__ __forceinline__ uint32_t rank_search(const uint64_t* __restrict__ off, uint32_t n, uint64_t e)
 {
@@ -135,8 +121,8 @@ __global__ void __launch_bounds__(256) skipgram_kernel(const __grid_constant__ S
         for (uint32_t idx = threadIdx.x; idx < per_row; idx += blockDim.x) {
             uint32_t a = 0, b = 0;
             const bool ok = ends(idx, a, b);
-            sg_store(P.centers + o0 + idx, ok ? a : kPadSg);
-            sg_store(P.contexts + o0 + idx, ok ? b : kPadSg);
+            P.centers[o0 + idx] = ok ? a : kPadSg;
+            P.contexts[o0 + idx] = ok ? b : kPadSg;
         }
         // negatives 2kk and 2kk+1 of a slot come from one Philox block (words o1:o0 and
         // o3:o2): one thread per block, its two words stored side by side
@@ -164,8 +150,8 @@ __global__ void __launch_bounds__(256) skipgram_kernel(const __grid_constant__ S
                 if (k0 + 1 < K) v1 = rank((uint64_t)o.w << 32 | o.z);
             }
             uint32_t* dst = P.negs + (o0 + sl) * K + k0;
-            sg_store(dst, v0);
-            if (k0 + 1 < K) sg_store(dst + 1, v1);
+            dst[0] = v0;
+            if (k0 + 1 < K) dst[1] = v1;
         }
     }
 }
