@@ -13,7 +13,10 @@ namespace walk {
 
 constexpr uint32_t kPad = 0xFFFFFFFFu;
 constexpr uint32_t kNone = 0xFFFFFFFFu;
-constexpr int kBlock = 256;
+#ifndef GRAPE_BLOCK
+#define GRAPE_BLOCK 256
+#endif
+constexpr int kBlock = GRAPE_BLOCK;   // threads per block of the walk kernels
 #ifndef GRAPE_MIN_BLOCKS
 #define GRAPE_MIN_BLOCKS 4
 #endif
