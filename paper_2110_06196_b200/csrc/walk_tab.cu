@@ -50,6 +50,13 @@ enum : uint32_t { ST_START = 0, ST_NODE, ST_GUIDE, ST_REC, ST_HASH, ST_CAND, ST_
 #define GRAPE_TAB_DRAW_UNROLL 1
 #endif
 constexpr int kDrawUnroll = GRAPE_TAB_DRAW_UNROLL;
+#ifndef GRAPE_SUSS_UNROLL
+#define GRAPE_SUSS_UNROLL 1
+#endif
+constexpr int kSussUnroll = GRAPE_SUSS_UNROLL;
+#ifndef GRAPE_SUSS_MIN_BLOCKS
+#define GRAPE_SUSS_MIN_BLOCKS GRAPE_TAB_MIN_BLOCKS   // resident blocks per SM of the SUSS kernels
+#endif   // candidate pairs per unrolled step of the SUSS burst
 #ifndef GRAPE_TAB_SYNC_TOP
 #define GRAPE_TAB_SYNC_TOP 0     // explicit reconvergence points (measured: the emit one matters)
 #endif
@@ -66,7 +73,7 @@ constexpr int kDrawUnroll = GRAPE_TAB_DRAW_UNROLL;
 // full record's degree word or from the node record's high word.
 template <bool WEIGHTED, bool FAT, bool COMPACT, bool NODE2VEC, bool NEED_MEMBER, bool STATS, int MODE,
           bool WIDE = false>
-__global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(const __grid_constant__ TabParams P)
+__global__ void __launch_bounds__(kBlock, MODE == 1 ? GRAPE_SUSS_MIN_BLOCKS : GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(const __grid_constant__ TabParams P)
 {
     using off_t_ = typename std::conditional<WIDE, uint64_t, uint32_t>::type;   // a row start
     constexpr uint32_t kDegMask = WIDE ? 0x03FFFFFFu : 0x0FFFFFFFu;                  // degree bits of a record
@@ -608,12 +615,59 @@ __global__ void __launch_bounds__(kBlock, GRAPE_TAB_MIN_BLOCKS) walk_tab_kernel(
             if (!__any_sync(0xffffffffu, draw)) break;
             const bool sub = SUSS && vdeg > P.dT;   // this step runs on a SUSS sub-sample
             if (SUSS && WEIGHTED && draw && sub && cb < P.dT) {   // first: read the dT candidates
-                draw = false;
                 wc = 0;
                 bt = kNone;
-                cph = false;
-                ri = suss_index(0);
-                st = ST_CAND;
+                if constexpr (!COMPACT) {
+                    // full records carry both ends of a candidate's interval: all dT records are
+                    // read in this iteration, two candidates per Philox block (candidates 2k and
+                    // 2k+1 take its two halves, as suss_index does), the row-local bucket bounds
+                    // floor(b deg / dT) stepped incrementally (quotient and remainder)
+                    const uint32_t dq = vdeg / P.dT, dr = vdeg - dq * P.dT;
+                    uint32_t lq = 0, lr = 0;   // floor(b deg / dT), b deg mod dT
+                    auto next_bound = [&]() {
+                        lq += dq;
+                        lr += dr;
+                        if (lr >= P.dT) { lr -= P.dT; ++lq; }
+                    };
+#pragma unroll kSussUnroll
+                    for (uint32_t b = 0; b < P.dT; b += 2) {
+                        const uint4 o = philox_block_rk(P.rk, P.base + i, s, 0x80000000u | (b >> 1));
+                        const bool two = b + 1 < P.dT;
+                        const uint32_t l0 = lq;
+                        next_bound();
+                        const uint32_t l1 = lq;
+                        if (two) next_bound();
+                        const uint32_t l2 = lq;
+                        const uint32_t i0 = l0 + bounded32((uint64_t)o.y << 32 | o.x, l1 - l0);
+                        const uint32_t i1 = two ? l1 + bounded32((uint64_t)o.w << 32 | o.z, l2 - l1) : i0;
+                        GRAPE_DCHECK(i0 < vdeg && i1 < vdeg, "SUSS candidate within the row");
+                        const uint32_t* r0 = (const uint32_t*)P.rec + ((uint64_t)vstart + i0) * 8;
+                        const uint32_t* r1 = (const uint32_t*)P.rec + ((uint64_t)vstart + i1) * 8;
+                        const uint2 a0 = __ldg((const uint2*)r0), a1 = __ldg((const uint2*)r1);   // {x, hi}
+                        const uint32_t z0 = __ldg(r0 + 7), z1 = __ldg(r1 + 7);                 // lo
+                        if (STATS) {
+                            cnt[C_LOADS] += two ? 2 : 1;
+                            cnt[C_REC] += two ? 2 : 1;
+                        }
+                        wc += a0.y - z0;
+                        P.scratch[(uint64_t)(2 * b) * P.lanes + gl] = wc;
+                        P.scratch[(uint64_t)(2 * b + 1) * P.lanes + gl] = a0.x;
+                        if (a0.x == tid) bt = b;
+                        if (two) {
+                            wc += a1.y - z1;
+                            P.scratch[(uint64_t)(2 * b + 2) * P.lanes + gl] = wc;
+                            P.scratch[(uint64_t)(2 * b + 3) * P.lanes + gl] = a1.x;
+                            if (a1.x == tid) bt = b + 1;
+                        }
+                    }
+                    cb = P.dT;   // the sub-sample is in scratch: this round draws on it
+                } else {   // compact records: one candidate per iteration (ST_CAND; a weight may need
+                           // the predecessor's record)
+                    draw = false;
+                    cph = false;
+                    ri = suss_index(0);
+                    st = ST_CAND;
+                }
             }
             if (draw) draw_once(k + 1 < GRAPE_TAB_DRAWS, sub);
         }
