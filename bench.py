@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -668,6 +669,37 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def _sg_lookup_roofline(n, m, lookups, launch_s):
+    """The pair kernel's bound: one random node-guide read per negative (rank of a
+    uniform arc index) against the measured random-lookup rate at the
+    guide's size (profiles/r02_l2_lookup.json, tools/l2_lookup.cu; log-size interpolation).
+    The guide's size follows skipgram.cu ensure_node_guide: 16-B entries, 4 buckets
+    per node while n * 64 B <= 128 MiB, else 1."""
+    per_node = 4 if n * 64 <= (128 << 20) else 1
+    sh = 0
+    while (m >> sh) + 1 > per_node * n:
+        sh += 1
+    table = ((m >> sh) + 1) * 16
+    try:
+        ref = json.load(open(os.path.join(ROOT, "profiles", "r02_l2_lookup.json")))
+    except OSError:
+        return None
+    mb = table / 2**20
+    xs, ys = ref["table_mb"], ref["unroll1"]
+    if mb <= xs[0]:
+        ceil = ys[0]
+    elif mb >= xs[-1]:
+        ceil = ys[-1]
+    else:
+        j = next(i for i in range(1, len(xs)) if xs[i] >= mb)
+        f = (math.log(mb) - math.log(xs[j - 1])) / (math.log(xs[j]) - math.log(xs[j - 1]))
+        ceil = ys[j - 1] + f * (ys[j] - ys[j - 1])
+    ach = lookups / launch_s / 1e9
+    return {"lookups_per_launch": lookups, "achieved_G_per_s": ach, "ceiling_G_per_s": ceil, "frac": ach / ceil,
+            "node_guide_bytes": table,
+            "ceiling_source": "profiles/r02_l2_lookup.json (random 8-B lookups vs table size, this GPU model)"}
+
+
 def run_skipgram(args):
     """--skipgram: the SkipGram consumer.  One step =
     the config's walks for a batch of B walk ids (the walk kernel) + their window-w
@@ -784,7 +816,8 @@ def run_skipgram(args):
                              "frac": bytes_pair * args.steps / t_pair / 1e9 / peak, "traffic": pair_traffic,
                              "traffic_source": ("measured in this run: CUPTI range profiler over one untimed "
                                                 "pair-kernel launch" if pair_traffic else None),
-                             "peak_source": peak_src, "algorithmic_bytes_per_launch": bytes_pair},
+                             "peak_source": peak_src, "algorithmic_bytes_per_launch": bytes_pair,
+                             "random_access": _sg_lookup_roofline(g.n, g.m, valid * K, t_pair / args.steps)},
                 "cpu_baseline": cpu, "e2e": None, "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     dg.free()

@@ -173,10 +173,10 @@ struct grape_graph {
     std::mutex stage_mu;
     void* stage_buf = nullptr;
     uint64_t stage_bytes = 0;
-    // SkipGram negatives (skipgram.cu): node guide over arc-index buckets of
+    // SkipGram negatives (skipgram.cu): node guide (16-B entries) over arc-index buckets of
     // 2^node_guide_shift arcs, built on the first grape_skipgram_pairs call
     std::mutex node_guide_mu;
-    uint2* node_guide = nullptr;
+    uint4* node_guide = nullptr;
     uint32_t node_guide_shift = 0;
     uint32_t max_degree;
     uint64_t max_row_weight;

@@ -5,15 +5,15 @@
 // whose row holds a uniform arc index — the rank the paper implements on its
 // Elias-Fano arrays.
 //
-// Rank on the device: a node guide over arc-index buckets of 2^sh arcs (about
-// 2 or 8 per node, ensure_node_guide), entry b = {rank(b << sh), where that row ends relative to the
-// bucket}, built once per graph (lazily, on the first call).  A query reads its
-// bucket's entry and is done when e falls in that row — most arcs belong to rows
-// much longer than a bucket; otherwise it steps over the rows that end at or
-// before e in off[].
+// Rank on the device: a node guide over arc-index buckets of 2^sh arcs (about 4
+// or 1 per node, ensure_node_guide), 16-B entry b = {v0 = rank(b << sh), and where
+// rows v0, v0 + 1, v0 + 2 end relative to the bucket}, built once per graph
+// (lazily, on the first call).  A query reads its bucket's entry and is done unless
+// three rows end at or before it inside the bucket; then it steps over off[].
 //
-// One block per walk row (staged in shared memory); its threads write the row's
-// slots, then its negatives, in order: every store of a warp is contiguous.
+// One block per walk row (staged in shared memory with its slots' validity bits);
+// its threads write the row's slots, then its negatives, in order: every store of
+// a warp is contiguous.
 #include <cstdlib>
 #include <mutex>
 
@@ -36,16 +36,23 @@ __device__ __forceinline__ uint32_t rank_search(const uint64_t* __restrict__ off
     return lo;
 }
 
-// entry b = {v = rank(b << sh), min(off[v+1] - (b << sh), 2^32 - 1)}: a query whose
-// offset into the bucket is below the second word is answered by this one read
+// entry b = {v0 = rank(b << sh), E1, E2, E3}: E_k = off[v0 + k] - (b << sh), the end of
+// row v0 + k - 1 relative to the bucket (2^32 - 1 when past 2^32 - 1 or past row n - 1):
+// a query at offset o into the bucket is row v0 + [o >= E1] + [o >= E2] + [o >= E3]
+// unless o >= E3
 __global__ void build_node_guide(const uint64_t* __restrict__ off, uint32_t n, uint32_t sh, uint64_t nb,
-                                 uint2* __restrict__ gidx)
+                                 uint4* __restrict__ gidx)
 {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += stride) {
-        const uint32_t v = rank_search(off, n, b << sh);
-        const uint64_t rel = off[v + 1] - (b << sh);
-        gidx[b] = make_uint2(v, rel < 0xFFFFFFFFull ? (uint32_t)rel : 0xFFFFFFFFu);
+        const uint64_t b0 = b << sh;
+        const uint32_t v = rank_search(off, n, b0);
+        uint32_t E[3];
+        for (uint32_t k = 0; k < 3; ++k) {
+            const uint64_t rel = v + 1 + k <= n ? off[v + 1 + k] - b0 : ~0ull;
+            E[k] = rel < 0xFFFFFFFFull ? (uint32_t)rel : 0xFFFFFFFFu;
+        }
+        gidx[b] = make_uint4(v, E[0], E[1], E[2]);
     }
 }
 
@@ -75,7 +82,7 @@ struct FastDiv {
 struct SgParams {
     const uint64_t* off;
     uint32_t n;
-    const uint2* gidx;
+    const uint4* gidx;
     uint32_t sh;
     uint64_t m;
     const uint32_t* walks;
@@ -89,18 +96,21 @@ struct SgParams {
     uint32_t* negs;
 };
 
-constexpr uint32_t kRowSmemWords = 12288;   // walk rows up to 48 KB are staged in shared memory
+constexpr uint32_t kRowSmemWords = 12288;   // a row and its slots' validity bits up to 48 KB are staged
 
 // One block per walk row at a time (grid-stride over rows): the row is staged in
-// shared memory, then the block's threads cover the row's L*2w slots and its
-// L*2w*K negative words in order, so every store of a warp is contiguous and no
-// 64-bit division is needed (32-bit index arithmetic within a row).
-__global__ void __launch_bounds__(256) skipgram_kernel(const __grid_constant__ SgParams P)
+// shared memory, then the block's threads cover the row's L*2w slots (each slot's
+// validity also kept as one bit in shared memory) and its L*2w*K negative words in
+// order, so every store of a warp is contiguous and no 64-bit division is needed
+// (32-bit index arithmetic within a row).
+__global__ void __launch_bounds__(256, 8) skipgram_kernel(const __grid_constant__ SgParams P)
 {
     extern __shared__ uint32_t srow[];
     const uint32_t L = P.L, tw = 2 * P.w, K = P.K;
     const uint32_t per_row = L * tw;
-    const bool staged = L <= kRowSmemWords;
+    const uint32_t bit_words = (per_row + 31) / 32;
+    const bool staged = L + bit_words <= kRowSmemWords;
+    uint32_t* sbits = srow + L;   // staged: bit idx of word idx/32 = slot idx is valid
     for (uint64_t r = blockIdx.x; r < P.num_walks; r += gridDim.x) {
         const uint32_t* grow = P.walks + r * L;
         __syncthreads();   // the previous row's readers are done
@@ -118,24 +128,32 @@ __global__ void __launch_bounds__(256) skipgram_kernel(const __grid_constant__ S
         };
         const uint64_t o0 = r * per_row;                        // local slot offset of the row
         const uint64_t g0 = (P.base + r) * per_row;             // global slot id of its first slot
-        for (uint32_t idx = threadIdx.x; idx < per_row; idx += blockDim.x) {
+        // slots: whole warps step together over consecutive slots (the loop bound is
+        // rounded up to a warp), so each warp's ballot is one word of validity bits
+        const uint32_t per_row_w = (per_row + 31) & ~31u;
+        for (uint32_t idx = threadIdx.x; idx < per_row_w; idx += blockDim.x) {
             uint32_t a = 0, b = 0;
-            const bool ok = ends(idx, a, b);
-            P.centers[o0 + idx] = ok ? a : kPadSg;
-            P.contexts[o0 + idx] = ok ? b : kPadSg;
+            const bool in = idx < per_row;
+            const bool ok = in && ends(idx, a, b);
+            if (in) {
+                P.centers[o0 + idx] = ok ? a : kPadSg;
+                P.contexts[o0 + idx] = ok ? b : kPadSg;
+            }
+            const unsigned bits = __ballot_sync(0xffffffffu, ok);
+            if (staged && (threadIdx.x & 31) == 0) sbits[idx >> 5] = bits;
         }
+        if (staged) __syncthreads();   // the validity bits are complete
         // negatives 2kk and 2kk+1 of a slot come from one Philox block (words o1:o0 and
         // o3:o2): one thread per block, its two words stored side by side
         const uint32_t Kh = (K + 1) / 2;
         const uint32_t nk = per_row * Kh;
         auto rank = [&](uint64_t x64) {
             const uint64_t e = __umul64hi(x64, P.m);                 // BOUNDED(x64, m)
-            const uint2 ge = __ldg(P.gidx + (e >> P.sh));
-            uint32_t v = ge.x;
-            if (e - ((e >> P.sh) << P.sh) >= ge.y) {                 // past the bucket's first row
-                ++v;
-                while (__ldg(P.off + v + 1) <= e) ++v;               // rows ending at or before e
-            }
+            const uint4 ge = __ldg(P.gidx + (e >> P.sh));
+            const uint32_t o = (uint32_t)(e & ((1ull << P.sh) - 1));   // offset into the bucket
+            uint32_t v = ge.x + (o >= ge.y) + (o >= ge.z) + (o >= ge.w);
+            if (o >= ge.w)                                            // three rows end before e
+                while (__ldg(P.off + v + 1) <= e) ++v;
             GRAPE_DCHECK(e < P.m && v < P.n && __ldg(P.off + v) <= e && e < __ldg(P.off + v + 1),
                          "negative = the row holding arc e");
             return v;
@@ -144,7 +162,8 @@ __global__ void __launch_bounds__(256) skipgram_kernel(const __grid_constant__ S
             const uint32_t sl = P.k_div.div(idx), kk = idx - sl * Kh;
             const uint32_t k0 = 2 * kk;
             uint32_t a = 0, b = 0, v0 = kPadSg, v1 = kPadSg;
-            if (ends(sl, a, b) && P.m != 0) {
+            const bool ok = staged ? ((sbits[sl >> 5] >> (sl & 31)) & 1u) != 0 : ends(sl, a, b);
+            if (ok && P.m != 0) {
                 const uint4 o = philox_block_rk(P.rk, g0 + sl, 0xFFFFFFFFu, kk);
                 v0 = rank((uint64_t)o.y << 32 | o.x);
                 if (k0 + 1 < K) v1 = rank((uint64_t)o.w << 32 | o.z);
@@ -162,18 +181,17 @@ cudaError_t ensure_node_guide(grape_graph* g, cudaStream_t stream)
 {
     std::lock_guard<std::mutex> lk(g->node_guide_mu);
     if (g->node_guide != nullptr || g->m == 0) return cudaSuccess;
-    // buckets per node: 8 (64 B per node; a query past its bucket's first row steps
-    // over fewer rows) while that guide stays L2-sized (<= 128 MB), else 2 (16 B per
-    // node).  Measured on the pair kernel, 2e6 walks x 80, w = 5, K = 5: configs[1]
-    // (1M nodes) 52.5 -> 47.9 ms with 8; configs[4] (67M nodes, the guide in DRAM either
-    // way) 153 -> 164 ms with 8, so 2 there.  GRAPE_SG_GUIDE_PER_NODE overrides (A/B).
-    uint32_t per_node = (uint64_t)g->n * 64 <= (128ull << 20) ? 8 : 2;
+    // buckets per node: 4 (64 B per node) while that guide stays L2-sized (<= 128 MB),
+    // else 1 (16 B per node).  Each 16-B entry resolves a query up to three row ends
+    // into its bucket (the 8-B entries of round 1 resolved one, at 8 and 2 per node:
+    // configs[1] pair kernel 47.9 ms with those).  GRAPE_SG_GUIDE_PER_NODE overrides (A/B).
+    uint32_t per_node = (uint64_t)g->n * 64 <= (128ull << 20) ? 4 : 1;
     if (const char* s = getenv("GRAPE_SG_GUIDE_PER_NODE")) per_node = (uint32_t)atoi(s) > 0 ? (uint32_t)atoi(s) : per_node;
     uint32_t sh = 0;
     while ((g->m >> sh) + 1 > (uint64_t)per_node * g->n) ++sh;
     const uint64_t nb = (g->m >> sh) + 1;
-    uint2* gidx = nullptr;
-    cudaError_t e = cudaMalloc(&gidx, nb * sizeof(uint2));
+    uint4* gidx = nullptr;
+    cudaError_t e = cudaMalloc(&gidx, nb * sizeof(uint4));
     if (e != cudaSuccess) return e;
     const unsigned blocks = (unsigned)((nb + 255) / 256 < 4096 ? (nb + 255) / 256 : 4096);
     build_node_guide<<<blocks, 256, 0, stream>>>(g->off, g->n, sh, nb, gidx);
@@ -216,7 +234,8 @@ cudaError_t launch_skipgram(const grape_graph* g, const uint32_t* walks, uint64_
     uint64_t blocks = num_walks;
     const uint64_t cap = (uint64_t)sms * 8;   // 8 resident blocks of 256 per SM, grid-stride over rows
     if (blocks > cap) blocks = cap;
-    const size_t smem = L <= kRowSmemWords ? (size_t)L * 4 : 0;
+    const uint64_t words = (uint64_t)L + ((uint64_t)L * 2 * window + 31) / 32;   // row + validity bits
+    const size_t smem = words <= kRowSmemWords ? (size_t)words * 4 : 0;
     skipgram_kernel<<<(unsigned)blocks, 256, smem, stream>>>(P);
     return cudaGetLastError();
 }
