@@ -95,7 +95,7 @@ Mem classify(const void* ptr)
 #define GRAPE_HOST_CHUNK_MAX_MB 1024
 #endif
 #ifndef GRAPE_HOST_NBUF
-#define GRAPE_HOST_NBUF 2
+#define GRAPE_HOST_NBUF 4
 #endif
 
 // Host buffers: stage chunks through device memory.  Chunk k runs on the
