@@ -274,9 +274,11 @@ constexpr uint64_t kCoopLen = 32;
 // Scans of more than kNotriScanCap entries stop there with the flag clear ("may share a
 // neighbour": the walker then tests membership as usual).  The flag only enables a
 // shortcut, so clearing it never changes a walk; it bounds the build's cost on pairs
-// of high-degree nodes with no common neighbour (full scans of long rows).
+// of high-degree nodes with no common neighbour (full scans of long rows).  256
+// measured (round 2, tools/ab_build.sh): configs[2] build 710 -> 442 ms, configs[3]
+// 1608 -> 1386 ms, walks unchanged (configs[3] +0.4%); 64 costs walk time (+3%).
 #ifndef GRAPE_NOTRI_SCAN_CAP
-#define GRAPE_NOTRI_SCAN_CAP (1ull << 62)
+#define GRAPE_NOTRI_SCAN_CAP 256
 #endif
 constexpr uint64_t kNotriScanCap = GRAPE_NOTRI_SCAN_CAP;
 
