@@ -56,8 +56,15 @@ def test_product_line_n1():
     r = d["roofline"]
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] == pytest.approx(r["achieved"] / r["peak"])
     # DRAM traffic read from the GPU counters in this run (CUPTI, one untimed launch; configs[0]
-    # is L2-resident, so only that it was measured is asserted)
-    assert r["traffic_source"].startswith("measured in this run") and r["traffic"] > 0
+    # is L2-resident, so only that it was measured is asserted).  On a box whose profiler an
+    # earlier `ncu --set full` left unusable, CUPTI refuses the range (observed: Stop returns
+    # CUPTI_ERROR_UNKNOWN in every later process until the box is recycled); bench.py then says
+    # so on stderr and falls back to the committed capture, which it names
+    if r["traffic_source"].startswith("measured in this run"):
+        assert r["traffic"] > 0
+    else:
+        assert "dram probe: cupti" in p.stderr, p.stderr[-2000:]
+        assert r["traffic_source"].startswith("profiles/traffic_cfg1.json") and r["traffic"] > 0
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] == 4 * 10 ** 4 and e["d2h_bytes_per_step"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] > 0
