@@ -246,6 +246,33 @@ def _cpu_model() -> str:
     return platform.processor() or "unknown"
 
 
+def _gpu_local_cpus(local):
+    """The CPUs next to GPU `local` (its PCI device's local_cpulist in sysfs) that this
+    process may run on; None when unknown."""
+    try:
+        pr = torch.cuda.get_device_properties(local)
+        bus = f"{pr.pci_domain_id:04x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+        txt = open(f"/sys/bus/pci/devices/{bus}/local_cpulist").read().strip()
+        cpus = set()
+        for part in txt.split(","):
+            a, _, b = part.partition("-")
+            cpus.update(range(int(a), int(b or a) + 1))
+        cpus &= os.sched_getaffinity(0)
+        return cpus or None
+    except Exception:
+        return None
+
+
+def _cpu_ranges(cpus):
+    xs = sorted(cpus)
+    out, a = [], xs[0]
+    for p_, q_ in zip(xs, xs[1:] + [None]):
+        if q_ != p_ + 1:
+            out.append(f"{a}-{p_}" if p_ != a else f"{a}")
+            a = q_
+    return ",".join(out)
+
+
 def _dram_probe(launch, dev):
     """DRAM bytes (read + write) of the kernels `launch` runs, from the GPU counters
     (tools/libgrape_dram_probe.so, CUPTI range profiler; untimed).  None if unavailable."""
@@ -451,12 +478,25 @@ def run_ours(args):
     # ---- e2e: same metric through the C-ABI with HOST buffers (pinned), H2D/D2H inside
     e2e = None
     h_out = None
+    host_cpus = None
     if not args.no_e2e:
-        h_starts = starts.cpu().pin_memory()
-        try:   # W*L*4 bytes of pinned host memory per rank (34 GB on configs[4])
-            h_out = torch.empty((W, L), dtype=torch.int32, pin_memory=True)
-        except RuntimeError as ex:
-            e2e = {"unavailable": f"pinned host buffer of {W * L * 4 / 1e9:.1f} GB: {str(ex)[:120]}"}
+        # the pinned buffers are first-touched from the CPUs next to the GPU (its PCI
+        # device's local_cpulist), so their pages sit on the GPU's NUMA node: the D2H of a
+        # remote-node buffer crosses the socket link (measured: 136 ms instead of 61 ms per
+        # configs[1] call in some processes); the thread's affinity is restored after
+        host_cpus = None if os.environ.get("GRAPE_BENCH_NUMA") == "0" else _gpu_local_cpus(local)   # (A/B knob)
+        saved = os.sched_getaffinity(0) if host_cpus else None
+        if host_cpus:
+            os.sched_setaffinity(0, host_cpus)
+        try:
+            h_starts = starts.cpu().pin_memory()
+            try:   # W*L*4 bytes of pinned host memory per rank (34 GB on configs[4])
+                h_out = torch.empty((W, L), dtype=torch.int32, pin_memory=True)
+            except RuntimeError as ex:
+                e2e = {"unavailable": f"pinned host buffer of {W * L * 4 / 1e9:.1f} GB: {str(ex)[:120]}"}
+        finally:
+            if saved:
+                os.sched_setaffinity(0, saved)
         if _allreduce(1.0 if h_out is not None else 0.0, dist.ReduceOp.MIN, world) < 1.0:
             h_out = None   # every rank skips together (no half-entered collective)
             e2e = e2e or {"unavailable": "a rank could not pin its host buffer"}
@@ -485,6 +525,8 @@ def run_ours(args):
         e2e_tot = _allreduce(float(h_steps.item()), dist.ReduceOp.SUM, world)
         e2e = {"value": e2e_tot / e2e_s, "unit": "steps/s", "h2d_bytes_per_step": int(W * 4),
                "d2h_bytes_per_step": int(W * L * 4 + 8), "steps_timed": e2e_steps,
+               "host_buffers": ("pinned, first-touched on the GPU-local CPUs " + _cpu_ranges(host_cpus)
+                                if host_cpus else "pinned (GPU-local CPUs unknown)"),
                "path": ("grape_walks_approx" if dT else
                         ("grape_walks_node2vec_cdf" if args.sampler == "cdf" else
                          "grape_walks_node2vec_folded" if args.sampler == "folded" else
