@@ -481,9 +481,10 @@ def run_ours(args):
     host_cpus = None
     if not args.no_e2e:
         # the pinned buffers are first-touched from the CPUs next to the GPU (its PCI
-        # device's local_cpulist), so their pages sit on the GPU's NUMA node: the D2H of a
-        # remote-node buffer crosses the socket link (measured: 136 ms instead of 61 ms per
-        # configs[1] call in some processes); the thread's affinity is restored after
+        # device's local_cpulist), so on a multi-socket host their pages sit on the GPU's
+        # NUMA node and the copies do not cross the socket link; the thread's affinity is
+        # restored after.  (The pool's boxes have one NUMA node: a no-op there, measured
+        # equal; their occasional slow host-buffer calls are host-side pauses.)
         host_cpus = None if os.environ.get("GRAPE_BENCH_NUMA") == "0" else _gpu_local_cpus(local)   # (A/B knob)
         saved = os.sched_getaffinity(0) if host_cpus else None
         if host_cpus:
