@@ -406,6 +406,11 @@ def run_ours(args):
         W_total = min(W_total, args.max_walks)
     L = wk["L"]
     lo, hi = rank_slice(W_total, W_total, rank, world, args.scaling)
+    if args.slice:   # one rank's slice of an N-rank strong-scaling run, walked by this single process
+        r_, n_ = (int(t) for t in args.slice.split("/"))
+        if world > 1 or not 0 <= r_ < n_ or args.scaling != "strong":
+            raise SystemExit("--slice R/N: one process, 0 <= R < N, strong scaling")
+        lo, hi = rank_slice(W_total, W_total, r_, n_, "strong")
     base = lo
     W = hi - lo                                   # this rank's walks
     if args.scaling == "strong":
@@ -682,6 +687,8 @@ def run_ours(args):
             cfg["scale_down"] = args.scale_down
         if args.max_walks:
             cfg["max_walks"] = args.max_walks
+        if args.slice:
+            cfg["slice"] = f"{args.slice}: wids [{lo}, {hi}) only (one rank of an N-rank run, emulated on one GPU)"
         if args.dist_tables:
             cfg["tables"] = (f"distributed: rank r owns part r of the sampling tables ({world} parts, CUDA IPC), "
                              f"every rank walks over all parts")
@@ -905,6 +912,9 @@ def main():
     ap.add_argument("--scale-down", type=int, default=0, help="shrink the config's graph by 2^k (tests)")
     ap.add_argument("--max-walks", type=int, default=0,
                     help="walk only the first N walks of the config's list (ncu captures of the long configs)")
+    ap.add_argument("--slice", default="",
+                    help="R/N: walk rank R's slice of an N-rank strong-scaling run in this one process "
+                         "(the per-rank launch time and its tail, measured on one GPU)")
     ap.add_argument("--device", type=int, default=None,
                     help="CUDA device of every rank (default LOCAL_RANK); tests pin two ranks to cuda:0")
     ap.add_argument("--dist-backend", default=None, choices=["nccl", "gloo"],
