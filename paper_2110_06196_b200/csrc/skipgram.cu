@@ -96,14 +96,17 @@ struct SgParams {
     uint32_t* negs;
 };
 
-constexpr uint32_t kRowSmemWords = 12288;   // a row and its slots' validity bits up to 48 KB are staged
+constexpr uint32_t kRowSmemWords = 12288;
+#ifndef GRAPE_SG_MIN_BLOCKS
+#define GRAPE_SG_MIN_BLOCKS 8   // resident blocks of 256 per SM the pair kernel is compiled for
+#endif   // a row and its slots' validity bits up to 48 KB are staged
 
 // One block per walk row at a time (grid-stride over rows): the row is staged in
 // shared memory, then the block's threads cover the row's L*2w slots (each slot's
 // validity also kept as one bit in shared memory) and its L*2w*K negative words in
 // order, so every store of a warp is contiguous and no 64-bit division is needed
 // (32-bit index arithmetic within a row).
-__global__ void __launch_bounds__(256, 8) skipgram_kernel(const __grid_constant__ SgParams P)
+__global__ void __launch_bounds__(256, GRAPE_SG_MIN_BLOCKS) skipgram_kernel(const __grid_constant__ SgParams P)
 {
     extern __shared__ uint32_t srow[];
     const uint32_t L = P.L, tw = 2 * P.w, K = P.K;
@@ -232,7 +235,7 @@ cudaError_t launch_skipgram(const grape_graph* g, const uint32_t* walks, uint64_
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
     if (sms < 1) sms = 1;
     uint64_t blocks = num_walks;
-    const uint64_t cap = (uint64_t)sms * 8;   // 8 resident blocks of 256 per SM, grid-stride over rows
+    const uint64_t cap = (uint64_t)sms * GRAPE_SG_MIN_BLOCKS;   // one wave of resident blocks, grid-stride over rows
     if (blocks > cap) blocks = cap;
     const uint64_t words = (uint64_t)L + ((uint64_t)L * 2 * window + 31) / 32;   // row + validity bits
     const size_t smem = words <= kRowSmemWords ? (size_t)words * 4 : 0;
