@@ -299,6 +299,38 @@ def _dram_probe(launch, dev):
         return None
 
 
+def _issue_probe(launch, dev):
+    """Issue counters of the kernels `launch` runs (one more untimed launch; the probe's metric
+    set 1): warp instructions, thread instructions, cycles with an instruction issued and active
+    cycles, each summed over the SM sub-partitions.  None if unavailable."""
+    path = os.path.join(ROOT, "tools", "libgrape_dram_probe.so")
+    if not os.path.exists(path):
+        return None
+    try:
+        import ctypes
+        lib = ctypes.CDLL(path)
+        lib.grape_dram_probe_error.restype = ctypes.c_char_p
+        if not hasattr(lib, "grape_probe_begin_set"):
+            return None
+        torch.cuda.synchronize(dev)
+        if lib.grape_probe_begin_set(1) != 0:
+            print("issue probe:", lib.grape_dram_probe_error().decode(), file=sys.stderr)
+            return None
+        launch()
+        torch.cuda.synchronize(dev)
+        v = (ctypes.c_double * 4)()
+        if lib.grape_probe_end_set(v) != 0:
+            print("issue probe:", lib.grape_dram_probe_error().decode(), file=sys.stderr)
+            return None
+        if v[0] <= 0 or v[3] <= 0:
+            return None
+        return {"warp_instructions": v[0], "thread_instructions": v[1], "issue_active_cycles": v[2],
+                "active_cycles": v[3]}
+    except Exception as ex:   # measurement aid only: never fail the bench over it
+        print("issue probe:", ex, file=sys.stderr)
+        return None
+
+
 def _needs_flush(g, W, L):
     """Workloads whose CSR and output fit twice in L2 get an L2 flush between timed steps
     (decided from the CSR, so both arms state the same config)."""
@@ -555,6 +587,7 @@ def run_ours(args):
     # ---- roofline of the walk kernel: event counts from the counting
     # build of the same kernel (grape_walks_stats, untimed), times the measured time.
     roof = None
+    issue_raw = None
     if rank == 0 and args.sampler != "cdf":   # (no counting build of the CDF sampler)
         _, ev = grape.walks_stats(dg, starts, L, node2vec=node2vec, p=wk["p"], q=wk["q"], seed=wk["seed"],
                                   degree_threshold=dT, sampler=args.sampler if node2vec else "rejection",
@@ -583,6 +616,7 @@ def run_ours(args):
             traffic = _dram_probe(lambda: one(None), dev)
             if traffic is not None:
                 traffic_src = "measured in this run: CUPTI range profiler over one untimed launch (tools/dram_probe.cpp)"
+                issue_raw = _issue_probe(lambda: one(None), dev)   # the issue counters of one more
         tfile = os.path.join(ROOT, "profiles", f"traffic_cfg{k}.json")
         kname = "walk_tab_kernel" if info.get("tables") else "walk_sm_kernel"
         if traffic is None and os.path.exists(tfile):
@@ -665,6 +699,30 @@ def run_ours(args):
                         "L2-resident, so DRAM traffic (dram_gbs) is below this"}
         del deg
     clocks = clk.summary()
+    if rank == 0 and issue_raw and roof:
+        # the instruction-issue side of the same launch: the walker's other bound.
+        # Peak = one warp instruction per scheduler per cycle: SMs x 4 schedulers x the SM clock
+        # sampled under load.
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz")
+        t_l = roof["avg_launch_ms"] / 1e3
+        wi = issue_raw["warp_instructions"]
+        roof["issue"] = {
+            "warp_instructions_per_launch": wi,
+            "warp_instructions_per_step": wi / max(steps_per_launch, 1),
+            "active_threads_per_instruction": issue_raw["thread_instructions"] / wi,
+            "issue_active_frac": issue_raw["issue_active_cycles"] / issue_raw["active_cycles"],
+            "achieved_per_s": wi / t_l,
+            "peak_per_s": (sms * 4 * mhz * 1e6) if mhz else None,
+            "frac": (wi / t_l / (sms * 4 * mhz * 1e6)) if mhz else None,
+            "source": "measured in this run: CUPTI range profiler over one untimed launch (smsp__inst_executed, "
+                      "smsp__thread_inst_executed, smsp__issue_active, smsp__cycles_active; tools/dram_probe.cpp); "
+                      "peak = SMs x 4 schedulers x 1 warp instruction per cycle x the sampled SM clock"}
+        # the utilisations side by side: the highest names what the launch is closest to being bound by
+        fr = {"dram_traffic": roof.get("dram_frac"), "random_access": (roof.get("random_access") or {}).get("frac"),
+              "issue": roof["issue"]["frac"]}
+        fr = {k_: v_ for k_, v_ in fr.items() if v_ is not None}
+        roof["utilisation"] = dict(fr, highest=max(fr, key=fr.get))
     if rank == 0:
         metric = "random-walk steps/sec (node2vec 2nd-order)" if node2vec else "random-walk steps/sec (first-order)"
         if dT:

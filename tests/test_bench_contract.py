@@ -62,6 +62,11 @@ def test_product_line_n1():
     # so on stderr and falls back to the committed capture, which it names
     if r["traffic_source"].startswith("measured in this run"):
         assert r["traffic"] > 0
+        # ... and so are the issue counters of one more launch (the walker's other bound)
+        iss = r["issue"]
+        assert iss["warp_instructions_per_launch"] > 0 and 1 <= iss["active_threads_per_instruction"] <= 32
+        assert 0 < iss["frac"] <= 1 and 0 < iss["issue_active_frac"] <= 1
+        assert r["utilisation"]["highest"] in ("dram_traffic", "random_access", "issue")
     else:
         assert "dram probe: cupti" in p.stderr, p.stderr[-2000:]
         assert r["traffic_source"].startswith("profiles/traffic_cfg1.json") and r["traffic"] > 0

@@ -8,6 +8,8 @@
 //   ... launch the kernel(s) ...
 //   grape_dram_probe_end(&read, &write, &ns) -> 0 on success: dram__bytes_read.sum and
 //       dram__bytes_write.sum of one user range around the launches (single pass; ns: 0)
+//   grape_probe_begin_set(1) / grape_probe_end_set(double out[4]) -> the same for the issue
+//       counters (warp instructions, thread instructions, issue-active cycles, active cycles)
 //   grape_dram_probe_error() -> the last failure as text
 #include <cstdio>
 #include <cstdlib>
@@ -29,8 +31,15 @@ CUpti_Profiler_Host_Object* g_host = nullptr;
 std::vector<uint8_t> g_config, g_counter;
 CUcontext g_ctx = nullptr;
 bool g_inited = false;
-const char* kMetrics[] = {"dram__bytes_read.sum", "dram__bytes_write.sum"};
-constexpr size_t kNumMetrics = 2;
+// metric sets: 0 = the DRAM bytes; 1 = the issue counters (warp instructions, thread
+// instructions, cycles with an instruction issued, active cycles — summed over the SM
+// sub-partitions), for the issue-slot utilisation of an instruction-bound kernel
+const char* kSet0[] = {"dram__bytes_read.sum", "dram__bytes_write.sum"};
+const char* kSet1[] = {"smsp__inst_executed.sum", "smsp__thread_inst_executed.sum", "smsp__issue_active.sum",
+                       "smsp__cycles_active.sum"};
+const char** kMetrics = kSet0;
+size_t kNumMetrics = 2;
+constexpr size_t kMaxMetrics = 4;
 constexpr size_t kMaxRanges = 64;
 
 bool fail(const char* what, CUptiResult r)
@@ -88,8 +97,23 @@ int grape_dram_probe_init(void)
 
 static int begin_impl(void);
 
+int grape_probe_begin_set(int set)
+{
+    if (g_obj != nullptr) {
+        g_err = "a probe is already running";
+        return 1;
+    }
+    if (set == 1) { kMetrics = kSet1; kNumMetrics = 4; }
+    else { kMetrics = kSet0; kNumMetrics = 2; }
+    const int rc = begin_impl();
+    if (rc != 0) cleanup();
+    return rc;
+}
+
 int grape_dram_probe_begin(void)
 {
+    kMetrics = kSet0;
+    kNumMetrics = 2;
     const int rc = begin_impl();
     if (rc != 0) cleanup();
     return rc;
@@ -185,7 +209,22 @@ static int begin_impl(void)
     return 0;
 }
 
+static int end_impl(double* out);
+
 int grape_dram_probe_end(double* read_bytes, double* write_bytes, double* ns)
+{
+    double v[kMaxMetrics] = {0, 0, 0, 0};
+    const int rc = end_impl(v);
+    *read_bytes = v[0];
+    *write_bytes = v[1];
+    *ns = 0;   // (durations are CUDA-event measurements in bench.py)
+    return rc;
+}
+
+// The running set's metric values, in the set's order (out: 4 doubles).
+int grape_probe_end_set(double* out) { return end_impl(out); }
+
+static int end_impl(double* out)
 {
     if (g_obj == nullptr) {
         g_err = "grape_dram_probe_end without begin";
@@ -200,7 +239,7 @@ int grape_dram_probe_end(double* read_bytes, double* write_bytes, double* ns)
         sp.pRangeProfilerObject = g_obj;
         TRY(cuptiRangeProfilerStop(&sp), "cuptiRangeProfilerStop");
         if (!sp.isAllPassSubmitted) {
-            g_err = "the DRAM counters needed more than one pass";
+            g_err = "the counters needed more than one pass";
             return 1;
         }
         CUpti_RangeProfiler_DecodeData_Params dd{CUpti_RangeProfiler_DecodeData_Params_STRUCT_SIZE};
@@ -213,9 +252,9 @@ int grape_dram_probe_end(double* read_bytes, double* write_bytes, double* ns)
         gi.pCounterDataImage = g_counter.data();
         gi.counterDataImageSize = g_counter.size();
         TRY(cuptiRangeProfilerGetCounterDataInfo(&gi), "cuptiRangeProfilerGetCounterDataInfo");
-        double sum[kNumMetrics] = {0, 0};
+        double sum[kMaxMetrics] = {0, 0, 0, 0};
         for (size_t r = 0; r < gi.numTotalRanges; ++r) {
-            double v[kNumMetrics] = {0, 0};
+            double v[kMaxMetrics] = {0, 0, 0, 0};
             CUpti_Profiler_Host_EvaluateToGpuValues_Params ev{CUpti_Profiler_Host_EvaluateToGpuValues_Params_STRUCT_SIZE};
             ev.pHostObject = g_host;
             ev.pCounterDataImage = g_counter.data();
@@ -227,9 +266,7 @@ int grape_dram_probe_end(double* read_bytes, double* write_bytes, double* ns)
             TRY(cuptiProfilerHostEvaluateToGpuValues(&ev), "cuptiProfilerHostEvaluateToGpuValues");
             for (size_t q = 0; q < kNumMetrics; ++q) sum[q] += v[q];
         }
-        *read_bytes = sum[0];
-        *write_bytes = sum[1];
-        *ns = 0;   // (durations are CUDA-event measurements in bench.py)
+        for (size_t q = 0; q < kMaxMetrics; ++q) out[q] = sum[q];
         if (gi.numTotalRanges == 0) {
             g_err = "no kernel ranges were recorded";
             return 1;
