@@ -63,6 +63,21 @@ __device__ __forceinline__ void st_cs_v4(void* p, uint32_t a, uint32_t b, uint32
 // 32 lanes of a warp hit 32 banks), flushed as one aligned 32-B sector.  Entry
 // s of a row goes to slot (phase + s) & 7, phase = the row's 4-B offset within
 // its 32-B sector, so a flush at slot 7 always ends a real sector of `out`.
+#ifndef GRAPE_ROW_OUTLINE
+#define GRAPE_ROW_OUTLINE 0   // the partial-sector flush as a call (keeps its loop out of the walkers' hot code)
+#endif
+// entries [first, end) of a row from their staging slots, one by one (a row's partial
+// first or last sector)
+#if GRAPE_ROW_OUTLINE
+__device__ __noinline__
+#else
+__device__ __forceinline__
+#endif
+void flush_entries(uint32_t* row, const uint32_t* slot, uint32_t phase, uint32_t first, uint32_t end)
+{
+    for (uint32_t q = first; q < end; ++q) row[q] = slot[((phase + q) & 7) * kBlock];
+}
+
 struct RowWriter {
     uint32_t* slot;     // &smem[tid]; slot j at slot[j * kBlock]
     uint32_t* row;      // &out[i * L]
@@ -85,7 +100,7 @@ struct RowWriter {
                 st_cs_v4(p, slot[0], slot[kBlock], slot[2 * kBlock], slot[3 * kBlock]);
                 st_cs_v4(p + 4, slot[4 * kBlock], slot[5 * kBlock], slot[6 * kBlock], slot[7 * kBlock]);
             } else {
-                for (uint32_t q = first; q <= s; ++q) row[q] = slot[((phase + q) & 7) * kBlock];
+                flush_entries(row, slot, phase, first, s + 1);
             }
             first = s + 1;
         }
@@ -103,7 +118,7 @@ struct RowWriter {
     }
     __device__ __forceinline__ void finish(uint32_t end)   // flush [first, end)
     {
-        for (uint32_t q = first; q < end; ++q) row[q] = slot[((phase + q) & 7) * kBlock];
+        flush_entries(row, slot, phase, first, end);
     }
 };
 

@@ -57,6 +57,12 @@ constexpr int kSussUnroll = GRAPE_SUSS_UNROLL;
 #ifndef GRAPE_SUSS_MIN_BLOCKS
 #define GRAPE_SUSS_MIN_BLOCKS GRAPE_TAB_MIN_BLOCKS   // resident blocks per SM of the SUSS kernels
 #endif   // candidate pairs per unrolled step of the SUSS burst
+#ifndef GRAPE_TAB_EMIT_SPOT
+#define GRAPE_TAB_EMIT_SPOT 0    // 1: a register-decided return is emitted inside the draw round when another follows (measured slower: DESIGN.md §7)
+#endif
+#ifndef GRAPE_TAB_SEL_ADV
+#define GRAPE_TAB_SEL_ADV 1      // 1: emit / back update the walk's state through one set of selects (full records)
+#endif
 #ifndef GRAPE_TAB_SYNC_TOP
 #define GRAPE_TAB_SYNC_TOP 0     // explicit reconvergence points (measured: the emit one matters)
 #endif
@@ -521,6 +527,38 @@ __global__ void __launch_bounds__(kBlock, MODE == 1 ? GRAPE_SUSS_MIN_BLOCKS : GR
             w.put(s, x);
             ++steps;
             bool need_node = false;
+            if constexpr (GRAPE_TAB_SEL_ADV && !COMPACT) {
+                // one update for both ways to advance (x == t when back): t <- v; v <- the taken
+                // arc's head (emit: from its record) or the old t (back); T, S and the flags from
+                // the record, or swapped
+                uint32_t fnlo, fnhi, fnslo, fnshi, fxd, fxw, ffl;
+                off_t_ fxs;
+                if constexpr (WEIGHTED) {
+                    fnlo = sec[2]; fnhi = sec[3]; fnslo = sec[7]; fnshi = sec[1];
+                    fxs = sec[4]; fxd = sec[5] & kDegMask; fxw = sec[6];
+                    if constexpr (WIDE) fxs |= (off_t_)((sec[5] >> 26) & 3u) << 32;
+                    ffl = (sec[5] >> 28) & 3u;
+                } else {
+                    fxs = hxs;
+                    if constexpr (WIDE) fxs |= (off_t_)((hxd >> 26) & 3u) << 32;
+                    ffl = (hxd >> 28) & 3u;
+                    fxd = hxd & kDegMask;
+                    fxw = fxd;
+                    fnlo = hrev;
+                    fnhi = hrev == kNone ? hrev : hrev + 1;
+                    fnslo = ri;
+                    fnshi = ri + 1;
+                }
+                const uint32_t ovid = vid, ovdeg = vdeg, ovW = vW, otlo = tlo, othi = thi;
+                const off_t_ ovs = vstart;
+                const bool ont = nt;
+                vid = x;
+                vstart = emit ? fxs : tstart; vdeg = emit ? fxd : tdeg; vW = emit ? fxw : tW;
+                tid = ovid; tstart = ovs; tdeg = ovdeg; tW = ovW;
+                tlo = emit ? fnlo : slo; thi = emit ? fnhi : shi;
+                slo = emit ? fnslo : otlo; shi = emit ? fnshi : othi;
+                nt = emit ? (ffl >> 1) != 0 : ntr; ntr = emit ? (ffl & 1) != 0 : ont;
+            } else
             if (emit) {   // the record of the taken arc: T, S, flags and (full records) x's node record
                 uint32_t fnlo, fnhi, fnslo, fnshi, fxd = 0, fxw = 0, ffl;
                 off_t_ fxs = 0;
@@ -669,7 +707,7 @@ __global__ void __launch_bounds__(kBlock, MODE == 1 ? GRAPE_SUSS_MIN_BLOCKS : GR
                     st = ST_CAND;
                 }
             }
-            if (draw) draw_once(k + 1 < GRAPE_TAB_DRAWS, sub);
+            if (draw) draw_once(GRAPE_TAB_EMIT_SPOT && k + 1 < GRAPE_TAB_DRAWS, sub);
         }
         if (draw) st = ST_DRAW;   // still drawing: no load next iteration
     }
