@@ -63,6 +63,9 @@ constexpr int kSussUnroll = GRAPE_SUSS_UNROLL;
 #ifndef GRAPE_TAB_SEL_ADV
 #define GRAPE_TAB_SEL_ADV 1      // 1: emit / back update the walk's state through one set of selects (full records)
 #endif
+#ifndef GRAPE_TAB_ADDR_TABLE
+#define GRAPE_TAB_ADDR_TABLE 1   // 1: the load's table base and shift from a per-state parameter table
+#endif
 #ifndef GRAPE_TAB_SYNC_TOP
 #define GRAPE_TAB_SYNC_TOP 0     // explicit reconvergence points (measured: the emit one matters)
 #endif
@@ -162,7 +165,8 @@ __global__ void __launch_bounds__(kBlock, MODE == 1 ? GRAPE_SUSS_MIN_BLOCKS : GR
         uint32_t j;
         {   // the one load of this iteration: a single address computation for every state
             const bool rec = st == ST_REC || (SUSS && st == ST_CAND), gd = st == ST_GUIDE, nd = st == ST_NODE;
-            const uint32_t mul = rec ? 1u : gd ? P.G : 0u;
+            uint32_t mul = rec ? 1u : gd ? P.G : 0u;
+            if constexpr (GRAPE_TAB_ADDR_TABLE == 2 && !PARTS && !SUSS) mul = P.tbl_mul[st < ST_DRAW ? st : 0u];
             uint64_t e = (uint64_t)mul * vstart + (rec ? ri : st == ST_HASH ? hb : idx);
             const char* b = rec ? (const char*)P.rec : gd ? (const char*)P.guide
                           : nd ? (const char*)P.nodes : (const char*)P.ehash;
@@ -172,6 +176,11 @@ __global__ void __launch_bounds__(kBlock, MODE == 1 ? GRAPE_SUSS_MIN_BLOCKS : GR
                 b = (const char*)P.starts;
                 e = i;
                 sh = 2;
+            }
+            if constexpr (GRAPE_TAB_ADDR_TABLE && !PARTS && !SUSS) {   // base and shift of the state's table
+                const uint32_t k = st < ST_DRAW ? st : 0u;
+                b = P.tbl_base[k];
+                sh = P.tbl_shift[k];
             }
             const char* addr = b + (e << sh);
             if (PARTS && st != ST_START) {   // part (offset >> k) of table T, at offset mod 2^k
@@ -441,12 +450,13 @@ __global__ void __launch_bounds__(kBlock, MODE == 1 ? GRAPE_SUSS_MIN_BLOCKS : GR
                 else draw = true;
             }
         } else if (st0 == ST_HASH) {   // one bucket (8 slots) of t's set
-            bool found = false, empty = false;
+            // a bucket fills from slot 0 up (graph_tables.cu build_ehash: a slot is only tried
+            // after the ones before it were found taken, and nothing is ever removed), so it
+            // has an empty slot iff its last slot is empty
+            bool found = false;
+            const bool empty = sec[7] == kEmptySlot;
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                found |= sec[q] == x;
-                empty |= sec[q] == kEmptySlot;
-            }
+            for (int q = 0; q < 8; ++q) found |= sec[q] == x;
             if (found || empty) {
                 if (found ? u <= P.t1_m1 : u <= P.tq_m1) {
                     if constexpr (WEIGHTED) {

@@ -41,6 +41,9 @@ struct TabParams {
     unsigned long long* stats;
     uint32_t tp_m1, t1_m1, tq_m1;   // accept iff u <= T_c - 1
     const PartMap* pmap;            // MODE 3 (§8(f) f4 layout, partition.cu): the partition map
+    const char* tbl_base[6];        // per load state (ST_START .. ST_CAND): the table it reads
+    uint32_t tbl_shift[6];          //   and log2 of its entry size
+    uint32_t tbl_mul[6];            //   and how many entries it holds per arc of the row start (0: not per row)
 #if GRAPE_CHECKED
     uint64_t lim[4];                // checked build: bytes of records, guide, node records, edge hash
     uint64_t m;
@@ -125,6 +128,14 @@ inline TabParams tab_params(const grape_graph* g, const WalkArgs& a, const Thres
     P.out = a.out;
     P.steps_out = a.steps_out;
     P.stats = a.stats;
+    auto lg2 = [](uint32_t b) { uint32_t k = 0; while ((1u << k) < b) ++k; return k; };
+    P.tbl_base[0] = (const char*)P.starts;  P.tbl_shift[0] = 2;
+    P.tbl_base[1] = (const char*)P.nodes;   P.tbl_shift[1] = 4;
+    P.tbl_base[2] = (const char*)P.guide;   P.tbl_shift[2] = lg2(g->guide_bytes ? g->guide_bytes : 8);
+    P.tbl_base[3] = (const char*)P.rec;     P.tbl_shift[3] = lg2(g->rec_bytes ? g->rec_bytes : 32);
+    P.tbl_base[4] = (const char*)P.ehash;   P.tbl_shift[4] = 5;
+    P.tbl_base[5] = (const char*)P.rec;     P.tbl_shift[5] = P.tbl_shift[3];
+    P.tbl_mul[2] = P.G; P.tbl_mul[3] = 1; P.tbl_mul[5] = 1;   // (P{} zeroed the rest)
     P.tp_m1 = (uint32_t)(T.Tp - 1);
     P.t1_m1 = (uint32_t)(T.T1 - 1);
     P.tq_m1 = (uint32_t)(T.Tq - 1);
