@@ -231,8 +231,9 @@ __global__ void __launch_bounds__(kBlock, MODE == 1 ? GRAPE_SUSS_MIN_BLOCKS : GR
         bool have_rec = false;   // the sector in hand is x's record
         bool kept = false;
         // one attempt of a drawing lane: Philox, the band of u, the decisions that need no
-        // read (§8(c) c12); more: another draw follows in this iteration (a register-decided
-        // return is then emitted on the spot)
+        // read (§8(c) c12); more (GRAPE_TAB_EMIT_SPOT builds only): another draw follows in this
+        // iteration and a register-decided return is emitted on the spot; by default the lane
+        // goes to ST_BACK and the next iteration's emit block takes it
         auto draw_once = [&](const bool more, const bool sub) {
             if (STATS) ++cnt[C_ATTEMPT];
             Draw dr;
@@ -656,7 +657,7 @@ __global__ void __launch_bounds__(kBlock, MODE == 1 ? GRAPE_SUSS_MIN_BLOCKS : GR
         // ---- draws: Philox, the band of u, and the decisions that need no read
         // (§8(c) c12).  A lane whose attempt is decided from registers draws again
         // in the same iteration, up to GRAPE_TAB_DRAWS draws; a register-decided
-        // return x = t is emitted on the spot when another draw follows it.
+        // return x = t ends the lane's draws (ST_BACK: emitted by the next iteration).
 #pragma unroll kDrawUnroll
         for (int k = 0; k < GRAPE_TAB_DRAWS; ++k) {
             if (GRAPE_TAB_SYNC_DRAW) __syncwarp();
