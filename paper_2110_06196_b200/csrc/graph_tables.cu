@@ -237,6 +237,9 @@ __global__ void build_ehash(const uint64_t* __restrict__ off, const uint32_t* __
         uint64_t b = ((uint64_t)fmix32(x) * nb) >> 32;
         for (uint64_t tries = 0; tries < nb; ++tries) {   // nb * 8 slots >= deg + 1 > items: ends
             uint32_t* slot = reinterpret_cast<uint32_t*>(ehash.at(32 * (base + b)));   // a bucket is one sector
+            // slot q is tried only after slots 0 .. q-1 were found taken and nothing is removed, so
+            // a bucket's taken slots are always a prefix: the walker (walk_tab.cu, ST_HASH) reads
+            // "has an empty slot" from slot 7 alone and the checked build asserts the prefix
             int q = 0;
             while (q < 8 && atomicCAS(slot + q, kEmpty, x) != kEmpty) ++q;
             if (q < 8) break;

@@ -456,6 +456,16 @@ __global__ void __launch_bounds__(kBlock, MODE == 1 ? GRAPE_SUSS_MIN_BLOCKS : GR
             // has an empty slot iff its last slot is empty
             bool found = false;
             const bool empty = sec[7] == kEmptySlot;
+#if GRAPE_CHECKED
+            {   // the invariant itself: no empty slot before a taken one
+                bool gap = false, seen_empty = false;
+                for (int q = 0; q < 8; ++q) {
+                    gap |= seen_empty && sec[q] != kEmptySlot;
+                    seen_empty |= sec[q] == kEmptySlot;
+                }
+                GRAPE_DCHECK(!gap, "edge-hash bucket filled from slot 0 up");
+            }
+#endif
 #pragma unroll
             for (int q = 0; q < 8; ++q) found |= sec[q] == x;
             if (found || empty) {
